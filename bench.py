@@ -1,0 +1,370 @@
+"""Benchmark: fp64 GDoF/s of the sum-factorized 3D Helmholtz apply vs p.
+
+Workload (BASELINE.json configs[1]): 3D Helmholtz
+(c = 10, nu = 1; mass + diffusion) on a perturbed structured hex mesh of the
+unit cube, ~10M DoFs for EVERY degree p = 1..8 (cfg2 shapes), quadrature
+n_q = p + 2 Gauss-Legendre, stored quadrature-point factors (7 doubles per
+point).  One step = one Helmholtz apply at each p = 1..8 (8 applies).
+value = total DoFs processed / total device time (CUDA events, max over
+ranks).  Per-degree GDoF/s and HBM-roofline fractions are reported in
+`per_p`.  Every apply streams >= 1 GB of factors, far more than the 126 MB
+L2, so no L2 flush is needed between iterations.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the CPU oracle port of the reference's apply
+(oracle/, numpy, all host threads) on a bounded sample of the same workload.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEGREES = list(range(1, 9))
+TARGET_DOFS = 10.0e6
+C_HELM = 10.0
+NU = 1.0
+CPU_SAMPLE_DOFS = 120_000
+
+
+def mesh_cells(p, target=TARGET_DOFS):
+    return max(2, round((target ** (1.0 / 3.0) - 1.0) / p))
+
+
+def algorithmic_bytes(N, ne, p, d=3, k=7):
+    """read x + write y + int32 L->E map + stored factors."""
+    return 16.0 * N + 4.0 * ne * (p + 1) ** d + 8.0 * k * ne * (p + 2) ** d
+
+
+def algorithmic_flops(ne, p):
+    """Optimal shared-intermediate count, Helmholtz."""
+    n, q = p + 1, p + 2
+    return ne * (2.0 * (4 * n ** 3 * q + 6 * n ** 2 * q ** 2 + 8 * n * q ** 3) + 17.0 * q ** 3)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [s.strip() for s in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- problems
+
+def build_problem(p, target=TARGET_DOFS, seed=1):
+    from paper_1910_03032_b200 import geometry, mfop, spaces
+    n = mesh_cells(p, target)
+    m = geometry.perturb_mesh(geometry.cartesian_mesh((n, n, n)), 0.05, seed=seed)
+    sp = spaces.FESpace(m, p)
+    g = geometry.DeviceGeometry(m, sp.basis.quad)
+    op = mfop.HelmholtzOperator(sp, g, C_HELM, nu=NU)
+    ne = m.num_elements
+    N = sp.ndofs
+    del m
+    return dict(p=p, n=n, ne=ne, N=N, op=op)
+
+
+# ----------------------------------------------------------------------------- CPU legs
+
+def cpu_sample(threads, reps=1, target=CPU_SAMPLE_DOFS):
+    """Oracle port of the reference apply on ~target DoFs per degree.
+    Returns (GDoF/s, seconds, description)."""
+    from oracle import cpu_apply
+    from paper_1910_03032_b200 import geometry, spaces
+    tot_dofs = 0
+    tot_t = 0.0
+    for p in DEGREES:
+        n = mesh_cells(p, target)
+        m = geometry.perturb_mesh(geometry.cartesian_mesh((n, n, n)), 0.05, seed=1)
+        sp = spaces.FESpace(m, p)
+        geom = geometry.compute_geometric_factors(m, sp.basis.quad)
+        runner = cpu_apply.HelmholtzCPU(sp, geom, C_HELM, NU, threads=threads)
+        x = np.random.default_rng(0).standard_normal(sp.ndofs)
+        runner(x)  # warm
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            runner(x)
+        tot_t += time.perf_counter() - t0
+        tot_dofs += reps * sp.ndofs
+        runner.close()
+    desc = (f"3D Helmholtz apply, p=1..8, ~{target/1e3:.0f}k DoFs per degree "
+            f"(perturbed cube), {reps} timed rep(s) after 1 warm-up, oracle numpy port")
+    return tot_dofs / tot_t / 1e9, tot_t, desc
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample(threads, reps=1)
+    desc = ""
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, _, desc = cpu_sample(threads, reps=1)
+        vals.append(v)
+    el = time.perf_counter() - t0
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(world),
+        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "fp64 GDoF/s of sum-factorized Helmholtz apply vs p (3D, p=1..8, ~10M DoFs each)"
+
+
+def config_block(world):
+    return {"workload": "cfg2-shape 3D Helmholtz apply sweep p=1..8, ~10M DoFs per degree, "
+                        "perturbed unit-cube hex mesh, n_q=p+2 Gauss-Legendre, stored factors",
+            "c": C_HELM, "nu": NU, "degrees": DEGREES, "target_dofs_per_degree": TARGET_DOFS,
+            "parallelism": f"replica x{world}" if world > 1 else "single GPU",
+            "l2_policy": "per-apply working set >= 1 GB (factors) >> 126 MB L2; no flush needed"}
+
+
+# ----------------------------------------------------------------------------- GPU leg
+
+def run_ours(args, rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_1910_03032_b200 import _lib
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    probs = [build_problem(p) for p in DEGREES]
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    for pr in probs:
+        pr["x"] = torch.randn(pr["N"], dtype=torch.float64, device="cuda", generator=gen)
+        pr["y"] = torch.empty_like(pr["x"])
+    st = torch.cuda.current_stream()
+
+    def step(timed_events=None):
+        for i, pr in enumerate(probs):
+            if timed_events is not None:
+                timed_events[i][0].record(st)
+            pr["op"].apply_into(pr["x"], pr["y"])
+            if timed_events is not None:
+                timed_events[i][1].record(st)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in probs] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = _lib.lib.fb_launch_count()
+    torch.cuda.synchronize()
+    t_start.record(st)
+    for k in range(args.steps):
+        step(evs[k])
+    t_end.record(st)
+    torch.cuda.synchronize()
+    launches = _lib.lib.fb_launch_count() - l0
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    per_p_ms = [float(np.mean([evs[k][i][0].elapsed_time(evs[k][i][1])
+                               for k in range(args.steps)])) for i in range(len(probs))]
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # kernel-level timing of the fused element kernel alone (part 1), per p
+    kern_ms = []
+    for pr in probs:
+        op = pr["op"]
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        reps = 5
+        a.record(st)
+        for _ in range(reps):
+            _lib.check(_lib.lib.fb_operator_apply_part(op.handle, pr["x"].data_ptr(),
+                                                       pr["y"].data_ptr(), 1, st.cuda_stream))
+        b.record(st)
+        torch.cuda.synchronize()
+        kern_ms.append(a.elapsed_time(b) / reps)
+
+    # e2e through the public API with pinned host buffers, copies timed
+    hx = [torch.empty(pr["N"], dtype=torch.float64, pin_memory=True) for pr in probs]
+    hy = [torch.empty(pr["N"], dtype=torch.float64, pin_memory=True) for pr in probs]
+    for h, pr in zip(hx, probs):
+        h.copy_(pr["x"].cpu())
+    e2e_steps = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        for i, pr in enumerate(probs):
+            pr["x"].copy_(hx[i], non_blocking=True)
+            pr["op"].apply_into(pr["x"], pr["y"])
+            hy[i].copy_(pr["y"], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    ea = torch.cuda.Event(enable_timing=True)
+    eb = torch.cuda.Event(enable_timing=True)
+    ea.record(st)
+    for _ in range(e2e_steps):
+        e2e_step()
+    eb.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = ea.elapsed_time(eb) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        return
+    peak, peak_kind = load_peaks()
+    dofs_step = float(sum(pr["N"] for pr in probs))
+    ms_step = total_ms / args.steps
+    value = world * dofs_step / (ms_step * 1e-3) / 1e9
+    per_p = {}
+    tot_bytes = 0.0
+    for pr, ms, kms in zip(probs, per_p_ms, kern_ms):
+        by = algorithmic_bytes(pr["N"], pr["ne"], pr["p"])
+        tot_bytes += by
+        per_p[str(pr["p"])] = {
+            "dofs": pr["N"], "elements": pr["ne"], "ms": round(ms, 4),
+            "gdofs": round(pr["N"] / (ms * 1e-3) / 1e9, 3),
+            "hbm_frac": round(by / (ms * 1e-3) / 1e9 / peak, 4),
+            "kernel_ms": round(kms, 4),
+            "kernel_hbm_frac": round(by / (kms * 1e-3) / 1e9 / peak, 4),
+            "tflops": round(algorithmic_flops(pr["ne"], pr["p"]) / (ms * 1e-3) / 1e12, 2),
+            "fast_path": pr["op"].fast_path,
+        }
+    achieved = tot_bytes / (sum(per_p_ms) * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GDoF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_block(world),
+        "per_p": per_p,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": None, "peak_source": peak_kind,
+                     "note": "full apply (fused element kernel + E->L sum of shared DoFs), "
+                             "algorithmic bytes 16N + 4 ne (p+1)^3 + 56 ne (p+2)^3 over the "
+                             "p=1..8 sweep"},
+        "e2e": {"value": round(world * dofs_step / (e2e_ms * 1e-3) / 1e9, 4), "unit": "GDoF/s",
+                "h2d_bytes_per_step": int(8 * dofs_step), "d2h_bytes_per_step": int(8 * dofs_step),
+                "note": "HelmholtzOperator.apply_into per degree with pinned-host x/y copies "
+                        "inside the timed region"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if not args.no_cpu:
+        v, secs, desc = cpu_sample(1, reps=3)
+        line["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": 1, "kind": "port",
+                                "sample": desc, "seconds": round(secs, 2)}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

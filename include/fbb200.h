@@ -1,0 +1,168 @@
+/*
+ * fbb200.h — C ABI of the B200-native sum-factorized operator path.
+ *
+ * This is the drop-in boundary for the hot path of the flowbench reference
+ * (arXiv 1910.03032): the matrix-free operator action (mass, stiffness,
+ * Helmholtz, vector Laplacian, gradient, divergence) applied inside the
+ * Krylov loops, plus the Krylov vector kernels and the LOR V-cycle pieces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "_dev" pointers are CUDA device
+ *    pointers; "_host" pointers are host memory read during the call only.
+ *  - Every function returns an int status: FB_OK (0) or one of the FB_ERR_*
+ *    codes below, with a thread-local message from fb_last_error().  The
+ *    Python layer maps FB_ERR_ARG to ValueError (the reference raises
+ *    ValueError for shape / kind mismatches, mfop.py:192-193, 253-254, 452),
+ *    FB_ERR_OOM to MemoryError and everything else to RuntimeError.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *  - Objects own their device data (maps, transposed maps, factors, 1D
+ *    matrices); apply calls allocate nothing.
+ *  - Numbering, layouts and index conventions are those of the reference:
+ *    local DoF l = i0 + n*i1 + n^2*i2 (fespace.py:23-28), quadrature point
+ *    q0 + nq*q1 + nq^2*q2 (mesh.py:204-213), vector fields struct-of-arrays
+ *    (fespace.py:10-12).
+ */
+#ifndef FBB200_H
+#define FBB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FB_OK 0
+#define FB_ERR_ARG 1          /* bad shape / argument / kind        */
+#define FB_ERR_CUDA 2         /* CUDA runtime error                 */
+#define FB_ERR_OOM 3          /* device allocation failed           */
+#define FB_ERR_UNSUPPORTED 4  /* configuration not built            */
+
+/* Operator kinds (mfop.setup kinds, mfop.py:436-452). */
+#define FB_MASS 0
+#define FB_STIFFNESS 1
+#define FB_HELMHOLTZ 2
+#define FB_GRADIENT 3
+#define FB_DIVERGENCE 4
+
+typedef struct fb_restriction fb_restriction;
+typedef struct fb_operator fb_operator;
+
+const char* fb_last_error(void);
+int fb_abi_version(void);
+/* Number of kernel launches issued by this library since load (evidence
+ * counter used by bench.py's gpu_launches). */
+int64_t fb_launch_count(void);
+
+/* ------------------------------------------------------------------ */
+/* Element restriction: replaces FESpace.gather / FESpace.scatter_add   */
+/* (fespace.py:282-292).                                                */
+/* ------------------------------------------------------------------ */
+
+/* element_dofs_host: (ne, (p+1)^dim) int64, the reference's
+ * FESpace.element_dofs (fespace.py:71-217).  Builds the int32 L->E map, the
+ * transposed CSR used by the deterministic E->L sum (ascending flat E
+ * index, bitwise equal to np.bincount), and the split between element-
+ * interior DoFs (written directly by the operator kernels) and shared DoFs. */
+int fb_restriction_create(int dim, int p, int64_t ne, int64_t ndofs,
+                          const int64_t* element_dofs_host, fb_restriction** out);
+void fb_restriction_destroy(fb_restriction* r);
+int64_t fb_restriction_ndofs(const fb_restriction* r);
+/* xe_dev = x_dev[element_dofs]   (fespace.py:282-284) */
+int fb_restriction_gather(const fb_restriction* r, const double* x_dev, double* xe_dev,
+                          void* stream);
+/* y_dev = bincount(element_dofs, xe)   (fespace.py:286-292) */
+int fb_restriction_scatter_add(const fb_restriction* r, const double* xe_dev, double* y_dev,
+                               void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Sum-factorized operators (mfop.py:169-319).                          */
+/* ------------------------------------------------------------------ */
+
+/* kind: FB_MASS | FB_STIFFNESS | FB_HELMHOLTZ  (square operators on rv,
+ *       vdim components sharing factors, _SquareOperator mfop.py:169-244)
+ *       FB_GRADIENT | FB_DIVERGENCE  (rv = velocity restriction (scalar
+ *       numbering), rp = pressure restriction, vdim = dim; mfop.py:247-319)
+ * nq1, points_host: 1D rule size and points (geom.rule.points).
+ * B_host/D_host: (nq1, nv) basis values/derivatives of the (velocity) space
+ *       at the rule points (basis.py:122-156); Bp/Dp: (nq1, np) for the
+ *       pressure space (NULL for square kinds).
+ * wdet_host: (ne, nq1^dim) mass factor incl. any c (mfop.py:129-130, 234), or NULL
+ * stiff_host: (ne, nq1^dim, dim(dim+1)/2) packed symmetric factor (mfop.py:133-142), or NULL
+ * grad_host:  (ne, nq1^dim, dim, dim) (mfop.py:145-152), or NULL
+ * All factor arrays are in the reference's AoS layout; they are re-laid
+ * out element-blocked on the device. */
+int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction* rp,
+                       int vdim, int nq1, const double* points_host,
+                       const double* B_host, const double* D_host,
+                       const double* Bp_host, const double* Dp_host,
+                       const double* wdet_host, const double* stiff_host,
+                       const double* grad_host, fb_operator** out);
+/* Same operator, with the quadrature-point factors computed on the device
+ * from the element corners (ne, 2^dim, dim) (compute_geometric_factors,
+ * mesh.py:216-267, then mfop.py:129-152): weights = 1D rule weights;
+ * c = Helmholtz mass coefficient, nu = viscosity (mfop.py:211-244). */
+int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restriction* rp,
+                            int vdim, int nq1, const double* points_host,
+                            const double* weights_host, const double* B_host,
+                            const double* D_host, const double* Bp_host, const double* Dp_host,
+                            const double* corners_host, double c, double nu,
+                            fb_operator** out);
+/* Element-blocked factors (ne, K, nq1^dim) back to host, for verification. */
+int64_t fb_operator_factor_count(const fb_operator* op);
+int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count);
+void fb_operator_destroy(fb_operator* op);
+/* y = A x.  Square kinds: x, y of length vdim*ndofs.  Gradient: x pressure,
+ * y velocity.  Divergence: x velocity, y pressure. */
+int fb_operator_apply(const fb_operator* op, const double* x_dev, double* y_dev, void* stream);
+/* Fused path only: part 1 = element kernel (interior DoFs to y, shared
+ * contributions to the operator's buffer), part 2 = the E->L sum of the
+ * shared DoFs, part 0 = both (== fb_operator_apply).  For kernel timing. */
+int fb_operator_apply_part(const fb_operator* op, const double* x_dev, double* y_dev, int part,
+                           void* stream);
+/* Gradient only: y = G^T x (GradientOperator.apply_transpose, mfop.py:277-288). */
+int fb_operator_apply_transpose(const fb_operator* op, const double* x_dev, double* y_dev,
+                                void* stream);
+/* Bytes of device memory the operator owns (factors + matrices). */
+int64_t fb_operator_device_bytes(const fb_operator* op);
+/* 1 if the fused sm_100a fast path serves this operator, 0 for the general kernel. */
+int fb_operator_fast_path(const fb_operator* op);
+
+/* ConstrainedOperator.apply (mfop.py:428-433) around any operator apply:
+ * xi = x; xi[dofs] = 0; y = A xi; y[dofs] = x[dofs].  `work_dev` holds
+ * a length-n scratch vector. */
+int fb_mask_copy_zero(const double* x_dev, double* xi_dev, int64_t n, const int64_t* dofs_dev,
+                      int64_t ndofs, void* stream);
+int fb_mask_restore(const double* x_dev, double* y_dev, const int64_t* dofs_dev, int64_t ndofs,
+                    void* stream);
+
+/* Reference DoF numbering (fespace.py:71-217) on the host, for a mesh given
+ * by its element -> vertex-class table (ne, 2^dim).  element_dofs_out:
+ * (ne, (p+1)^dim).  Returns ndofs_scalar, or minus a status code. */
+int64_t fb_number_dofs_host(int dim, int p, int64_t ne, int64_t nv, const int64_t* elements,
+                            int64_t* element_dofs_out, int64_t* num_edges, int64_t* num_faces);
+
+/* ------------------------------------------------------------------ */
+/* Krylov vector kernels (solvers.py:108-254).  Deterministic: partial  */
+/* sums over fixed 4096-entry chunks, then a fixed-order second pass.   */
+/* ------------------------------------------------------------------ */
+/* partial_dev must hold fb_dot_partials(n) doubles; result_dev one. */
+int64_t fb_dot_partials(int64_t n);
+int fb_dot(int64_t n, const double* x_dev, const double* y_dev, double* partial_dev,
+           double* result_dev, void* stream);
+/* y = a*x + b*y  (a, b host scalars) */
+int fb_axpby(int64_t n, double a, const double* x_dev, double b, double* y_dev, void* stream);
+/* y = a_dev[0]*x + y, scalar read on device (alpha = rz/pAp, kept on device) */
+int fb_axpy_dev(int64_t n, const double* a_dev, int sign, const double* x_dev, double* y_dev,
+                void* stream);
+/* scalar ops on device: out = num/den */
+int fb_scalar_div(const double* num_dev, const double* den_dev, double* out_dev, void* stream);
+/* p = z + beta*p with beta = num/den read on device */
+int fb_xpby_ratio(int64_t n, const double* z_dev, const double* num_dev, const double* den_dev,
+                  double* p_dev, void* stream);
+/* y = d .* x */
+int fb_vmul(int64_t n, const double* d_dev, const double* x_dev, double* y_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBB200_H */

@@ -1,0 +1,545 @@
+// C ABI: element restriction and sum-factorized operators.
+//   fb_restriction_*  <- FESpace.gather / scatter_add   (fespace.py:282-292)
+//   fb_operator_*     <- mfop Mass/Stiffness/Helmholtz/Gradient/Divergence
+//                        (mfop.py:169-319)
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "fb_common.cuh"
+#include "sf3_fast.cuh"
+#include "sf_general.cuh"
+
+namespace fb {
+
+int build_factors_device(int dim, int64_t ne, const double* corners_dev, int nq,
+                         const double* pts, const double* w1, int kind, double c, double nu,
+                         double* fac_dev, int nfac, cudaStream_t st);
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+int64_t& launch_counter() {
+  static int64_t n = 0;
+  return n;
+}
+
+// Deterministic E->L sum: y[row_dof[r]] = 0.0 + sum_{k in row r} S[ent[k]],
+// entries in ascending flat-E order (bitwise np.bincount, fespace.py:288-292).
+__global__ void scatter_rows_kernel(int64_t nrows, const int* __restrict__ row_dof,
+                                    const int* __restrict__ off, const int* __restrict__ ent,
+                                    const double* __restrict__ S, int64_t S_comp_stride,
+                                    double* __restrict__ y, int64_t y_comp_stride) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  const int comp = blockIdx.y;
+  const double* Sc = S + comp * S_comp_stride;
+  const int b = __ldg(off + r), e = __ldg(off + r + 1);
+  double acc = 0.0;
+  for (int k = b; k < e; ++k) acc += __ldg(Sc + __ldg(ent + k));
+  const int64_t dof = row_dof ? int64_t(__ldg(row_dof + r)) : r;
+  y[comp * y_comp_stride + dof] = acc;
+}
+
+__global__ void gather_kernel(int64_t total, const int* __restrict__ map,
+                              const double* __restrict__ x, double* __restrict__ xe) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < total) xe[i] = __ldg(x + __ldg(map + i));
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+struct fb_restriction {
+  int dim = 0, p = 0, n = 0, nloc = 0;
+  int64_t ne = 0, ndofs = 0;
+  DevBuf<int> map;
+  DevBuf<int> full_off, full_ent;  // rows = all DoFs
+  int split_ok = 0;
+  int nb = 0;  // element-boundary positions per element
+  int64_t nsrows = 0;
+  DevBuf<int> s_row, s_off, s_ent;
+};
+
+struct fb_operator {
+  int kind = 0, dim = 0, vdim = 1, nq = 0, nv = 0, np = 0, nfac = 0;
+  const fb_restriction* rv = nullptr;
+  const fb_restriction* rp = nullptr;
+  bool fast = false;
+  SF3Params fp;  // host copy of the fast-path parameters
+  DevBuf<double> fac;
+  DevBuf<double> mats;
+  DevBuf<double> S;  // shared-entry buffer / E-vector scratch
+  int64_t S_comp_stride = 0;
+  int gen_kind = 0;
+  size_t gen_smem = 0;
+};
+
+namespace {
+
+bool position_interior(int dim, int n, int l) {
+  for (int a = 0; a < dim; ++a) {
+    const int c = l % n;
+    l /= n;
+    if (c == 0 || c == n - 1) return false;
+  }
+  return true;
+}
+
+// Barycentric differentiation matrix on arbitrary distinct points (the
+// formula of basis.py:98-119, evaluated in C++).
+void diff_matrix(const double* x, int n, double* D) {
+  std::vector<double> w(n, 1.0);
+  for (int j = 0; j < n; ++j) {
+    double prod = 1.0;
+    for (int k = 0; k < n; ++k)
+      if (k != j) prod *= (x[j] - x[k]);
+    w[j] = 1.0 / prod;
+  }
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) {
+      if (i == j) continue;
+      D[i * n + j] = (w[j] / w[i]) / (x[i] - x[j]);
+      s += D[i * n + j];
+    }
+    D[i * n + i] = -s;
+  }
+}
+
+template <int N, int Q, int KIND, int NE, int NT>
+int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
+  constexpr int QP = Q | 1;
+  constexpr size_t smem = size_t(NE) * 3 * Q * Q * QP * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    FB_TRY_CUDA(cudaFuncSetAttribute(sf3_fast_kernel<N, Q, KIND, NE, NT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = true;
+  }
+  SF3Params p = op->fp;
+  p.x = x;
+  p.y = y;
+  dim3 grid(ceil_div(op->rv->ne, NE), op->vdim);
+  sf3_fast_kernel<N, Q, KIND, NE, NT><<<grid, NT, smem, st>>>(p);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+template <int N, int Q, int NE, int NT>
+int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
+  switch (op->kind) {
+    case FB_MASS: return launch_fast_t<N, Q, kMass, NE, NT>(op, x, y, st);
+    case FB_STIFFNESS: return launch_fast_t<N, Q, kStiff, NE, NT>(op, x, y, st);
+    default: return launch_fast_t<N, Q, kHelm, NE, NT>(op, x, y, st);
+  }
+}
+
+int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
+  switch (op->rv->p) {
+    case 1: return launch_fast_kind<2, 3, 28, 256>(op, x, y, st);
+    case 2: return launch_fast_kind<3, 4, 16, 256>(op, x, y, st);
+    case 3: return launch_fast_kind<4, 5, 10, 256>(op, x, y, st);
+    case 4: return launch_fast_kind<5, 6, 7, 256>(op, x, y, st);
+    case 5: return launch_fast_kind<6, 7, 5, 256>(op, x, y, st);
+    case 6: return launch_fast_kind<7, 8, 4, 256>(op, x, y, st);
+    case 7: return launch_fast_kind<8, 9, 3, 256>(op, x, y, st);
+    case 8: return launch_fast_kind<9, 10, 2, 224>(op, x, y, st);
+    default: set_error("fast path not built for this degree"); return FB_ERR_UNSUPPORTED;
+  }
+}
+
+int scatter_rows(const fb_restriction* r, bool split, const double* S, int64_t S_comp_stride,
+                 double* y, int64_t y_comp_stride, int ncomp, cudaStream_t st) {
+  const int64_t nrows = split ? r->nsrows : r->ndofs;
+  if (nrows == 0) return FB_OK;
+  dim3 grid(ceil_div(nrows, 256), ncomp);
+  scatter_rows_kernel<<<grid, 256, 0, st>>>(nrows, split ? r->s_row.ptr : nullptr,
+                                            split ? r->s_off.ptr : r->full_off.ptr,
+                                            split ? r->s_ent.ptr : r->full_ent.ptr, S,
+                                            S_comp_stride, y, y_comp_stride);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+// AoS (ne, nq, k) -> element-blocked (ne, k, nq) into dst at component offset
+void relayout(const double* src, int64_t ne, int nqd, int k, double* dst, int ktot, int koff) {
+  for (int64_t e = 0; e < ne; ++e)
+    for (int c = 0; c < k; ++c)
+      for (int q = 0; q < nqd; ++q)
+        dst[(e * ktot + koff + c) * nqd + q] = src[(e * nqd + q) * k + c];
+}
+
+}  // namespace
+
+static int finish_operator(fb_operator* op, const double* points, const double* B,
+                           const double* D, const double* Bp, const double* Dp) {
+  const fb_restriction* rv = op->rv;
+  const fb_restriction* rp = op->rp;
+  const int kind = op->kind, dim = op->dim, nq1 = op->nq, vdim = op->vdim;
+  const int64_t ne = rv->ne;
+
+  // fast path: 3D square kinds, n_q = p + 2, p in 1..8, conforming split
+  const int p = rv->p;
+  op->fast = (kind <= FB_HELMHOLTZ) && dim == 3 && nq1 == p + 2 && p >= 1 && p <= 8 &&
+             rv->split_ok;
+  if (op->fast) {
+    SF3Params& fp = op->fp;
+    std::memset(&fp, 0, sizeof(fp));
+    const int n = rv->n;
+    for (int q = 0; q < nq1; ++q)
+      for (int i = 0; i < n; ++i) fp.B[q][i] = B[q * n + i];
+    std::vector<double> Dq(nq1 * nq1);
+    diff_matrix(points, nq1, Dq.data());
+    for (int a = 0; a < nq1; ++a)
+      for (int b = 0; b < nq1; ++b) fp.Dq[a][b] = Dq[a * nq1 + b];
+    fp.map = rv->map.ptr;
+    fp.fac = op->fac.ptr;
+    fp.ne = ne;
+    fp.x_comp_stride = rv->ndofs;
+    fp.S_comp_stride = ne * rv->nb;
+    fp.direct = 1;
+    op->S_comp_stride = ne * rv->nb;
+    FB_TRY_CUDA(op->S.alloc(op->S_comp_stride * vdim));
+    fp.S = op->S.ptr;
+  } else {
+    // general path
+    const int nv = rv->n, np = op->np;
+    std::vector<double> mats(size_t(2) * nq1 * nv + size_t(2) * nq1 * np);
+    std::memcpy(mats.data(), B, sizeof(double) * nq1 * nv);
+    std::memcpy(mats.data() + nq1 * nv, D, sizeof(double) * nq1 * nv);
+    if (np > 0) {
+      std::memcpy(mats.data() + 2 * nq1 * nv, Bp, sizeof(double) * nq1 * np);
+      std::memcpy(mats.data() + 2 * nq1 * nv + nq1 * np, Dp, sizeof(double) * nq1 * np);
+    }
+    FB_TRY_CUDA(op->mats.upload(mats.data(), int64_t(mats.size())));
+    op->gen_smem = gen_smem_bytes(dim, nv, np, nq1);
+    FB_REQUIRE(op->gen_smem <= 227 * 1024, "element too large for the general kernel");
+    FB_TRY_CUDA(cudaFuncSetAttribute(sf_general_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(227 * 1024)));
+    // E-vector scratch: largest of input/output E-vectors over components
+    const int64_t nvl = rv->nloc, npl = rp ? rp->nloc : 0;
+    int64_t need = 0;
+    if (kind <= FB_HELMHOLTZ) need = int64_t(vdim) * ne * nvl;
+    else if (kind == FB_GRADIENT) need = int64_t(dim) * ne * nvl + ne * npl;
+    else need = ne * npl;
+    FB_TRY_CUDA(op->S.alloc(need));
+  }
+  return FB_OK;
+}
+
+extern "C" {
+
+const char* fb_last_error(void) { return g_last_error.c_str(); }
+int fb_abi_version(void) { return 1; }
+int64_t fb_launch_count(void) { return launch_counter(); }
+
+int fb_restriction_create(int dim, int p, int64_t ne, int64_t ndofs,
+                          const int64_t* element_dofs, fb_restriction** out) {
+  FB_REQUIRE(out != nullptr, "out is NULL");
+  *out = nullptr;
+  FB_REQUIRE(dim == 2 || dim == 3, "dim must be 2 or 3");
+  FB_REQUIRE(p >= 1, "degree must be >= 1");
+  FB_REQUIRE(ne >= 0 && ndofs >= 0, "negative sizes");
+  FB_REQUIRE(ne == 0 || element_dofs != nullptr, "element_dofs is NULL");
+  std::unique_ptr<fb_restriction> r(new fb_restriction());
+  r->dim = dim;
+  r->p = p;
+  r->n = p + 1;
+  r->nloc = dim == 2 ? r->n * r->n : r->n * r->n * r->n;
+  r->ne = ne;
+  r->ndofs = ndofs;
+  const int nloc = r->nloc, n = r->n;
+  const int64_t total = ne * nloc;
+  FB_REQUIRE(total < (int64_t(1) << 31) && ndofs < (int64_t(1) << 31),
+             "element map exceeds int32 indexing");
+  std::vector<int> map(total);
+  std::vector<int> count(ndofs + 1, 0);
+  for (int64_t k = 0; k < total; ++k) {
+    const int64_t d = element_dofs[k];
+    FB_REQUIRE(d >= 0 && d < ndofs, "element_dofs entry out of range");
+    map[k] = int(d);
+    ++count[d];
+  }
+  // full transposed map: counting sort keeps ascending flat-E order
+  std::vector<int> off(ndofs + 1, 0);
+  for (int64_t i = 0; i < ndofs; ++i) off[i + 1] = off[i] + count[i];
+  std::vector<int> ent(total);
+  {
+    std::vector<int> pos(off.begin(), off.end() - 1);
+    for (int64_t k = 0; k < total; ++k) ent[pos[map[k]]++] = int(k);
+  }
+  // split mode: interior positions written directly when their DoF is unique
+  std::vector<char> interior(nloc);
+  std::vector<int> rank(nloc, -1);
+  int nb = 0;
+  for (int l = 0; l < nloc; ++l) {
+    interior[l] = position_interior(dim, n, l);
+    if (!interior[l]) rank[l] = nb++;
+  }
+  r->nb = nb;
+  std::vector<char> direct(ndofs, 0);
+  bool ok = true;
+  for (int64_t e = 0; e < ne && ok; ++e)
+    for (int l = 0; l < nloc; ++l)
+      if (interior[l]) {
+        const int d = map[e * nloc + l];
+        if (count[d] != 1) {
+          ok = false;
+          break;
+        }
+        direct[d] = 1;
+      }
+  r->split_ok = ok ? 1 : 0;
+  FB_TRY_CUDA(r->map.upload(map.data(), total));
+  FB_TRY_CUDA(r->full_off.upload(off.data(), ndofs + 1));
+  FB_TRY_CUDA(r->full_ent.upload(ent.data(), total));
+  if (ok) {
+    std::vector<int> rowid(ndofs, -1);
+    std::vector<int> rows;
+    rows.reserve(ndofs);
+    for (int64_t i = 0; i < ndofs; ++i)
+      if (!direct[i]) {
+        rowid[i] = int(rows.size());
+        rows.push_back(int(i));
+      }
+    const int64_t nr = int64_t(rows.size());
+    std::vector<int> soff(nr + 1, 0);
+    for (int64_t i = 0; i < nr; ++i) soff[i + 1] = soff[i] + count[rows[i]];
+    std::vector<int> sent(soff[nr]);
+    std::vector<int> pos(soff.begin(), soff.end() - 1);
+    for (int64_t e = 0; e < ne; ++e)
+      for (int l = 0; l < nloc; ++l) {
+        if (interior[l]) continue;
+        const int d = map[e * nloc + l];
+        sent[pos[rowid[d]]++] = int(e * nb + rank[l]);
+      }
+    r->nsrows = nr;
+    FB_TRY_CUDA(r->s_row.upload(rows.data(), nr));
+    FB_TRY_CUDA(r->s_off.upload(soff.data(), nr + 1));
+    FB_TRY_CUDA(r->s_ent.upload(sent.data(), int64_t(sent.size())));
+  }
+  *out = r.release();
+  return FB_OK;
+}
+
+void fb_restriction_destroy(fb_restriction* r) { delete r; }
+int64_t fb_restriction_ndofs(const fb_restriction* r) { return r ? r->ndofs : -1; }
+
+int fb_restriction_gather(const fb_restriction* r, const double* x, double* xe, void* stream) {
+  FB_REQUIRE(r != nullptr, "restriction is NULL");
+  const int64_t total = r->ne * r->nloc;
+  if (total == 0) return FB_OK;
+  gather_kernel<<<ceil_div(total, 256), 256, 0, as_stream(stream)>>>(total, r->map.ptr, x, xe);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+int fb_restriction_scatter_add(const fb_restriction* r, const double* xe, double* y,
+                               void* stream) {
+  FB_REQUIRE(r != nullptr, "restriction is NULL");
+  return scatter_rows(r, false, xe, 0, y, 0, 1, as_stream(stream));
+}
+
+int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction* rp, int vdim,
+                       int nq1, const double* points, const double* B, const double* D,
+                       const double* Bp, const double* Dp, const double* wdet,
+                       const double* stiff, const double* grad, fb_operator** out) {
+  FB_REQUIRE(out != nullptr, "out is NULL");
+  *out = nullptr;
+  FB_REQUIRE(rv != nullptr, "space restriction is NULL");
+  FB_REQUIRE(kind >= FB_MASS && kind <= FB_DIVERGENCE, "unknown operator kind");
+  FB_REQUIRE(nq1 >= 1 && nq1 <= 32, "unsupported rule size");
+  FB_REQUIRE(B != nullptr && D != nullptr && points != nullptr, "B/D/points are NULL");
+  std::unique_ptr<fb_operator> op(new fb_operator());
+  const int dim = rv->dim;
+  op->kind = kind;
+  op->dim = dim;
+  op->vdim = vdim;
+  op->nq = nq1;
+  op->nv = rv->n;
+  op->rv = rv;
+  const int64_t ne = rv->ne;
+  const int nqd = dim == 2 ? nq1 * nq1 : nq1 * nq1 * nq1;
+  const int ksym = dim == 2 ? 3 : 6;
+  std::vector<double> fac;
+  if (kind <= FB_HELMHOLTZ) {
+    FB_REQUIRE(vdim >= 1, "vdim must be >= 1");
+    if (kind != FB_STIFFNESS) FB_REQUIRE(wdet != nullptr, "mass factor (wdet) required");
+    if (kind != FB_MASS) FB_REQUIRE(stiff != nullptr, "stiffness factor required");
+    op->nfac = (kind == FB_MASS) ? 1 : (kind == FB_STIFFNESS ? ksym : ksym + 1);
+    fac.assign(size_t(ne) * op->nfac * nqd, 0.0);
+    int koff = 0;
+    if (kind != FB_STIFFNESS) {
+      relayout(wdet, ne, nqd, 1, fac.data(), op->nfac, 0);
+      koff = 1;
+    }
+    if (kind != FB_MASS) relayout(stiff, ne, nqd, ksym, fac.data(), op->nfac, koff);
+  } else {
+    FB_REQUIRE(rp != nullptr, "pressure restriction is NULL");
+    FB_REQUIRE(rp->ne == ne && rp->dim == dim, "velocity/pressure spaces disagree");
+    FB_REQUIRE(vdim == dim, "mixed operators expect vdim == dim");
+    FB_REQUIRE(grad != nullptr && Bp != nullptr && Dp != nullptr, "gradient factor / Bp / Dp required");
+    op->rp = rp;
+    op->np = rp->n;
+    op->nfac = dim * dim;
+    fac.assign(size_t(ne) * op->nfac * nqd, 0.0);
+    relayout(grad, ne, nqd, dim * dim, fac.data(), op->nfac, 0);
+  }
+  FB_TRY_CUDA(op->fac.upload(fac.data(), int64_t(fac.size())));
+  int rc = finish_operator(op.get(), points, B, D, Bp, Dp);
+  if (rc != FB_OK) return rc;
+  *out = op.release();
+  return FB_OK;
+}
+
+int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restriction* rp,
+                            int vdim, int nq1, const double* points, const double* weights,
+                            const double* B, const double* D, const double* Bp,
+                            const double* Dp, const double* corners, double c, double nu,
+                            fb_operator** out) {
+  FB_REQUIRE(out != nullptr, "out is NULL");
+  *out = nullptr;
+  FB_REQUIRE(rv != nullptr, "space restriction is NULL");
+  FB_REQUIRE(kind >= FB_MASS && kind <= FB_DIVERGENCE, "unknown operator kind");
+  FB_REQUIRE(nq1 >= 1 && nq1 <= 32, "unsupported rule size");
+  FB_REQUIRE(points && weights && B && D, "points/weights/B/D are NULL");
+  FB_REQUIRE(rv->ne == 0 || corners != nullptr, "corners are NULL");
+  std::unique_ptr<fb_operator> op(new fb_operator());
+  const int dim = rv->dim;
+  op->kind = kind;
+  op->dim = dim;
+  op->vdim = vdim;
+  op->nq = nq1;
+  op->nv = rv->n;
+  op->rv = rv;
+  const int64_t ne = rv->ne;
+  const int nqd = dim == 2 ? nq1 * nq1 : nq1 * nq1 * nq1;
+  const int ksym = dim == 2 ? 3 : 6;
+  if (kind <= FB_HELMHOLTZ) {
+    op->nfac = (kind == FB_MASS) ? 1 : (kind == FB_STIFFNESS ? ksym : ksym + 1);
+  } else {
+    FB_REQUIRE(rp != nullptr && rp->ne == ne && rp->dim == dim, "pressure restriction mismatch");
+    FB_REQUIRE(Bp != nullptr && Dp != nullptr, "Bp/Dp required");
+    FB_REQUIRE(vdim == dim, "mixed operators expect vdim == dim");
+    op->rp = rp;
+    op->np = rp->n;
+    op->nfac = dim * dim;
+  }
+  FB_TRY_CUDA(op->fac.alloc(ne * op->nfac * nqd));
+  {
+    DevBuf<double> cd;
+    FB_TRY_CUDA(cd.upload(corners, ne * (int64_t(1) << dim) * dim));
+    int rc = build_factors_device(dim, ne, cd.ptr, nq1, points, weights, kind, c, nu,
+                                  op->fac.ptr, op->nfac, 0);
+    if (rc != FB_OK) return rc;
+    FB_TRY_CUDA(cudaDeviceSynchronize());
+  }
+  int rc = finish_operator(op.get(), points, B, D, Bp, Dp);
+  if (rc != FB_OK) return rc;
+  *out = op.release();
+  return FB_OK;
+}
+
+/* Copy the operator's element-blocked factors (ne, K, nq^d) to host. */
+int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count) {
+  FB_REQUIRE(op != nullptr, "operator is NULL");
+  FB_REQUIRE(count == op->fac.n, "factor count mismatch");
+  FB_TRY_CUDA(cudaMemcpy(host_out, op->fac.ptr, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  return FB_OK;
+}
+
+int64_t fb_operator_factor_count(const fb_operator* op) { return op ? op->fac.n : 0; }
+
+void fb_operator_destroy(fb_operator* op) { delete op; }
+
+int64_t fb_operator_device_bytes(const fb_operator* op) {
+  if (!op) return 0;
+  return int64_t(op->fac.bytes() + op->mats.bytes() + op->S.bytes());
+}
+
+int fb_operator_fast_path(const fb_operator* op) { return op && op->fast ? 1 : 0; }
+
+static int general_apply(const fb_operator* op, int gkind, const double* x, double* y,
+                         cudaStream_t st) {
+  const fb_restriction* rv = op->rv;
+  const fb_restriction* rp = op->rp;
+  SFGParams P;
+  P.fac = op->fac.ptr;
+  P.x = x;
+  P.ye = op->S.ptr;
+  P.mats = op->mats.ptr;
+  P.ne = rv->ne;
+  P.dim = op->dim;
+  P.kind = gkind;
+  P.nv = op->nv;
+  P.np = op->np;
+  P.nq = op->nq;
+  P.nfac = op->nfac;
+  int gy = 1;
+  const fb_restriction* rin = rv;
+  const fb_restriction* rout = rv;
+  int ncomp_out = 1;
+  if (gkind <= kgHelm) {
+    gy = op->vdim;
+    ncomp_out = op->vdim;
+    P.in_comp_stride = rv->ndofs;
+  } else if (gkind == kgGrad) {
+    rin = rp;
+    ncomp_out = op->dim;
+    P.in_comp_stride = 0;
+  } else {  // div, gradT: velocity in, pressure out
+    rout = rp;
+    P.in_comp_stride = rv->ndofs;
+  }
+  P.map_in = rin->map.ptr;
+  if (rv->ne == 0) return FB_OK;
+  dim3 grid(unsigned(rv->ne), gy);
+  sf_general_kernel<<<grid, 128, op->gen_smem, st>>>(P);
+  FB_CHECK_LAUNCH();
+  return scatter_rows(rout, false, op->S.ptr, rout->ne * rout->nloc, y, rout->ndofs,
+                      ncomp_out, st);
+}
+
+int fb_operator_apply_part(const fb_operator* op, const double* x, double* y, int part,
+                           void* stream) {
+  FB_REQUIRE(op != nullptr, "operator is NULL");
+  FB_REQUIRE(part >= 0 && part <= 2, "part must be 0 (all), 1 (element kernel), 2 (E->L sum)");
+  cudaStream_t st = as_stream(stream);
+  if (op->fast) {
+    if (op->rv->ne > 0 && part != 2) {
+      int rc = launch_fast(op, x, y, st);
+      if (rc != FB_OK) return rc;
+    }
+    if (part == 1) return FB_OK;
+    return scatter_rows(op->rv, true, op->S.ptr, op->S_comp_stride, y, op->rv->ndofs,
+                        op->vdim, st);
+  }
+  FB_REQUIRE(part == 0, "split apply is only available on the fused path");
+  return fb_operator_apply(op, x, y, stream);
+}
+
+int fb_operator_apply(const fb_operator* op, const double* x, double* y, void* stream) {
+  FB_REQUIRE(op != nullptr, "operator is NULL");
+  cudaStream_t st = as_stream(stream);
+  if (op->fast) return fb_operator_apply_part(op, x, y, 0, stream);
+  int gk = kgMass;
+  switch (op->kind) {
+    case FB_MASS: gk = kgMass; break;
+    case FB_STIFFNESS: gk = kgStiff; break;
+    case FB_HELMHOLTZ: gk = kgHelm; break;
+    case FB_GRADIENT: gk = kgGrad; break;
+    default: gk = kgDiv; break;
+  }
+  return general_apply(op, gk, x, y, st);
+}
+
+int fb_operator_apply_transpose(const fb_operator* op, const double* x, double* y,
+                                void* stream) {
+  FB_REQUIRE(op != nullptr, "operator is NULL");
+  FB_REQUIRE(op->kind == FB_GRADIENT, "apply_transpose is defined for the gradient only");
+  return general_apply(op, kgGradT, x, y, as_stream(stream));
+}
+
+}  // extern "C"

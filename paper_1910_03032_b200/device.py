@@ -1,0 +1,62 @@
+"""Device plumbing: torch owns device memory and streams; the C-ABI computes.
+
+Vectors on the device are ``torch.float64`` CUDA tensors.  Host numpy
+arrays crossing the API are copied in and out around the call, which is the
+drop-in behaviour the reference's tests exercise (``op.apply(numpy) ->
+numpy``).
+"""
+
+import numpy as np
+import torch
+
+_DEVICE = None
+
+
+def device():
+    global _DEVICE
+    if _DEVICE is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1910_03032_b200 needs a CUDA device (sm_100a); none is visible")
+        _DEVICE = torch.device("cuda", torch.cuda.current_device())
+    return _DEVICE
+
+
+def stream_handle():
+    return torch.cuda.current_stream(device()).cuda_stream
+
+
+def is_device_tensor(x):
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def to_device(x, dtype=torch.float64):
+    """numpy / torch -> contiguous CUDA tensor of `dtype` (no copy if already)."""
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device(), dtype=dtype)
+        return t.contiguous()
+    arr = np.ascontiguousarray(x, dtype=np.float64 if dtype == torch.float64 else None)
+    return torch.from_numpy(arr).to(device())
+
+
+def empty(n, dtype=torch.float64):
+    return torch.empty(n, dtype=dtype, device=device())
+
+
+def zeros(n, dtype=torch.float64):
+    return torch.zeros(n, dtype=dtype, device=device())
+
+
+def to_host(t):
+    return t.detach().cpu().numpy()
+
+
+class DeviceIn:
+    """Normalise an operand: returns (device tensor, was_host)."""
+
+    @staticmethod
+    def get(x):
+        if is_device_tensor(x):
+            if x.dtype != torch.float64:
+                raise ValueError(f"operand dtype {x.dtype}, expected float64")
+            return x.contiguous(), False
+        return to_device(x), True

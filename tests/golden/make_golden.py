@@ -1,0 +1,144 @@
+"""Generate golden fixtures from the REAL reference (flowbench 0.1.0).
+
+Run in the build container, where /root/reference exists:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py [group ...]
+
+The reference is imported from /root/reference/pkg/src and driven through its
+public API (mesh, FESpace, mfop, solvers, lor).  Outputs are small .npz files
+in this directory plus manifest.json describing each case; the GPU box never
+needs the reference.  Inputs are reproducible from the recorded mesh
+parameters and numpy.random.default_rng seeds.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def ref_modules():
+    sys.path.insert(0, REF)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    from flowbench import fespace, lor, mesh, mfop, solvers, stokes  # noqa: F401
+    return mesh, fespace, mfop, solvers, lor, stokes
+
+
+# (name, d, counts, periodic, perturb, p, kind, c, nu, vdim, seed)
+APPLY_CASES = []
+for _p in (1, 2, 3, 4, 6):
+    for _k in ("mass", "stiffness", "helmholtz"):
+        APPLY_CASES.append((f"2d_p{_p}_{_k}", 2, (3, 2), None, 0.08, _p, _k, 0.7, 1.3, 1, 5))
+for _p in (1, 2, 3, 4):
+    for _k in ("mass", "stiffness", "helmholtz"):
+        APPLY_CASES.append((f"3d_p{_p}_{_k}", 3, (2, 2, 2), None, 0.08, _p, _k, 0.7, 1.3, 1, 5))
+for _p in (5, 6, 7, 8):
+    for _k in ("mass", "stiffness", "helmholtz"):
+        APPLY_CASES.append((f"3d_p{_p}_{_k}", 3, (3, 2, 2), None, 0.05, _p, _k, 10.0, 1.0, 1, 7))
+APPLY_CASES += [
+    ("3d_p3_affine_helmholtz", 3, (3, 3, 2), None, 0.0, 3, "helmholtz", 10.0, 1.0, 1, 1),
+    ("3d_p2_periodic_helmholtz", 3, (3, 3, 3), (True, True, True), 0.05, 2, "helmholtz", 2.0, 0.5, 1, 2),
+    ("3d_p4_periodic_stiffness", 3, (3, 4, 3), (True, False, True), 0.05, 4, "stiffness", 0.0, 1.0, 1, 3),
+    ("3d_p3_vector_stiffness", 3, (2, 2, 2), None, 0.08, 3, "stiffness", 0.0, 1.3, 3, 4),
+    ("3d_p4_vector_helmholtz", 3, (2, 2, 2), None, 0.08, 4, "helmholtz", 10.0, 1.0, 3, 4),
+    ("2d_p3_vector_mass", 2, (3, 2), None, 0.08, 3, "mass", 0.0, 1.0, 2, 0),
+    ("cfg1_poisson", 2, (16, 16), None, 0.0, 4, "stiffness", 0.0, 1.0, 1, 0),
+    ("2d_p12_helmholtz", 2, (2, 2), None, 0.05, 12, "helmholtz", 1.0, 1.0, 1, 9),
+]
+
+# (name, d, counts, periodic, perturb, pv, pp, seed)
+MIXED_CASES = [
+    ("2d_th3", 2, (3, 2), None, 0.08, 3, 2, 3),
+    ("3d_th3", 3, (2, 2, 2), None, 0.08, 3, 2, 3),
+    ("3d_th2_periodic", 3, (3, 3, 3), (True,) * 3, 0.05, 2, 1, 4),
+    ("3d_th5", 3, (2, 2, 1), None, 0.05, 5, 4, 6),
+]
+
+
+def build(mesh_mod, fes_mod, d, counts, periodic, perturb, p, vdim=1):
+    m = mesh_mod.cartesian_mesh(counts, periodic=periodic)
+    if perturb:
+        m = mesh_mod.perturb_mesh(m, perturb, seed=11)
+    sp = fes_mod.FESpace(m, p, vdim=vdim)
+    geom = mesh_mod.compute_geometric_factors(m, sp.basis.quad)
+    return m, sp, geom
+
+
+def make_apply():
+    mesh, fespace, mfop, _, _, _ = ref_modules()
+    out, manifest = {}, []
+    for (name, d, counts, periodic, perturb, p, kind, c, nu, vdim, seed) in APPLY_CASES:
+        _, sp, geom = build(mesh, fespace, d, counts, periodic, perturb, p, vdim)
+        kw = {"mass": {}, "stiffness": {"nu": nu}, "helmholtz": {"c": c, "nu": nu}}[kind]
+        op = mfop.setup(kind, space=sp, geom=geom, **kw)
+        x = np.random.default_rng(seed).standard_normal(sp.ndofs)
+        out[name + "/y"] = op.apply(x)
+        # constrained variant (mfop.py:416-433) on the full boundary
+        if sp.mesh.boundary_faces.shape[0]:
+            bd = sp.expand_dofs(sp.boundary_dof_set())
+            out[name + "/yc"] = mfop.ConstrainedOperator(op, bd).apply(x)
+        out[name + "/element_dofs_sum"] = np.array([sp.element_dofs.sum(), sp.ndofs_scalar])
+        manifest.append(dict(name=name, d=d, counts=counts, periodic=periodic, perturb=perturb,
+                             p=p, kind=kind, c=c, nu=nu, vdim=vdim, seed=seed,
+                             ndofs=int(sp.ndofs)))
+    mixed = []
+    for (name, d, counts, periodic, perturb, pv, pp, seed) in MIXED_CASES:
+        m, vs, geom = build(mesh, fespace, d, counts, periodic, perturb, pv, vdim=d)
+        ps = fespace.FESpace(m, pp)
+        G = mfop.GradientOperator(vs, ps, geom)
+        D = mfop.DivergenceOperator(vs, ps, geom)
+        rng = np.random.default_rng(seed)
+        q = rng.standard_normal(ps.ndofs_scalar)
+        v = rng.standard_normal(vs.ndofs)
+        out[name + "/G"] = G.apply(q)
+        out[name + "/Gt"] = G.apply_transpose(v)
+        out[name + "/D"] = D.apply(v)
+        mixed.append(dict(name=name, d=d, counts=counts, periodic=periodic, perturb=perturb,
+                          pv=pv, pp=pp, seed=seed))
+    np.savez_compressed(os.path.join(HERE, "apply.npz"), **out)
+    return {"apply": manifest, "mixed": mixed}
+
+
+def make_numbering():
+    mesh, fespace, _, _, _, _ = ref_modules()
+    cases = [(2, (3, 2), None, 3), (3, (2, 2, 2), None, 3), (3, (3, 2, 4), None, 4),
+             (3, (3, 3, 3), (True,) * 3, 3), (2, (3, 4), (True, False), 4),
+             (3, (4, 3, 3), (False, True, True), 2), (3, (2, 3, 2), None, 1)]
+    out, manifest = {}, []
+    for i, (d, counts, periodic, p) in enumerate(cases):
+        m = mesh.perturb_mesh(mesh.cartesian_mesh(counts, periodic=periodic), 0.08, seed=11)
+        sp = fespace.FESpace(m, p)
+        key = f"n{i}"
+        out[key + "/element_dofs"] = sp.element_dofs
+        out[key + "/boundary"] = sp.boundary_dof_set()
+        out[key + "/owner_elem"] = sp.dof_owner_elem
+        out[key + "/corners"] = m.corners
+        geom = mesh.compute_geometric_factors(m, sp.basis.quad)
+        out[key + "/detj"] = geom.detj
+        out[key + "/jinv"] = geom.jinv
+        manifest.append(dict(key=key, d=d, counts=counts, periodic=periodic, p=p,
+                             ndofs=int(sp.ndofs_scalar)))
+    np.savez_compressed(os.path.join(HERE, "numbering.npz"), **out)
+    return {"numbering": manifest}
+
+
+GROUPS = {"apply": make_apply, "numbering": make_numbering}
+
+
+def main(argv):
+    groups = argv or list(GROUPS)
+    path = os.path.join(HERE, "manifest.json")
+    manifest = json.load(open(path)) if os.path.exists(path) else {}
+    for g in groups:
+        manifest.update(GROUPS[g]())
+        print("wrote", g)
+    with open(path, "w") as f:
+        json.dump(manifest, f, indent=1)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
