@@ -20,6 +20,7 @@ struct GeomParams {
   double* __restrict__ fac;            // (ne, K, nq^d)
   int64_t ne;
   int dim, nq, kind, nfac;
+  int64_t fstride;
   double c, nu;
   double pts[32];
   double w1[32];
@@ -81,7 +82,7 @@ __global__ void factor_kernel(const __grid_constant__ GeomParams P) {
   double w = 1.0;
   for (int a = d - 1; a >= 0; --a) w = __dmul_rn(w, P.w1[qi[a]]);
   const double wdet = __dmul_rn(detj, w);
-  double* out = P.fac + e * P.nfac * nqd + q;
+  double* out = P.fac + e * P.fstride + q;
   int k = 0;
   if (P.kind == FB_MASS || P.kind == FB_HELMHOLTZ) {
     out[int64_t(k++) * nqd] = P.kind == FB_HELMHOLTZ ? __dmul_rn(P.c, wdet) : wdet;
@@ -103,7 +104,7 @@ __global__ void factor_kernel(const __grid_constant__ GeomParams P) {
 
 int build_factors_device(int dim, int64_t ne, const double* corners_dev, int nq,
                          const double* pts, const double* w1, int kind, double c, double nu,
-                         double* fac_dev, int nfac, cudaStream_t st) {
+                         double* fac_dev, int nfac, int64_t fstride, cudaStream_t st) {
   GeomParams P;
   P.corners = corners_dev;
   P.fac = fac_dev;
@@ -112,6 +113,7 @@ int build_factors_device(int dim, int64_t ne, const double* corners_dev, int nq,
   P.nq = nq;
   P.kind = kind;
   P.nfac = nfac;
+  P.fstride = fstride;
   P.c = c;
   P.nu = nu;
   for (int i = 0; i < nq && i < 32; ++i) {

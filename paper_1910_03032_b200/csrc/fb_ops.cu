@@ -14,7 +14,7 @@ namespace fb {
 
 int build_factors_device(int dim, int64_t ne, const double* corners_dev, int nq,
                          const double* pts, const double* w1, int kind, double c, double nu,
-                         double* fac_dev, int nfac, cudaStream_t st);
+                         double* fac_dev, int nfac, int64_t fstride, cudaStream_t st);
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -59,10 +59,13 @@ struct fb_restriction {
   int nb = 0;  // element-boundary positions per element
   int64_t nsrows = 0;
   DevBuf<int> s_row, s_off, s_ent;
+  int nlocp = 0;           // per-element stride of map_pad (multiple of 4)
+  DevBuf<int> map_pad;     // (ne, nlocp) for 16-byte bulk copies
 };
 
 struct fb_operator {
   int kind = 0, dim = 0, vdim = 1, nq = 0, nv = 0, np = 0, nfac = 0;
+  int64_t fstride = 0;  // per-element factor stride (nfac * nq^dim rounded to even)
   const fb_restriction* rv = nullptr;
   const fb_restriction* rp = nullptr;
   bool fast = false;
@@ -107,44 +110,44 @@ void diff_matrix(const double* x, int n, double* D) {
   }
 }
 
-template <int N, int Q, int KIND, int NE, int NT>
+template <int N, int Q, int KIND, int NE, int NT, int MINB>
 int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
-  constexpr int QP = Q | 1;
-  constexpr size_t smem = size_t(NE) * 3 * Q * Q * QP * sizeof(double);
+  constexpr size_t smem = SF3Shape<N, Q, KIND, NE>::SMEM;
   static bool configured = false;
   if (!configured) {
-    FB_TRY_CUDA(cudaFuncSetAttribute(sf3_fast_kernel<N, Q, KIND, NE, NT>,
+    FB_TRY_CUDA(cudaFuncSetAttribute(sf3_fast_kernel<N, Q, KIND, NE, NT, MINB>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = true;
   }
   SF3Params p = op->fp;
   p.x = x;
   p.y = y;
-  dim3 grid(ceil_div(op->rv->ne, NE), op->vdim);
-  sf3_fast_kernel<N, Q, KIND, NE, NT><<<grid, NT, smem, st>>>(p);
+  sf3_fast_kernel<N, Q, KIND, NE, NT, MINB><<<ceil_div(op->rv->ne, NE), NT, smem, st>>>(p);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
 
-template <int N, int Q, int NE, int NT>
+template <int N, int Q, int NE, int NT, int MINB>
 int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   switch (op->kind) {
-    case FB_MASS: return launch_fast_t<N, Q, kMass, NE, NT>(op, x, y, st);
-    case FB_STIFFNESS: return launch_fast_t<N, Q, kStiff, NE, NT>(op, x, y, st);
-    default: return launch_fast_t<N, Q, kHelm, NE, NT>(op, x, y, st);
+    case FB_MASS: return launch_fast_t<N, Q, kMass, NE, NT, MINB>(op, x, y, st);
+    case FB_STIFFNESS: return launch_fast_t<N, Q, kStiff, NE, NT, MINB>(op, x, y, st);
+    default: return launch_fast_t<N, Q, kHelm, NE, NT, MINB>(op, x, y, st);
   }
 }
 
+// (N, Q, elements per CTA, threads, min CTAs/SM) per degree; shared memory
+// per CTA is the map block plus 4 work buffers per element (25-45 KB).
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   switch (op->rv->p) {
-    case 1: return launch_fast_kind<2, 3, 28, 256>(op, x, y, st);
-    case 2: return launch_fast_kind<3, 4, 16, 256>(op, x, y, st);
-    case 3: return launch_fast_kind<4, 5, 10, 256>(op, x, y, st);
-    case 4: return launch_fast_kind<5, 6, 7, 256>(op, x, y, st);
-    case 5: return launch_fast_kind<6, 7, 5, 256>(op, x, y, st);
-    case 6: return launch_fast_kind<7, 8, 4, 256>(op, x, y, st);
-    case 7: return launch_fast_kind<8, 9, 3, 256>(op, x, y, st);
-    case 8: return launch_fast_kind<9, 10, 2, 224>(op, x, y, st);
+    case 1: return launch_fast_kind<2, 3, 32, 288, 3>(op, x, y, st);
+    case 2: return launch_fast_kind<3, 4, 16, 256, 3>(op, x, y, st);
+    case 3: return launch_fast_kind<4, 5, 8, 256, 3>(op, x, y, st);
+    case 4: return launch_fast_kind<5, 6, 5, 256, 3>(op, x, y, st);
+    case 5: return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
+    case 6: return launch_fast_kind<7, 8, 2, 192, 4>(op, x, y, st);
+    case 7: return launch_fast_kind<8, 9, 1, 128, 4>(op, x, y, st);
+    case 8: return launch_fast_kind<9, 10, 1, 128, 4>(op, x, y, st);
     default: set_error("fast path not built for this degree"); return FB_ERR_UNSUPPORTED;
   }
 }
@@ -162,12 +165,13 @@ int scatter_rows(const fb_restriction* r, bool split, const double* S, int64_t S
   return FB_OK;
 }
 
-// AoS (ne, nq, k) -> element-blocked (ne, k, nq) into dst at component offset
-void relayout(const double* src, int64_t ne, int nqd, int k, double* dst, int ktot, int koff) {
+// AoS (ne, nq, k) -> element-blocked (ne, [k, nq] padded to fstride)
+void relayout(const double* src, int64_t ne, int nqd, int k, double* dst, int64_t fstride,
+              int koff) {
   for (int64_t e = 0; e < ne; ++e)
     for (int c = 0; c < k; ++c)
       for (int q = 0; q < nqd; ++q)
-        dst[(e * ktot + koff + c) * nqd + q] = src[(e * nqd + q) * k + c];
+        dst[e * fstride + int64_t(koff + c) * nqd + q] = src[(e * nqd + q) * k + c];
 }
 
 }  // namespace
@@ -193,12 +197,12 @@ static int finish_operator(fb_operator* op, const double* points, const double* 
     diff_matrix(points, nq1, Dq.data());
     for (int a = 0; a < nq1; ++a)
       for (int b = 0; b < nq1; ++b) fp.Dq[a][b] = Dq[a * nq1 + b];
-    fp.map = rv->map.ptr;
+    fp.map = rv->map_pad.ptr;
     fp.fac = op->fac.ptr;
     fp.ne = ne;
     fp.x_comp_stride = rv->ndofs;
     fp.S_comp_stride = ne * rv->nb;
-    fp.direct = 1;
+    fp.vdim = vdim;
     op->S_comp_stride = ne * rv->nb;
     FB_TRY_CUDA(op->S.alloc(op->S_comp_stride * vdim));
     fp.S = op->S.ptr;
@@ -293,6 +297,13 @@ int fb_restriction_create(int dim, int p, int64_t ne, int64_t ndofs,
       }
   r->split_ok = ok ? 1 : 0;
   FB_TRY_CUDA(r->map.upload(map.data(), total));
+  {
+    r->nlocp = (nloc + 3) / 4 * 4;
+    std::vector<int> mp(size_t(ne) * r->nlocp, 0);
+    for (int64_t e = 0; e < ne; ++e)
+      std::memcpy(mp.data() + e * r->nlocp, map.data() + e * nloc, sizeof(int) * nloc);
+    FB_TRY_CUDA(r->map_pad.upload(mp.data(), int64_t(mp.size())));
+  }
   FB_TRY_CUDA(r->full_off.upload(off.data(), ndofs + 1));
   FB_TRY_CUDA(r->full_ent.upload(ent.data(), total));
   if (ok) {
@@ -369,13 +380,14 @@ int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction*
     if (kind != FB_STIFFNESS) FB_REQUIRE(wdet != nullptr, "mass factor (wdet) required");
     if (kind != FB_MASS) FB_REQUIRE(stiff != nullptr, "stiffness factor required");
     op->nfac = (kind == FB_MASS) ? 1 : (kind == FB_STIFFNESS ? ksym : ksym + 1);
-    fac.assign(size_t(ne) * op->nfac * nqd, 0.0);
+    op->fstride = (int64_t(op->nfac) * nqd + 1) / 2 * 2;
+    fac.assign(size_t(ne) * op->fstride, 0.0);
     int koff = 0;
     if (kind != FB_STIFFNESS) {
-      relayout(wdet, ne, nqd, 1, fac.data(), op->nfac, 0);
+      relayout(wdet, ne, nqd, 1, fac.data(), op->fstride, 0);
       koff = 1;
     }
-    if (kind != FB_MASS) relayout(stiff, ne, nqd, ksym, fac.data(), op->nfac, koff);
+    if (kind != FB_MASS) relayout(stiff, ne, nqd, ksym, fac.data(), op->fstride, koff);
   } else {
     FB_REQUIRE(rp != nullptr, "pressure restriction is NULL");
     FB_REQUIRE(rp->ne == ne && rp->dim == dim, "velocity/pressure spaces disagree");
@@ -384,8 +396,9 @@ int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction*
     op->rp = rp;
     op->np = rp->n;
     op->nfac = dim * dim;
-    fac.assign(size_t(ne) * op->nfac * nqd, 0.0);
-    relayout(grad, ne, nqd, dim * dim, fac.data(), op->nfac, 0);
+    op->fstride = (int64_t(op->nfac) * nqd + 1) / 2 * 2;
+    fac.assign(size_t(ne) * op->fstride, 0.0);
+    relayout(grad, ne, nqd, dim * dim, fac.data(), op->fstride, 0);
   }
   FB_TRY_CUDA(op->fac.upload(fac.data(), int64_t(fac.size())));
   int rc = finish_operator(op.get(), points, B, D, Bp, Dp);
@@ -427,12 +440,14 @@ int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restric
     op->np = rp->n;
     op->nfac = dim * dim;
   }
-  FB_TRY_CUDA(op->fac.alloc(ne * op->nfac * nqd));
+  op->fstride = (int64_t(op->nfac) * nqd + 1) / 2 * 2;
+  FB_TRY_CUDA(op->fac.alloc(ne * op->fstride));
+  FB_TRY_CUDA(cudaMemset(op->fac.ptr, 0, op->fac.bytes()));
   {
     DevBuf<double> cd;
     FB_TRY_CUDA(cd.upload(corners, ne * (int64_t(1) << dim) * dim));
     int rc = build_factors_device(dim, ne, cd.ptr, nq1, points, weights, kind, c, nu,
-                                  op->fac.ptr, op->nfac, 0);
+                                  op->fac.ptr, op->nfac, op->fstride, 0);
     if (rc != FB_OK) return rc;
     FB_TRY_CUDA(cudaDeviceSynchronize());
   }
@@ -477,6 +492,7 @@ static int general_apply(const fb_operator* op, int gkind, const double* x, doub
   P.np = op->np;
   P.nq = op->nq;
   P.nfac = op->nfac;
+  P.fstride = op->fstride;
   int gy = 1;
   const fb_restriction* rin = rv;
   const fb_restriction* rout = rv;

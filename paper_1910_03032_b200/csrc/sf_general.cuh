@@ -24,6 +24,7 @@ struct SFGParams {
   int64_t ne;
   int64_t in_comp_stride;           // L-vector component stride of the input
   int dim, kind, nv, np, nq, nfac;
+  int64_t fstride;
 };
 
 // out (+)= (M2 (x) M1 (x) M0) in, M_a row-major (qa x na), in dims (n2,n1,n0)
@@ -171,7 +172,7 @@ __global__ void sf_general_kernel(const __grid_constant__ SFGParams P) {
   const int nqd = ipow(nq, dim);
   const int nvd = ipow(nv, dim);
   const int npd = np > 0 ? ipow(np, dim) : 0;
-  const double* fe = P.fac + e * int64_t(P.nfac) * nqd;
+  const double* fe = P.fac + e * P.fstride;
   const int kind = P.kind;
   __syncthreads();
 
