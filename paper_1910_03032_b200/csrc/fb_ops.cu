@@ -35,7 +35,11 @@ __global__ void scatter_rows_kernel(int64_t nrows, const int* __restrict__ row_d
   const double* Sc = S + comp * S_comp_stride;
   const int b = __ldg(off + r), e = __ldg(off + r + 1);
   double acc = 0.0;
-  for (int k = b; k < e; ++k) acc += __ldg(Sc + __ldg(ent + k));
+  if (ent) {
+    for (int k = b; k < e; ++k) acc += __ldg(Sc + __ldg(ent + k));
+  } else {  // slots already in row order (fused path)
+    for (int k = b; k < e; ++k) acc += __ldg(Sc + k);
+  }
   const int64_t dof = row_dof ? int64_t(__ldg(row_dof + r)) : r;
   y[comp * y_comp_stride + dof] = acc;
 }
@@ -61,6 +65,8 @@ struct fb_restriction {
   DevBuf<int> s_row, s_off, s_ent;
   int nlocp = 0;           // per-element stride of map_pad (multiple of 4)
   DevBuf<int> map_pad;     // (ne, nlocp) for 16-byte bulk copies
+  int nbp = 0;             // per-element stride of s_pos (multiple of 4)
+  DevBuf<int> s_pos;       // (ne, nbp): transposed-CSR slot of each boundary contribution
 };
 
 struct fb_operator {
@@ -113,16 +119,24 @@ void diff_matrix(const double* x, int n, double* D) {
 template <int N, int Q, int KIND, int NE, int NT, int MINB>
 int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   constexpr size_t smem = SF3Shape<N, Q, KIND, NE>::SMEM;
-  static bool configured = false;
-  if (!configured) {
-    FB_TRY_CUDA(cudaFuncSetAttribute(sf3_fast_kernel<N, Q, KIND, NE, NT, MINB>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = true;
+  // persistent grid: as many CTAs as can be resident at once
+  static int resident = 0;
+  if (resident == 0) {
+    auto kern = sf3_fast_kernel<N, Q, KIND, NE, NT, MINB>;
+    FB_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
+    int dev = 0, sms = 0, per_sm = 0;
+    FB_TRY_CUDA(cudaGetDevice(&dev));
+    FB_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FB_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    resident = sms * (per_sm > 0 ? per_sm : 1);
   }
   SF3Params p = op->fp;
   p.x = x;
   p.y = y;
-  sf3_fast_kernel<N, Q, KIND, NE, NT, MINB><<<ceil_div(op->rv->ne, NE), NT, smem, st>>>(p);
+  p.nbatch = ceil_div(op->rv->ne, NE);
+  const int grid = p.nbatch < resident ? p.nbatch : resident;
+  sf3_fast_kernel<N, Q, KIND, NE, NT, MINB><<<grid, NT, smem, st>>>(p);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
@@ -137,13 +151,14 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 }
 
 // (N, Q, elements per CTA, threads, min CTAs/SM) per degree; shared memory
-// per CTA is the map block plus 4 work buffers per element (25-45 KB).
+// per CTA: double-buffered map/slot stage, gather buffer, 4 work buffers per
+// element (34-52 KB); the grid is persistent (all CTAs resident).
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   switch (op->rv->p) {
     case 1: return launch_fast_kind<2, 3, 32, 288, 3>(op, x, y, st);
     case 2: return launch_fast_kind<3, 4, 16, 256, 3>(op, x, y, st);
     case 3: return launch_fast_kind<4, 5, 8, 256, 3>(op, x, y, st);
-    case 4: return launch_fast_kind<5, 6, 5, 256, 3>(op, x, y, st);
+    case 4: return launch_fast_kind<5, 6, 4, 160, 5>(op, x, y, st);
     case 5: return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
     case 6: return launch_fast_kind<7, 8, 2, 192, 4>(op, x, y, st);
     case 7: return launch_fast_kind<8, 9, 1, 128, 4>(op, x, y, st);
@@ -159,7 +174,7 @@ int scatter_rows(const fb_restriction* r, bool split, const double* S, int64_t S
   dim3 grid(ceil_div(nrows, 256), ncomp);
   scatter_rows_kernel<<<grid, 256, 0, st>>>(nrows, split ? r->s_row.ptr : nullptr,
                                             split ? r->s_off.ptr : r->full_off.ptr,
-                                            split ? r->s_ent.ptr : r->full_ent.ptr, S,
+                                            split ? nullptr : r->full_ent.ptr, S,
                                             S_comp_stride, y, y_comp_stride);
   FB_CHECK_LAUNCH();
   return FB_OK;
@@ -198,12 +213,13 @@ static int finish_operator(fb_operator* op, const double* points, const double* 
     for (int a = 0; a < nq1; ++a)
       for (int b = 0; b < nq1; ++b) fp.Dq[a][b] = Dq[a * nq1 + b];
     fp.map = rv->map_pad.ptr;
+    fp.spos = rv->s_pos.ptr;
     fp.fac = op->fac.ptr;
     fp.ne = ne;
     fp.x_comp_stride = rv->ndofs;
     fp.S_comp_stride = ne * rv->nb;
     fp.vdim = vdim;
-    op->S_comp_stride = ne * rv->nb;
+    op->S_comp_stride = ne * rv->nb;  // == number of transposed-CSR slots
     FB_TRY_CUDA(op->S.alloc(op->S_comp_stride * vdim));
     fp.S = op->S.ptr;
   } else {
@@ -318,18 +334,22 @@ int fb_restriction_create(int dim, int p, int64_t ne, int64_t ndofs,
     const int64_t nr = int64_t(rows.size());
     std::vector<int> soff(nr + 1, 0);
     for (int64_t i = 0; i < nr; ++i) soff[i + 1] = soff[i] + count[rows[i]];
-    std::vector<int> sent(soff[nr]);
+    // slot of every (element, boundary position) contribution in row order;
+    // within a row, slots ascend with the flat E index (np.bincount order)
+    r->nbp = (nb + 3) / 4 * 4;
+    std::vector<int> spos(size_t(ne) * r->nbp, 0);
     std::vector<int> pos(soff.begin(), soff.end() - 1);
     for (int64_t e = 0; e < ne; ++e)
       for (int l = 0; l < nloc; ++l) {
         if (interior[l]) continue;
         const int d = map[e * nloc + l];
-        sent[pos[rowid[d]]++] = int(e * nb + rank[l]);
+        spos[e * r->nbp + rank[l]] = pos[rowid[d]]++;
       }
     r->nsrows = nr;
     FB_TRY_CUDA(r->s_row.upload(rows.data(), nr));
     FB_TRY_CUDA(r->s_off.upload(soff.data(), nr + 1));
-    FB_TRY_CUDA(r->s_ent.upload(sent.data(), int64_t(sent.size())));
+    FB_TRY_CUDA(r->s_pos.upload(spos.data(), int64_t(spos.size())));
+    r->s_ent.reset();
   }
   *out = r.release();
   return FB_OK;

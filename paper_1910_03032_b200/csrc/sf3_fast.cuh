@@ -14,30 +14,33 @@
 // MACs/element = 2(n^3 q + n^2 q^2 + n q^3) + 6 q^4 (stiffness/Helmholtz),
 // versus 8 full 3-pass contractions in the reference.
 //
-// Data movement (B200):
-//   * at CTA entry one thread arms an mbarrier and issues a bulk async copy
-//     (cp.async.bulk, the TMA 1D engine) of the CTA's L->E map block into
-//     shared memory, plus a bulk L2 prefetch (cp.async.bulk.prefetch.L2) of
-//     its element-blocked factor block (ne, K, q^3): the factor stream runs
-//     HBM -> L2 while the CTA gathers and runs the forward passes.
-//   * as soon as the map lands, every thread issues cp.async (LDGSTS) 8-byte
-//     gathers x[map[l]] straight into the work buffer -- no register round
-//     trip, all loads in flight at once.
-//   * the pointwise stage reads the factors point-parallel from L2 (7 independent
-//     loads per point); keeping them out of shared memory lets 3-6 CTAs share
-//     an SM, which is what hides the shared-memory and FMA latencies.
-//   * vector operators (vdim > 1) loop over components inside the CTA, so the
-//     factors are read from HBM once per element, not once per component.
+// Schedule (persistent CTAs, one batch of NE elements per iteration):
+//   * the CTA walks batches blockIdx.x, +gridDim.x, ...; work items are
+//     (batch, component) pairs so vector operators (vdim > 1) reuse the
+//     batch's factors from L2 instead of re-reading them from HBM.
+//   * at the start of batch i one thread issues, for batch i+2, a bulk async
+//     copy (cp.async.bulk = TMA 1D engine) of its L->E map block and its
+//     transposed-map slot block into a 3-slot shared-memory ring (mbarrier
+//     per slot), and, for batch i+1, a bulk L2 prefetch
+//     (cp.async.bulk.prefetch.L2) of its element-blocked factor block, so the
+//     HBM stream of the next batches overlaps this batch's arithmetic.
+//   * right after the first pass of item i every thread issues cp.async
+//     (LDGSTS) 8-byte gathers x[map[l]] of item i+1 into the gather buffer;
+//     they land while item i finishes.
+//   * the pointwise stage reads the 7 factors per point from L2.
 //
 // Compute mapping: "one 1D line per thread per pass".  Each pass assigns
 // threads whole lines along the contraction direction, loads the line into
 // registers once and produces all outputs of that line (n loads for n*q
-// DFMAs); the 1D matrices are kernel parameters.  The z-line owner keeps U
-// and G_z in registers across the pointwise stage.
+// DFMAs); the 1D matrices are kernel parameters.  Derivative passes give a
+// thread the x-, y- (and z-) lines of one index pair so each Dq coefficient
+// feeds 2-3 DFMAs.  Work buffers use an odd x-pitch so x-lines are bank-
+// conflict free.
 //
 // Output: element-interior DoFs (multiplicity 1) are written straight to y;
-// element-boundary DoFs go to the shared-entry buffer S (ne, NB) and are
-// summed by scatter_rows in ascending flat-E order (bitwise np.bincount).
+// element-boundary contributions are written to their slot of the
+// transposed map (row = DoF, slots ascending in flat E index), so
+// scatter_rows sums contiguous runs in np.bincount order (bitwise equal).
 #pragma once
 
 #include "fb_common.cuh"
@@ -50,14 +53,16 @@ enum SFKind { kMass = 0, kStiff = 1, kHelm = 2 };
 
 struct SF3Params {
   const int* __restrict__ map;     // (ne, NLOCP) L->E map, int32, padded per element
+  const int* __restrict__ spos;    // (ne, NBP) transposed-CSR slot of each boundary contribution
   const double* __restrict__ fac;  // (ne, FACP) element-blocked factors (K, q^3), padded
   const double* __restrict__ x;    // input L-vector (all components)
   double* __restrict__ y;          // output L-vector: interior DoFs
-  double* __restrict__ S;          // (vdim, ne, NB) element-boundary contributions
+  double* __restrict__ S;          // (vdim, slots) element-boundary contributions, row order
   int64_t ne;
   int64_t x_comp_stride;           // component stride of x / y
   int64_t S_comp_stride;
   int vdim;
+  int nbatch;                      // ceil(ne / NE)
   double B[kMaxQ1][kMaxQ1];        // B[q][i]  basis values at rule points
   double Dq[kMaxQ1][kMaxQ1];       // Dq[q][r] collocated derivative at rule points
 };
@@ -91,10 +96,16 @@ struct SF3Shape {
   static constexpr int NK = KindInfo<KIND>::NK;
   static constexpr int FACP = round_up(NK * Q3, 2);
   static constexpr int NB = (N <= 2) ? NLOC : NLOC - (N - 2) * (N - 2) * (N - 2);
-  // shared-memory plan (bytes): [mbarrier | map | work]
-  static constexpr int OFF_MAP = 16;
-  static constexpr int OFF_WORK = round_up(OFF_MAP + NE * NLOCP * 4, 16);
-  static constexpr int NBUF = (KIND == kMass) ? 3 : 4;  // work buffers per element
+  static constexpr int NBP = round_up(NB, 4);
+  static constexpr int NBUF = (KIND == kMass) ? 2 : 4;  // work buffers per element
+  static constexpr int XBUF = N * N * (N | 1);          // gathered x_e (odd pitch)
+  // shared-memory plan (bytes):
+  //   [3 mbarriers | 3 x (map | slots) | gather buffer | work buffers]
+  static constexpr int NSTAGE = 3;
+  static constexpr int STAGE = round_up(NE * NLOCP * 4 + NE * NBP * 4, 16);
+  static constexpr int OFF_STAGE = 32;
+  static constexpr int OFF_X = OFF_STAGE + NSTAGE * STAGE;
+  static constexpr int OFF_WORK = round_up(OFF_X + NE * XBUF * 8, 16);
   static constexpr int SMEM = OFF_WORK + NE * NBUF * BUF * 8;
 };
 
@@ -159,288 +170,364 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
 
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 __device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 template <int N, int Q, int KIND, int NE, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constant__ SF3Params P) {
   using Sh = SF3Shape<N, Q, KIND, NE>;
   constexpr int QP = Sh::QP, BUF = Sh::BUF, NLOC = Sh::NLOC, NLOCP = Sh::NLOCP;
-  constexpr int Q2 = Sh::Q2, Q3 = Sh::Q3, FACP = Sh::FACP, NB = Sh::NB, NBUF = Sh::NBUF;
-  static_assert(Q <= kMaxQ1, "Q too large");
+  constexpr int Q2 = Sh::Q2, Q3 = Sh::Q3, FACP = Sh::FACP, NBP = Sh::NBP, NBUF = Sh::NBUF;
+  constexpr int NQX = N | 1;  // x pitch of the gather buffer
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
-  const int* smap = reinterpret_cast<const int*>(smem_raw + Sh::OFF_MAP);
+  double* sx = reinterpret_cast<double*>(smem_raw + Sh::OFF_X);
   double* smem = reinterpret_cast<double*>(smem_raw + Sh::OFF_WORK);
+  auto stage_map = [&](int s) {
+    return reinterpret_cast<const int*>(smem_raw + Sh::OFF_STAGE + s * Sh::STAGE);
+  };
+  auto stage_pos = [&](int s) {
+    return reinterpret_cast<const int*>(smem_raw + Sh::OFF_STAGE + s * Sh::STAGE +
+                                        NE * NLOCP * 4);
+  };
 
   const int tid = threadIdx.x;
-  const int64_t e0 = int64_t(blockIdx.x) * NE;
   const int64_t ne = P.ne;
-  const int nel = (ne - e0) < NE ? int(ne - e0) : NE;
-  const uint32_t bar_map = smem_u32(&bars[0]);
-
-  if (tid == 0) {
-    mbar_init(bar_map, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-    const uint32_t mbytes = uint32_t(nel) * NLOCP * 4u;
-    mbar_expect_tx(bar_map, mbytes);
-    bulk_g2s(smem_u32(smap), P.map + e0 * NLOCP, mbytes, bar_map);
-    // factors stream HBM -> L2 while the CTA gathers and runs the forward passes
-    bulk_prefetch_l2(P.fac + e0 * FACP, int64_t(nel) * FACP * 8);
-  }
+  const int nbatch = P.nbatch;
+  const int vdim = P.vdim;
 
   auto IX = [](int z, int yy, int xx) { return (z * Q + yy) * QP + xx; };
-
-  mbar_wait(bar_map, 0);
-
-#pragma unroll 1
-  for (int comp = 0; comp < P.vdim; ++comp) {
-    const double* __restrict__ x = P.x + comp * P.x_comp_stride;
-    double* __restrict__ y = P.y + comp * P.x_comp_stride;
-    double* __restrict__ S = P.S + comp * P.S_comp_stride;
-    if (comp > 0) __syncthreads();  // previous component done with b0
-
-    // ---- P0: gather x_e (L->E) via cp.async -------------------------------
+  auto XI = [](int z, int yy, int xx) { return (z * N + yy) * NQX + xx; };
+  auto nel_of = [&](int batch) {
+    const int64_t e0 = int64_t(batch) * NE;
+    return (ne - e0) < NE ? int(ne - e0) : NE;
+  };
+  // one thread: stage map/slots of `batch` into ring slot `s`
+  auto issue_stage = [&](int batch, int s) {
+    const int64_t e0 = int64_t(batch) * NE;
+    const int nel = nel_of(batch);
+    const uint32_t mbytes = uint32_t(nel) * NLOCP * 4u;
+    const uint32_t pbytes = uint32_t(nel) * NBP * 4u;
+    const uint32_t bar = smem_u32(&bars[s]);
+    mbar_expect_tx(bar, mbytes + pbytes);
+    bulk_g2s(smem_u32(stage_map(s)), P.map + e0 * NLOCP, mbytes, bar);
+    bulk_g2s(smem_u32(stage_pos(s)), P.spos + e0 * NBP, pbytes, bar);
+  };
+  auto prefetch_factors = [&](int batch) {
+    const int64_t e0 = int64_t(batch) * NE;
+    bulk_prefetch_l2(P.fac + e0 * FACP, int64_t(nel_of(batch)) * FACP * 8);
+  };
+  // all threads: cp.async gathers of component `comp` of `batch` into sx
+  auto issue_gather = [&](int batch, int comp, int s) {
+    const int nel = nel_of(batch);
+    const int* smap = stage_map(s);
+    const double* xc = P.x + comp * P.x_comp_stride;
 #pragma unroll 4
     for (int idx = tid; idx < nel * NLOC; idx += NT) {
       const int el = idx / NLOC, l = idx - el * NLOC;
       const int i = l % N, j = (l / N) % N, k = l / (N * N);
-      cp_async8(smem_u32(smem + el * NBUF * BUF + IX(k, j, i)), x + smap[el * NLOCP + l]);
+      cp_async8(smem_u32(sx + el * Sh::XBUF + XI(k, j, i)), xc + smap[el * NLOCP + l]);
     }
-    cp_async_wait_all();
-    __syncthreads();
+    cp_async_commit();
+  };
 
-    // ---- P1: x-lines (k,j): b0 -> b1 --------------------------------------
-    #pragma unroll 1
-    for (int L = tid; L < NE * N * N; L += NT) {
-      const int el = L / (N * N), r = L - el * N * N;
-      const int k = r / N, j = r - k * N;
-      const double* in = smem + el * NBUF * BUF + IX(k, j, 0);
-      double* out = smem + el * NBUF * BUF + BUF + IX(k, j, 0);
-      double v[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) v[i] = in[i];
-#pragma unroll
-      for (int a = 0; a < Q; ++a) {
-        double acc = 0.0;
-#pragma unroll
-        for (int i = 0; i < N; ++i) acc = fma(P.B[a][i], v[i], acc);
-        out[a] = acc;
-      }
-    }
-    __syncthreads();
+  if (tid == 0) {
+    for (int h = 0; h < Sh::NSTAGE; ++h) mbar_init(smem_u32(&bars[h]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
-    // ---- P2: y-lines (k,a): b1 -> b2 --------------------------------------
-    #pragma unroll 1
-    for (int L = tid; L < NE * N * Q; L += NT) {
-      const int el = L / (N * Q), r = L - el * N * Q;
-      const int k = r / Q, a = r - k * Q;
-      const double* in = smem + el * NBUF * BUF + BUF + IX(k, 0, a);
-      double* out = smem + el * NBUF * BUF + 2 * BUF + IX(k, 0, a);
-      double v[N];
-#pragma unroll
-      for (int j = 0; j < N; ++j) v[j] = in[j * QP];
-#pragma unroll
-      for (int b = 0; b < Q; ++b) {
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) acc = fma(P.B[b][j], v[j], acc);
-        out[b * QP] = acc;
-      }
-    }
-    __syncthreads();
+  int batch = blockIdx.x;
+  if (batch >= nbatch) return;
+  const int G = gridDim.x;
+  if (tid == 0) {
+    issue_stage(batch, 0);
+    prefetch_factors(batch);
+    if (batch + G < nbatch) issue_stage(batch + G, 1);
+  }
+  mbar_wait(smem_u32(&bars[0]), 0);
+  issue_gather(batch, 0, 0);
 
-    // ---- P3: z-lines (b,a): b2 -> U (b0) and Gz = Dq_z U (b3) --------------
+  // local iteration counter `it` over batches; ring slot it % 3 holds the
+  // batch's map/slots (staged two batches ahead); slot h's mbarrier completes
+  // once per three batches, so batch it waits on parity (it / 3) & 1.
 #pragma unroll 1
-    for (int L = tid; L < NE * Q2; L += NT) {
-      const int el = L / Q2, r = L - el * Q2;
-      const int b = r / Q, a = r - b * Q;
-      double* base = smem + el * NBUF * BUF;
-      double v[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) v[k] = base[2 * BUF + IX(k, b, a)];
-      double u[Q];
-#pragma unroll
-      for (int c = 0; c < Q; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) acc = fma(P.B[c][k], v[k], acc);
-        u[c] = acc;
-      }
-      if (KIND == kMass) {
-        // mass: scale by wdet and contract back along z right here
-        const double* __restrict__ f = P.fac + (e0 + el) * FACP + b * Q + a;
-#pragma unroll
-        for (int c = 0; c < Q; ++c) u[c] = __ldg(f + c * Q2) * u[c];
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double acc = 0.0;
-#pragma unroll
-          for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], u[c], acc);
-          base[IX(k, b, a)] = acc;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int s = 0; s < Q; ++s) acc = fma(P.Dq[c][s], u[s], acc);
-          base[3 * BUF + IX(c, b, a)] = acc;
-          base[IX(c, b, a)] = u[c];
-        }
-      }
+  for (int it = 0; batch < nbatch; ++it, batch += G) {
+    const int s = it % Sh::NSTAGE;
+    const int s1 = (it + 1) % Sh::NSTAGE;
+    const int next = batch + G;
+    const int64_t e0 = int64_t(batch) * NE;
+    const int nel = nel_of(batch);
+    const int* smap = stage_map(s);
+    const int* spos = stage_pos(s);
+    // slot (it+2)%3 was last read by batch it-1, finished at its final barrier
+    if (tid == 0) {
+      if (next + G < nbatch) issue_stage(next + G, (it + 2) % Sh::NSTAGE);
+      if (next < nbatch) prefetch_factors(next);
     }
-    __syncthreads();
 
-    if (KIND != kMass) {
-      // ---- P4: derivative lines: x (c,b) b0 -> b1; y (c,a) b0 -> b2 -------
 #pragma unroll 1
-      for (int L = tid; L < NE * 2 * Q2; L += NT) {
-        const int el = L / (2 * Q2);
-        int r = L - el * 2 * Q2;
-        double* base = smem + el * NBUF * BUF;
-        const bool xl = r < Q2;
-        if (!xl) r -= Q2;
-        const int c = r / Q, t = r - c * Q;
-        // x-line (c, b=t) stride 1;  y-line (c, a=t) stride QP
-        const int st = xl ? 1 : QP;
-        const double* in = base + (xl ? IX(c, t, 0) : IX(c, 0, t));
-        double* out = base + (xl ? BUF : 2 * BUF) + (xl ? IX(c, t, 0) : IX(c, 0, t));
-        double v[Q];
+    for (int comp = 0; comp < vdim; ++comp) {
+      double* __restrict__ y = P.y + comp * P.x_comp_stride;
+      double* __restrict__ S = P.S + comp * P.S_comp_stride;
+      cp_async_wait_all();
+      __syncthreads();
+
+      // ---- P1: x-lines (k,j): gather buffer -> b1 --------------------------
+#pragma unroll 1
+      for (int L = tid; L < NE * N * N; L += NT) {
+        const int el = L / (N * N), r = L - el * N * N;
+        const int k = r / N, j = r - k * N;
+        const double* in = sx + el * Sh::XBUF + XI(k, j, 0);
+        double* out = smem + el * NBUF * BUF + BUF + IX(k, j, 0);
+        double v[N];
 #pragma unroll
-        for (int s = 0; s < Q; ++s) v[s] = in[s * st];
+        for (int i = 0; i < N; ++i) v[i] = in[i];
 #pragma unroll
         for (int a = 0; a < Q; ++a) {
           double acc = 0.0;
 #pragma unroll
-          for (int s = 0; s < Q; ++s) acc = fma(P.Dq[a][s], v[s], acc);
-          out[a * st] = acc;
+          for (int i = 0; i < N; ++i) acc = fma(P.B[a][i], v[i], acc);
+          out[a] = acc;
         }
       }
       __syncthreads();
 
-      // ---- P5: pointwise quadrature-point factors (read from L2) -------------
-      //   b0: U -> f_u,  b1: G0 -> f0,  b2: G1 -> f1,  b3: G2 -> f2
-      constexpr int o = (KIND == kHelm) ? 1 : 0;
-#pragma unroll 2
-      for (int idx = tid; idx < NE * Q3; idx += NT) {
-        const int el = idx / Q3, qp = idx - el * Q3;
-        const int c = qp / Q2, ba = qp - c * Q2;
-        const int b = ba / Q, a = ba - b * Q;
-        double* base = smem + el * NBUF * BUF + IX(c, b, a);
-        const double* __restrict__ f = P.fac + (e0 + el) * FACP + qp;
-        const double w00 = __ldg(f + (o + 0) * Q3), w01 = __ldg(f + (o + 1) * Q3);
-        const double w02 = __ldg(f + (o + 2) * Q3), w11 = __ldg(f + (o + 3) * Q3);
-        const double w12 = __ldg(f + (o + 4) * Q3), w22 = __ldg(f + (o + 5) * Q3);
-        const double wm = (KIND == kHelm) ? __ldg(f) : 0.0;
-        const double g0 = base[BUF], g1 = base[2 * BUF], g2 = base[3 * BUF];
-        base[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
-        base[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
-        base[3 * BUF] = w02 * g0 + w12 * g1 + w22 * g2;
-        if (KIND == kHelm) base[0] = wm * base[0];
+      // gather buffer is free: start the next item's gathers now
+      if (comp + 1 < vdim) {
+        issue_gather(batch, comp + 1, s);
+      } else if (next < nbatch) {
+        mbar_wait(smem_u32(&bars[s1]), ((it + 1) / Sh::NSTAGE) & 1);
+        issue_gather(next, 0, s1);
       }
-      __syncthreads();
 
-      // ---- P6: transposed derivative lines, in place: x b1, y b2, z b3 -----
+      // ---- P2: y-lines (k,a): b1 -> b0 ------------------------------------
 #pragma unroll 1
-      for (int L = tid; L < NE * 3 * Q2; L += NT) {
-        const int el = L / (3 * Q2);
-        int r = L - el * 3 * Q2;
-        const int dir = r / Q2;
-        r -= dir * Q2;
-        const int c = r / Q, t = r - c * Q;
-        double* base = smem + el * NBUF * BUF;
-        // x: line (c, b=t); y: line (c, a=t); z: line (b=c, a=t)
-        const int st = dir == 0 ? 1 : (dir == 1 ? QP : Q * QP);
-        double* io = base + (dir + 1) * BUF +
-                     (dir == 0 ? IX(c, t, 0) : (dir == 1 ? IX(c, 0, t) : IX(0, c, t)));
-        double v[Q];
+      for (int L = tid; L < NE * N * Q; L += NT) {
+        const int el = L / (N * Q), r = L - el * N * Q;
+        const int k = r / Q, a = r - k * Q;
+        const double* in = smem + el * NBUF * BUF + BUF + IX(k, 0, a);
+        double* out = smem + el * NBUF * BUF + IX(k, 0, a);
+        double v[N];
 #pragma unroll
-        for (int s = 0; s < Q; ++s) v[s] = io[s * st];
+        for (int j = 0; j < N; ++j) v[j] = in[j * QP];
 #pragma unroll
-        for (int a = 0; a < Q; ++a) {
+        for (int b = 0; b < Q; ++b) {
           double acc = 0.0;
 #pragma unroll
-          for (int s = 0; s < Q; ++s) acc = fma(P.Dq[s][a], v[s], acc);
-          io[a * st] = acc;
+          for (int j = 0; j < N; ++j) acc = fma(P.B[b][j], v[j], acc);
+          out[b * QP] = acc;
         }
       }
       __syncthreads();
 
-      // ---- P7: transposed z-lines (b,a): (b0+b1+b2+b3) -> b0[k<N] ---------
+      // ---- P3: z-lines (b,a): b0 -> U (b0 in place), Gz = Dq_z U (b3) -------
 #pragma unroll 1
       for (int L = tid; L < NE * Q2; L += NT) {
         const int el = L / Q2, r = L - el * Q2;
         const int b = r / Q, a = r - b * Q;
         double* base = smem + el * NBUF * BUF;
-        double v[Q];
+        double v[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = base[IX(k, b, a)];
+        double u[Q];
 #pragma unroll
         for (int c = 0; c < Q; ++c) {
-          const int ix = IX(c, b, a);
-          const double fu = (KIND == kHelm) ? base[ix] : 0.0;  // stiffness: no mass term
-          v[c] = ((fu + base[BUF + ix]) + base[2 * BUF + ix]) + base[3 * BUF + ix];
-        }
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
           double acc = 0.0;
 #pragma unroll
-          for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], v[c], acc);
-          base[IX(k, b, a)] = acc;
+          for (int k = 0; k < N; ++k) acc = fma(P.B[c][k], v[k], acc);
+          u[c] = acc;
         }
-      }
-    }
-    __syncthreads();
-
-    // ---- P8: transposed y-lines (k,a): b0[k][b<Q][a] -> b1[k][j<N][a] ------
-    #pragma unroll 1
-    for (int L = tid; L < NE * N * Q; L += NT) {
-      const int el = L / (N * Q), r = L - el * N * Q;
-      const int k = r / Q, a = r - k * Q;
-      const double* in = smem + el * NBUF * BUF + IX(k, 0, a);
-      double* out = smem + el * NBUF * BUF + BUF + IX(k, 0, a);
-      double v[Q];
+        if (KIND == kMass) {
+          // mass: scale by wdet and contract back along z right here
+          const double* __restrict__ f = P.fac + (e0 + el) * FACP + b * Q + a;
+          const bool live = el < nel;
 #pragma unroll
-      for (int b = 0; b < Q; ++b) v[b] = in[b * QP];
+          for (int c = 0; c < Q; ++c) u[c] = (live ? __ldg(f + c * Q2) : 0.0) * u[c];
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        double acc = 0.0;
+          for (int k = 0; k < N; ++k) {
+            double acc = 0.0;
 #pragma unroll
-        for (int b = 0; b < Q; ++b) acc = fma(P.B[b][j], v[b], acc);
-        out[j * QP] = acc;
-      }
-    }
-    __syncthreads();
-
-    // ---- P9: transposed x-lines (k,j): b1[k][j][a<Q] -> y_e, then E->L ----
-    #pragma unroll 1
-    for (int L = tid; L < nel * N * N; L += NT) {
-      const int el = L / (N * N), r = L - el * N * N;
-      const int k = r / N, j = r - k * N;
-      const int64_t e = e0 + el;
-      const double* in = smem + el * NBUF * BUF + BUF + IX(k, j, 0);
-      double v[Q];
-#pragma unroll
-      for (int a = 0; a < Q; ++a) v[a] = in[a];
-      const bool edge_line = (k == 0 || k == N - 1 || j == 0 || j == N - 1);
-      const int* mrow = smap + el * NLOCP + (k * N + j) * N;
-      double* srow = S + e * NB;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < Q; ++a) acc = fma(P.B[a][i], v[a], acc);
-        if (!edge_line && i > 0 && i < N - 1) {
-          y[mrow[i]] = 0.0 + acc;  // bincount semantics: 0.0 + contribution
+            for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], u[c], acc);
+            base[IX(k, b, a)] = acc;
+          }
         } else {
-          srow[boundary_rank3<N>(k, j, i)] = acc;
+#pragma unroll
+          for (int c = 0; c < Q; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int t = 0; t < Q; ++t) acc = fma(P.Dq[c][t], u[t], acc);
+            base[3 * BUF + IX(c, b, a)] = acc;
+            base[IX(c, b, a)] = u[c];
+          }
+        }
+      }
+      __syncthreads();
+
+      if (KIND != kMass) {
+        // ---- P4: derivative lines: x (c,b) b0 -> b1; y (c,a) b0 -> b2 -----
+#pragma unroll 1
+        for (int L = tid; L < NE * Q2; L += NT) {
+          const int el = L / Q2, r = L - el * Q2;
+          const int c = r / Q, t = r - c * Q;
+          double* base = smem + el * NBUF * BUF;
+          // the x-line (c, b=t) and the y-line (c, a=t) share Dq coefficients
+          const double* inx = base + IX(c, t, 0);
+          const double* iny = base + IX(c, 0, t);
+          double vx[Q], vy[Q];
+#pragma unroll
+          for (int s2 = 0; s2 < Q; ++s2) {
+            vx[s2] = inx[s2];
+            vy[s2] = iny[s2 * QP];
+          }
+          double* ox = base + BUF + IX(c, t, 0);
+          double* oy = base + 2 * BUF + IX(c, 0, t);
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            double ax = 0.0, ay = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < Q; ++s2) {
+              ax = fma(P.Dq[a][s2], vx[s2], ax);
+              ay = fma(P.Dq[a][s2], vy[s2], ay);
+            }
+            ox[a] = ax;
+            oy[a * QP] = ay;
+          }
+        }
+        __syncthreads();
+
+        // ---- P5: pointwise quadrature-point factors (point-parallel, from L2)
+        //   b0: U -> f_u,  b1: G0 -> f0,  b2: G1 -> f1,  b3: G2 -> f2
+        constexpr int o = (KIND == kHelm) ? 1 : 0;
+#pragma unroll 2
+        for (int idx = tid; idx < nel * Q3; idx += NT) {
+          const int el = idx / Q3, qp = idx - el * Q3;
+          const int c = qp / Q2, ba = qp - c * Q2;
+          const int b = ba / Q, a = ba - b * Q;
+          double* pt = smem + el * NBUF * BUF + IX(c, b, a);
+          const double* __restrict__ f = P.fac + (e0 + el) * FACP + qp;
+          const double w00 = __ldg(f + (o + 0) * Q3), w01 = __ldg(f + (o + 1) * Q3);
+          const double w02 = __ldg(f + (o + 2) * Q3), w11 = __ldg(f + (o + 3) * Q3);
+          const double w12 = __ldg(f + (o + 4) * Q3), w22 = __ldg(f + (o + 5) * Q3);
+          const double wm = (KIND == kHelm) ? __ldg(f) : 0.0;
+          const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = pt[3 * BUF];
+          pt[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
+          pt[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
+          pt[3 * BUF] = w02 * g0 + w12 * g1 + w22 * g2;
+          if (KIND == kHelm) pt[0] = wm * pt[0];
+        }
+        __syncthreads();
+
+        // ---- P6: transposed derivative lines, in place: x b1, y b2, z b3 ---
+#pragma unroll 1
+        for (int L = tid; L < NE * Q2; L += NT) {
+          const int el = L / Q2, r = L - el * Q2;
+          const int c = r / Q, t = r - c * Q;
+          double* base = smem + el * NBUF * BUF;
+          // x-line (c, b=t), y-line (c, a=t), z-line (b=c, a=t): same Dq^T
+          double* io0 = base + BUF + IX(c, t, 0);
+          double* io1 = base + 2 * BUF + IX(c, 0, t);
+          double* io2 = base + 3 * BUF + IX(0, c, t);
+          double v0[Q], v1[Q], v2[Q];
+#pragma unroll
+          for (int s2 = 0; s2 < Q; ++s2) {
+            v0[s2] = io0[s2];
+            v1[s2] = io1[s2 * QP];
+            v2[s2] = io2[s2 * Q * QP];
+          }
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < Q; ++s2) {
+              const double d = P.Dq[s2][a];
+              a0 = fma(d, v0[s2], a0);
+              a1 = fma(d, v1[s2], a1);
+              a2 = fma(d, v2[s2], a2);
+            }
+            io0[a] = a0;
+            io1[a * QP] = a1;
+            io2[a * Q * QP] = a2;
+          }
+        }
+        __syncthreads();
+
+        // ---- P7: transposed z-lines (b,a): (b0+b1+b2+b3) -> b0[k<N] --------
+#pragma unroll 1
+        for (int L = tid; L < NE * Q2; L += NT) {
+          const int el = L / Q2, r = L - el * Q2;
+          const int b = r / Q, a = r - b * Q;
+          double* base = smem + el * NBUF * BUF;
+          double v[Q];
+#pragma unroll
+          for (int c = 0; c < Q; ++c) {
+            const int ix = IX(c, b, a);
+            const double fu = (KIND == kHelm) ? base[ix] : 0.0;  // stiffness: no mass term
+            v[c] = ((fu + base[BUF + ix]) + base[2 * BUF + ix]) + base[3 * BUF + ix];
+          }
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], v[c], acc);
+            base[IX(k, b, a)] = acc;
+          }
+        }
+        __syncthreads();
+      }
+
+      // ---- P8: transposed y-lines (k,a): b0[k][b<Q][a] -> b1[k][j<N][a] ----
+#pragma unroll 1
+      for (int L = tid; L < NE * N * Q; L += NT) {
+        const int el = L / (N * Q), r = L - el * N * Q;
+        const int k = r / Q, a = r - k * Q;
+        const double* in = smem + el * NBUF * BUF + IX(k, 0, a);
+        double* out = smem + el * NBUF * BUF + BUF + IX(k, 0, a);
+        double v[Q];
+#pragma unroll
+        for (int b = 0; b < Q; ++b) v[b] = in[b * QP];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int b = 0; b < Q; ++b) acc = fma(P.B[b][j], v[b], acc);
+          out[j * QP] = acc;
+        }
+      }
+      __syncthreads();
+
+      // ---- P9: transposed x-lines (k,j): b1[k][j][a<Q] -> y_e, then E->L --
+#pragma unroll 1
+      for (int L = tid; L < nel * N * N; L += NT) {
+        const int el = L / (N * N), r = L - el * N * N;
+        const int k = r / N, j = r - k * N;
+        const double* in = smem + el * NBUF * BUF + BUF + IX(k, j, 0);
+        double v[Q];
+#pragma unroll
+        for (int a = 0; a < Q; ++a) v[a] = in[a];
+        const bool edge_line = (k == 0 || k == N - 1 || j == 0 || j == N - 1);
+        const int* mrow = smap + el * NLOCP + (k * N + j) * N;
+        const int* prow = spos + el * NBP;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < Q; ++a) acc = fma(P.B[a][i], v[a], acc);
+          if (!edge_line && i > 0 && i < N - 1) {
+            y[mrow[i]] = 0.0 + acc;  // bincount semantics: 0.0 + contribution
+          } else {
+            S[prow[boundary_rank3<N>(k, j, i)]] = acc;
+          }
         }
       }
     }
+    __syncthreads();  // this batch's ring slot may be overwritten next
   }
 }
 
