@@ -46,6 +46,8 @@ extern "C" {
 
 typedef struct fb_restriction fb_restriction;
 typedef struct fb_operator fb_operator;
+typedef struct fb_csr fb_csr;
+typedef struct fb_trisolve fb_trisolve;
 
 const char* fb_last_error(void);
 int fb_abi_version(void);
@@ -159,8 +161,42 @@ int fb_scalar_div(const double* num_dev, const double* den_dev, double* out_dev,
 /* p = z + beta*p with beta = num/den read on device */
 int fb_xpby_ratio(int64_t n, const double* z_dev, const double* num_dev, const double* den_dev,
                   double* p_dev, void* stream);
+/* y = x / s (s host scalar; the reference's `r / beta`, fgmres) */
+int fb_div_scalar(int64_t n, const double* x_dev, double s, double* y_dev, void* stream);
+/* y = x - num_dev[0] / den  (mean deflation, solvers.py:60-64) */
+int fb_shift_ratio(int64_t n, const double* x_dev, const double* num_dev, double den,
+                   double* y_dev, void* stream);
+/* out = den > 0 ? num / den : 0  (CG step length with the pAp <= 0 guard) */
+int fb_safe_div(const double* num_dev, const double* den_dev, double* out_dev, void* stream);
 /* y = d .* x */
 int fb_vmul(int64_t n, const double* d_dev, const double* x_dev, double* y_dev, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Sparse pieces of the LOR V-cycle (solvers.py:269-392, lor.py:61-123) */
+/* ------------------------------------------------------------------ */
+/* CSR matrix on the device (int32 indices, fp64 values), copied from host
+ * int64 CSR arrays (scipy.sparse.csr_matrix). */
+int fb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* indptr_host,
+                  const int64_t* indices_host, const double* data_host, fb_csr** out);
+void fb_csr_destroy(fb_csr* A);
+/* y = A x, rows summed sequentially in index order (scipy csr_matvec order) */
+int fb_csr_spmv(const fb_csr* A, const double* x_dev, double* y_dev, void* stream);
+/* y = b - A x */
+int fb_csr_residual(const fb_csr* A, const double* b_dev, const double* x_dev, double* y_dev,
+                    void* stream);
+/* Sparse triangular solve T x = b (lower=1: forward, 0: backward; unit_diag
+ * ignores/omits the diagonal).  Sync-free: one launch per solve. */
+int fb_trisolve_create(int64_t n, const int64_t* indptr_host, const int64_t* indices_host,
+                       const double* data_host, int lower, int unit_diag, fb_trisolve** out);
+void fb_trisolve_destroy(fb_trisolve* T);
+int fb_trisolve_solve(const fb_trisolve* T, const double* b_dev, double* x_dev, void* stream);
+/* dst[i] = src[idx[i]] (scatter=0) or dst[idx[i]] = src[i] (scatter=1) */
+int fb_permute(int64_t n, const int* idx_dev, const double* src_dev, double* dst_dev, int scatter,
+               void* stream);
+/* ILU(0) in place on sorted CSR, IKJ order (kernels/numba_backend.py:64-103):
+ * returns -1 on success, else the failing row. */
+int64_t fb_ilu0_factor_host(int64_t n, const int64_t* indptr, const int64_t* indices,
+                            double* data);
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,18 @@ _SIGS = [
     ("fb_scalar_div", _int, [_vp, _vp, _vp, _vp]),
     ("fb_xpby_ratio", _int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     ("fb_vmul", _int, [_i64, _vp, _vp, _vp, _vp]),
+    ("fb_div_scalar", _int, [_i64, _vp, _dbl, _vp, _vp]),
+    ("fb_shift_ratio", _int, [_i64, _vp, _vp, _dbl, _vp, _vp]),
+    ("fb_safe_div", _int, [_vp, _vp, _vp, _vp]),
+    ("fb_csr_create", _int, [_i64, _i64, _i64, _vp, _vp, _vp, C.POINTER(_vp)]),
+    ("fb_csr_destroy", None, [_vp]),
+    ("fb_csr_spmv", _int, [_vp, _vp, _vp, _vp]),
+    ("fb_csr_residual", _int, [_vp, _vp, _vp, _vp, _vp]),
+    ("fb_trisolve_create", _int, [_i64, _vp, _vp, _vp, _int, _int, C.POINTER(_vp)]),
+    ("fb_trisolve_destroy", None, [_vp]),
+    ("fb_trisolve_solve", _int, [_vp, _vp, _vp, _vp]),
+    ("fb_permute", _int, [_i64, _vp, _vp, _vp, _int, _vp]),
+    ("fb_ilu0_factor_host", _i64, [_i64, _vp, _vp, _vp]),
 ]
 
 SYMBOLS = [s[0] for s in _SIGS]

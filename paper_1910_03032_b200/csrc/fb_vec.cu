@@ -85,6 +85,24 @@ __global__ void xpby_ratio_kernel(int64_t n, const double* __restrict__ z,
   if (i < n) p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
 }
 
+__global__ void div_scalar_kernel(int64_t n, const double* __restrict__ x, double s,
+                                  double* __restrict__ y) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __ddiv_rn(x[i], s);
+}
+
+__global__ void shift_ratio_kernel(int64_t n, const double* __restrict__ x,
+                                   const double* __restrict__ num, double den,
+                                   double* __restrict__ y) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const double m = __ddiv_rn(num[0], den);
+  if (i < n) y[i] = __dsub_rn(x[i], m);
+}
+
+__global__ void safe_div_kernel(const double* num, const double* den, double* out) {
+  out[0] = den[0] > 0.0 ? __ddiv_rn(num[0], den[0]) : 0.0;
+}
+
 __global__ void vmul_kernel(int64_t n, const double* __restrict__ d, const double* __restrict__ x,
                             double* __restrict__ y) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -159,6 +177,27 @@ int fb_xpby_ratio(int64_t n, const double* z, const double* num, const double* d
                   void* stream) {
   if (n <= 0) return FB_OK;
   xpby_ratio_kernel<<<ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, z, num, den, p);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+int fb_div_scalar(int64_t n, const double* x, double s, double* y, void* stream) {
+  if (n <= 0) return FB_OK;
+  div_scalar_kernel<<<ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, x, s, y);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+int fb_shift_ratio(int64_t n, const double* x, const double* num, double den, double* y,
+                   void* stream) {
+  if (n <= 0) return FB_OK;
+  shift_ratio_kernel<<<ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, x, num, den, y);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+int fb_safe_div(const double* num, const double* den, double* out, void* stream) {
+  safe_div_kernel<<<1, 1, 0, as_stream(stream)>>>(num, den, out);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }

@@ -1,0 +1,575 @@
+"""Krylov solvers and LOR preconditioners on the B200: drop-in for `solvers`.
+
+Same API as the reference (solvers.py:25-425): ``SolverConfig``,
+``SolveReport``, ``cg``, ``fgmres``, ``DiagonalPreconditioner``,
+``collocated_mass_diagonal``, ``deflate_mean``, ``MeanProjector``,
+``ILU0Smoother``, ``LORPreconditioner``, ``BlockDiagonalPreconditioner``,
+``InnerCG``.  The iterations keep the reference recurrences exactly
+(preconditioned-residual stopping test, true residual every 50 CG steps,
+right-preconditioned flexible GMRES with modified Gram-Schmidt, restart 50)
+but every vector lives on the device: dots, updates, SpMVs, triangular
+solves and operator applies are CUDA kernels of libfbb200, scalars such as
+alpha stay on the device, and the host reads back a few scalars per
+iteration for the stopping test.  A numpy right-hand side gives a numpy
+solution (drop-in); a CUDA tensor gives a CUDA tensor.
+
+Objects exposing ``apply_into(x, y)`` (this package's operators and
+preconditioners) run fully on the device.  scipy sparse matrices are moved
+to the device once.  Any other ``.apply``/callable is treated as a host
+(numpy) function and called through a device<->host round trip.
+"""
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+import torch
+
+from . import device as dev
+from . import lor as lor_mod
+from . import vec
+from .geometry import compute_geometric_factors
+from .quadrature import GAUSS_LOBATTO, quadrature_rule
+from .spaces import FESpace
+
+
+@dataclass
+class SolverConfig:
+    rel_tol: float = 1e-8
+    abs_tol: float = 0.0
+    max_iters: int = 500
+    restart: int = 50
+    label: str = ""
+
+
+@dataclass
+class SolveReport:
+    converged: bool
+    iterations: int
+    final_relres: float
+    seconds: float
+    label: str = ""
+    residuals: list = field(default_factory=list)
+
+    def __str__(self):
+        tag = "converged" if self.converged else "NOT converged"
+        name = f"{self.label}: " if self.label else ""
+        return (f"{name}{tag} in {self.iterations} iterations, "
+                f"relres {self.final_relres:.3e}, {self.seconds:.3f}s")
+
+
+# -- operand normalisation ------------------------------------------------------
+
+def _device_apply(A):
+    """Return f(x, y) computing y = A x on device tensors."""
+    if hasattr(A, "apply_into"):
+        return A.apply_into
+    if sp.issparse(A):
+        D = vec.DeviceCSR(A)
+        return D.apply_into
+    fn = A.apply if hasattr(A, "apply") else A
+    if not callable(fn):
+        raise TypeError(f"cannot interpret {type(A)} as an operator")
+
+    def host_apply(x, y):
+        y.copy_(dev.to_device(np.asarray(fn(dev.to_host(x)), dtype=np.float64)))
+        return y
+
+    return host_apply
+
+
+def _device_project(project):
+    if hasattr(project, "apply_into"):
+        return project.apply_into
+
+    def host_project(x, y):
+        y.copy_(dev.to_device(np.asarray(project(dev.to_host(x)), dtype=np.float64)))
+        return y
+
+    return host_project
+
+
+def _as_apply(A):
+    """Reference-compatible helper (solvers.py:50-57)."""
+    if hasattr(A, "apply"):
+        return A.apply
+    if sp.issparse(A):
+        return lambda v: A @ v
+    if callable(A):
+        return A
+    raise TypeError(f"cannot interpret {type(A)} as an operator")
+
+
+class _DeviceMixin:
+    """numpy-or-tensor `apply` on top of a device `apply_into`."""
+
+    def apply(self, r):
+        rd, host = dev.DeviceIn.get(r)
+        out = torch.empty_like(rd)
+        self.apply_into(rd, out)
+        return dev.to_host(out) if host else out
+
+    def __call__(self, r):
+        return self.apply(r)
+
+
+# -- mean deflation ---------------------------------------------------------------
+
+class MeanProjector(_DeviceMixin):
+    """v - (sum w_i v_i / sum w_i) 1, or v - mean(v) (solvers.py:60-74)."""
+
+    def __init__(self, weights=None):
+        self.weights = weights
+        self._w = None
+        self._den = None
+
+    def apply_into(self, v, out, stream=None):
+        n = v.shape[0]
+        if self._w is None or self._w.shape[0] != n:
+            if self.weights is None:
+                self._w = torch.ones(n, dtype=torch.float64, device=dev.device())
+                self._den = float(n)
+            else:
+                w = np.asarray(self.weights, dtype=np.float64)
+                self._w = dev.to_device(w)
+                self._den = float(w.sum())
+        num = vec.workspace(n).scalars[15:16]
+        vec.dot_into(self._w, v, num, stream)
+        vec.shift_ratio(v, num, self._den, out, stream)
+        return out
+
+
+def deflate_mean(v, weights=None):
+    return MeanProjector(weights).apply(v)
+
+
+class DiagonalPreconditioner(_DeviceMixin):
+    def __init__(self, diag):
+        self.inv = 1.0 / np.asarray(diag, dtype=np.float64)
+        self._inv = None
+
+    def apply_into(self, r, z, stream=None):
+        if self._inv is None:
+            self._inv = dev.to_device(self.inv)
+        return vec.vmul(self._inv, r, z, stream)
+
+
+def collocated_mass_diagonal(space, constrained=None):
+    """GLL-collocated (lumped) mass diagonal w_i det J(x_i) (solvers.py:87-105)."""
+    rule = quadrature_rule(GAUSS_LOBATTO, space.p + 1)
+    geom = compute_geometric_factors(space.mesh, rule)
+    vals = geom.detj * geom.w[None, :]
+    diag = np.bincount(space.element_dofs.ravel(), weights=vals.ravel(),
+                       minlength=space.ndofs_scalar)
+    if space.vdim > 1:
+        diag = np.tile(diag, space.vdim)
+    if constrained is not None and len(constrained):
+        diag = diag.copy()
+        diag[np.asarray(constrained, dtype=np.int64)] = 1.0
+    return diag
+
+
+# -- Krylov --------------------------------------------------------------------------
+
+def cg(A, b, precond=None, config=None, x0=None, project=None):
+    """Preconditioned CG with the reference recurrence (solvers.py:108-169)."""
+    apply_A = _device_apply(A)
+    M = _device_apply(precond) if precond is not None else None
+    proj = _device_project(project) if project is not None else None
+    cfg = config or SolverConfig()
+    t0 = time.perf_counter()
+    bd, host = dev.DeviceIn.get(b)
+    n = bd.shape[0]
+    x = dev.zeros(n) if x0 is None else dev.to_device(x0).clone()
+    r = dev.empty(n)
+    tmp = dev.empty(n)
+    z = dev.empty(n)
+    # device scalars: 0 rz, 1 pAp, 2 alpha, 3 rz_new
+    s = dev.zeros(4)
+    if x0 is None:
+        vec.copy(bd, r)  # A(0) == 0 exactly
+    else:
+        apply_A(x, tmp)
+        vec.copy(bd, r)
+        vec.axpby(-1.0, tmp, 1.0, r)
+    if proj is not None:
+        proj(r, r)
+    if M is not None:
+        M(r, z)
+    else:
+        vec.copy(r, z)
+    if proj is not None:
+        proj(z, z)
+    vec.dot_into(r, z, s[0:1])
+    rz = float(s[0].item())
+    norm0 = math.sqrt(abs(rz))
+    history = [1.0]
+
+    def done(conv, its, rel):
+        return (dev.to_host(x) if host else x), SolveReport(conv, its, rel,
+                                                           time.perf_counter() - t0, cfg.label,
+                                                           history)
+
+    if norm0 == 0.0 or norm0 <= cfg.abs_tol:
+        return done(True, 0, 0.0)
+    p = z.clone()
+    Ap = dev.empty(n)
+    relres = 1.0
+    it = 0
+    converged = False
+    for it in range(1, cfg.max_iters + 1):
+        apply_A(p, Ap)
+        vec.dot_into(p, Ap, s[1:2])
+        vec.safe_div(s[0:1], s[1:2], s[2:3])  # alpha = rz / pAp (0 if pAp <= 0)
+        vec.axpy_dev(s[2:3], p, x, +1)
+        if it % 50 == 0:
+            apply_A(x, tmp)
+            vec.copy(bd, r)
+            vec.axpby(-1.0, tmp, 1.0, r)
+            if proj is not None:
+                proj(r, r)
+        else:
+            vec.axpy_dev(s[2:3], Ap, r, -1)
+        if M is not None:
+            M(r, z)
+        else:
+            vec.copy(r, z)
+        if proj is not None:
+            proj(z, z)
+        vec.dot_into(r, z, s[3:4])
+        pAp, _, rz_new = s[1:4].tolist()
+        if pAp <= 0.0:
+            break
+        relres = math.sqrt(abs(rz_new)) / norm0
+        history.append(relres)
+        if cfg.rel_tol > 0.0 and relres <= cfg.rel_tol:
+            converged = True
+            break
+        if rz_new == 0.0:
+            converged = True
+            break
+        vec.xpby_ratio(z, s[3:4], s[0:1], p)  # p = z + (rz_new / rz) p
+        vec.copy(s[3:4], s[0:1])
+    if cfg.rel_tol == 0.0:
+        converged = True
+    return done(converged, it, relres)
+
+
+def fgmres(A, b, precond=None, config=None, x0=None, project=None):
+    """Right-preconditioned flexible GMRES(m) with MGS (solvers.py:172-254)."""
+    apply_A = _device_apply(A)
+    M = _device_apply(precond) if precond is not None else None
+    proj = _device_project(project) if project is not None else None
+    cfg = config or SolverConfig()
+    t0 = time.perf_counter()
+    bd, host = dev.DeviceIn.get(b)
+    n = bd.shape[0]
+    x = dev.zeros(n) if x0 is None else dev.to_device(x0).clone()
+    r = dev.empty(n)
+    tmp = dev.empty(n)
+
+    def residual():
+        apply_A(x, tmp)
+        vec.copy(bd, r)
+        vec.axpby(-1.0, tmp, 1.0, r)
+
+    def norm(v):
+        return math.sqrt(vec.dot(v, v).item())
+
+    if x0 is None:
+        vec.copy(bd, r)
+    else:
+        residual()
+    beta0 = norm(r)
+    history = [1.0]
+    if beta0 == 0.0 or beta0 <= cfg.abs_tol:
+        return (dev.to_host(x) if host else x), SolveReport(True, 0, 0.0,
+                                                           time.perf_counter() - t0, cfg.label,
+                                                           history)
+    target = cfg.rel_tol * beta0
+    m = cfg.restart
+    V = torch.zeros((m + 1, n), dtype=torch.float64, device=dev.device())
+    Z = torch.zeros((m, n), dtype=torch.float64, device=dev.device())
+    hcol = dev.zeros(m + 2)
+    w = dev.empty(n)
+    it = 0
+    relres = 1.0
+    converged = False
+    while it < cfg.max_iters and not converged:
+        beta = norm(r)
+        if beta <= max(target, cfg.abs_tol):
+            converged = True
+            break
+        H = np.zeros((m + 1, m))
+        cs = np.zeros(m)
+        sn = np.zeros(m)
+        g = np.zeros(m + 1)
+        g[0] = beta
+        vec.div_scalar(r, beta, V[0])
+        j = -1
+        for j in range(m):
+            if it >= cfg.max_iters:
+                j -= 1
+                break
+            it += 1
+            zj = Z[j]
+            if M is not None:
+                M(V[j], zj)
+            else:
+                vec.copy(V[j], zj)
+            if proj is not None:
+                proj(zj, zj)
+            apply_A(zj, w)
+            for i in range(j + 1):
+                vec.dot_into(V[i], w, hcol[i:i + 1])
+                vec.axpy_dev(hcol[i:i + 1], V[i], w, -1)
+            vec.dot_into(w, w, hcol[j + 1:j + 2])
+            col = hcol[:j + 2].tolist()
+            H[:j + 1, j] = col[:j + 1]
+            H[j + 1, j] = math.sqrt(col[j + 1])
+            if H[j + 1, j] > 1e-300:
+                vec.div_scalar(w, H[j + 1, j], V[j + 1])
+            for i in range(j):
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            denom = np.hypot(H[j, j], H[j + 1, j])
+            if denom == 0.0:
+                cs[j], sn[j] = 1.0, 0.0
+            else:
+                cs[j], sn[j] = H[j, j] / denom, H[j + 1, j] / denom
+            H[j, j] = cs[j] * H[j, j] + sn[j] * H[j + 1, j]
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            relres = abs(g[j + 1]) / beta0
+            history.append(relres)
+            if relres * beta0 <= max(target, cfg.abs_tol):
+                converged = True
+                break
+        k = j + 1
+        if k > 0:
+            y = scipy.linalg.solve_triangular(H[:k, :k], g[:k], lower=False)
+            for i in range(k):
+                vec.axpby(float(y[i]), Z[i], 1.0, x)
+        residual()
+        relres = norm(r) / beta0
+        if relres * beta0 <= max(target, cfg.abs_tol):
+            converged = True
+    return (dev.to_host(x) if host else x), SolveReport(converged, it, relres,
+                                                       time.perf_counter() - t0, cfg.label,
+                                                       history)
+
+
+# -- ILU(0) smoother -----------------------------------------------------------------
+
+def _first_touch_ordering(space):
+    return lor_mod.first_touch_ordering(space)
+
+
+def _degree_ladder(p):
+    return lor_mod.degree_ladder(p)
+
+
+class ILU0Smoother:
+    """ILU(0) in a fixed ordering; forward = (LU)^-1, backward = (LU)^-T
+    (solvers.py:269-311).  The factorisation runs once on the host (C++,
+    the reference's IKJ variant); the four triangular solves run on the
+    device.  A degenerate pivot falls back to damped Jacobi 0.6/diag."""
+
+    def __init__(self, A, order, backend=None):
+        A = A.tocsr()
+        n = A.shape[0]
+        self.n = n
+        self.order = np.asarray(order, dtype=np.int64)
+        Ap = A[self.order][:, self.order].tocsr()
+        Ap.sort_indices()
+        data = Ap.data.astype(np.float64, copy=True)
+        fail = vec.ilu0_factor_host(Ap.indptr, Ap.indices, data)
+        self.jacobi = None
+        self.fail_row = fail
+        if fail >= 0:
+            diag = A.diagonal().copy()
+            diag[diag == 0.0] = 1.0
+            self.jacobi = 0.6 / diag
+            self._jac = dev.to_device(self.jacobi)
+            return
+        F = sp.csr_matrix((data, Ap.indices.copy(), Ap.indptr.copy()), shape=(n, n))
+        L = sp.tril(F, k=-1, format="csr")
+        U = sp.triu(F, k=0, format="csr")
+        self.L_factor, self.U_factor = L, U
+        self._L = vec.TriSolve(L, lower=True, unit_diag=True)
+        self._U = vec.TriSolve(U, lower=False, unit_diag=False)
+        self._Ut = vec.TriSolve(U.T.tocsr(), lower=True, unit_diag=False)
+        self._Lt = vec.TriSolve(L.T.tocsr(), lower=False, unit_diag=True)
+        self._perm = torch.from_numpy(self.order.astype(np.int32)).to(dev.device())
+        self._a = dev.empty(n)
+        self._b = dev.empty(n)
+
+    def forward_into(self, r, out, stream=None):
+        if self.jacobi is not None:
+            return vec.vmul(self._jac, r, out, stream)
+        vec.permute(self._perm, r, self._a, scatter=False, stream=stream)
+        self._L.solve_into(self._a, self._b, stream)
+        self._U.solve_into(self._b, self._a, stream)
+        return vec.permute(self._perm, self._a, out, scatter=True, stream=stream)
+
+    def backward_into(self, r, out, stream=None):
+        if self.jacobi is not None:
+            return vec.vmul(self._jac, r, out, stream)
+        vec.permute(self._perm, r, self._a, scatter=False, stream=stream)
+        self._Ut.solve_into(self._a, self._b, stream)
+        self._Lt.solve_into(self._b, self._a, stream)
+        return vec.permute(self._perm, self._a, out, scatter=True, stream=stream)
+
+    def forward(self, r):
+        rd, host = dev.DeviceIn.get(r)
+        out = torch.empty_like(rd)
+        self.forward_into(rd, out)
+        return dev.to_host(out) if host else out
+
+    def backward(self, r):
+        rd, host = dev.DeviceIn.get(r)
+        out = torch.empty_like(rd)
+        self.backward_into(rd, out)
+        return dev.to_host(out) if host else out
+
+
+class SparseLUSolver:
+    """Coarse direct solve: host sparse LU (SuperLU via scipy, COLAMD, as the
+    reference's splu at solvers.py:372), device triangular solves."""
+
+    def __init__(self, A):
+        A = A.tocsc()
+        self.n = A.shape[0]
+        lu = spla.splu(A)
+        self.lu = lu
+        self._L = vec.TriSolve(lu.L.tocsr(), lower=True, unit_diag=True)
+        self._U = vec.TriSolve(lu.U.tocsr(), lower=False, unit_diag=False)
+        self._pr = torch.from_numpy(lu.perm_r.astype(np.int32)).to(dev.device())
+        self._pc = torch.from_numpy(lu.perm_c.astype(np.int32)).to(dev.device())
+        self._a = dev.empty(self.n)
+        self._b = dev.empty(self.n)
+
+    def solve_into(self, b, x, stream=None):
+        # Pr A Pc = L U:  x = Pc U^-1 L^-1 Pr b
+        vec.permute(self._pr, b, self._a, scatter=True, stream=stream)
+        self._L.solve_into(self._a, self._b, stream)
+        self._U.solve_into(self._b, self._a, stream)
+        return vec.permute(self._pc, self._a, x, scatter=False, stream=stream)
+
+    def solve(self, b):
+        bd, host = dev.DeviceIn.get(b)
+        out = torch.empty_like(bd)
+        self.solve_into(bd, out)
+        return dev.to_host(out) if host else out
+
+
+class LORPreconditioner(_DeviceMixin):
+    """Degree-ladder V(1,1) cycle on LOR matrices (solvers.py:321-392), applied
+    on the device: per level one ILU(0) forward sweep, residual SpMV, P^T
+    restriction, recursive correction, P prolongation, residual SpMV, ILU(0)
+    backward sweep; the Q1 bottom level is a sparse direct solve."""
+
+    def __init__(self, space, kind, nu=1.0, c=0.0, dirichlet_attrs=None,
+                 pure_neumann=False, backend=None):
+        if space.vdim != 1:
+            raise ValueError("LOR cycles act componentwise on scalar spaces")
+        if pure_neumann and dirichlet_attrs is not None:
+            raise ValueError("pure-Neumann cycle expects no constrained dofs")
+        self.pure_neumann = pure_neumann
+        mesh = space.mesh
+        self.levels = []
+        self.transfers = []
+        prev = None
+        for deg in lor_mod.degree_ladder(space.p):
+            lsp = space if deg == space.p else FESpace(mesh, deg)
+            if dirichlet_attrs is None:
+                bdr = np.zeros(0, dtype=np.int64)
+            elif dirichlet_attrs == "all":
+                bdr = lsp.boundary_dof_set()
+            else:
+                bdr = lsp.boundary_dof_set(dirichlet_attrs)
+            A = lor_mod.lor_matrix(lsp, kind, nu=nu, c=c, constrained=bdr)
+            if pure_neumann:
+                A = lor_mod.constrain_matrix(A, np.array([0], dtype=np.int64))
+            self.levels.append((lsp, A))
+            if prev is not None:
+                self.transfers.append(lor_mod.nodal_interpolation(prev, lsp))
+            prev = lsp
+        self.A = self.levels[0][1]
+        self.smoothers = [ILU0Smoother(A, lor_mod.first_touch_ordering(lsp), backend=backend)
+                          for lsp, A in self.levels[:-1]]
+        self._bottom = SparseLUSolver(self.levels[-1][1])
+        self._A = [vec.DeviceCSR(A) for _, A in self.levels]
+        self._P = [vec.DeviceCSR(P) for P in self.transfers]
+        self._Pt = [vec.DeviceCSR(P.T.tocsr()) for P in self.transfers]
+        sizes = [A.shape[0] for _, A in self.levels]
+        self._x = [dev.empty(n) for n in sizes]
+        self._r = [dev.empty(n) for n in sizes]
+        self._t = [dev.empty(n) for n in sizes]
+        self._t2 = [dev.empty(n) for n in sizes]
+        self._proj = MeanProjector() if pure_neumann else None
+
+    def _cycle(self, level, r, x, st):
+        if level == len(self.levels) - 1:
+            self._bottom.solve_into(r, x, st)
+            return
+        A = self._A[level]
+        sm = self.smoothers[level]
+        t, t2 = self._t[level], self._t2[level]
+        sm.forward_into(r, x, st)
+        A.residual_into(r, x, t, st)
+        rc, xc = self._r[level + 1], self._x[level + 1]
+        self._Pt[level].apply_into(t, rc, st)
+        self._cycle(level + 1, rc, xc, st)
+        self._P[level].apply_into(xc, t, st)
+        vec.axpby(1.0, t, 1.0, x, st)
+        A.residual_into(r, x, t, st)
+        sm.backward_into(t, t2, st)
+        vec.axpby(1.0, t2, 1.0, x, st)
+
+    def apply_into(self, r, out, stream=None):
+        st = dev.stream_handle() if stream is None else stream
+        rr = r
+        if self.pure_neumann:
+            rr = self._r[0]
+            self._proj.apply_into(r, rr, st)
+        self._cycle(0, rr, out, st)
+        if self.pure_neumann:
+            self._proj.apply_into(out, out, st)
+        return out
+
+
+class BlockDiagonalPreconditioner(_DeviceMixin):
+    """One scalar preconditioner per vector component (solvers.py:395-410)."""
+
+    def __init__(self, scalar_precond, vdim, ndofs_scalar):
+        self.inner = scalar_precond
+        self.vdim = vdim
+        self.ns = ndofs_scalar
+        self._apply = _device_apply(scalar_precond)
+
+    def apply_into(self, r, out, stream=None):
+        ns = self.ns
+        for c in range(self.vdim):
+            self._apply(r[c * ns:(c + 1) * ns], out[c * ns:(c + 1) * ns])
+        return out
+
+
+class InnerCG(_DeviceMixin):
+    """Fixed-iteration CG used as a preconditioner (solvers.py:413-425)."""
+
+    def __init__(self, A, precond=None, iterations=3):
+        self.A = A
+        self.precond = precond
+        self.cfg = SolverConfig(rel_tol=0.0, max_iters=iterations)
+
+    def apply_into(self, r, out, stream=None):
+        x, _ = cg(self.A, r, precond=self.precond, config=self.cfg)
+        out.copy_(x)
+        return out

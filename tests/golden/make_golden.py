@@ -126,7 +126,82 @@ def make_numbering():
     return {"numbering": manifest}
 
 
-GROUPS = {"apply": make_apply, "numbering": make_numbering}
+# (name, d, counts, perturb, p, kind, c, seeds)
+SOLVE_CASES = [
+    ("cfg1_poisson", 2, (16, 16), 0.0, 4, "stiffness", 0.0, (0, 1, 2)),
+    ("cfg1_helmholtz", 2, (16, 16), 0.0, 4, "helmholtz", 10.0, (0,)),
+    ("2d_p7_helmholtz_pert", 2, (6, 5), 0.05, 7, "helmholtz", 10.0, (3,)),
+    ("3d_p4_helmholtz", 3, (4, 4, 4), 0.0, 4, "helmholtz", 10.0, (0,)),
+    ("3d_p7_helmholtz", 3, (4, 4, 4), 0.0, 7, "helmholtz", 10.0, (0,)),
+    ("3d_p2_stiffness_pert", 3, (5, 4, 4), 0.05, 2, "stiffness", 0.0, (1,)),
+    ("3d_p3_mass", 3, (3, 3, 3), 0.0, 3, "mass", 0.0, (2,)),
+]
+
+
+def make_solvers():
+    mesh, fespace, mfop, solvers, lor, _ = ref_modules()
+    out, manifest = {}, []
+    for (name, d, counts, perturb, p, kind, c, seeds) in SOLVE_CASES:
+        m = mesh.cartesian_mesh(counts)
+        if perturb:
+            m = mesh.perturb_mesh(m, perturb, seed=11)
+        sp_ = fespace.FESpace(m, p)
+        geom = mesh.compute_geometric_factors(m, sp_.basis.quad)
+        kw = {"mass": {}, "stiffness": {"nu": 1.0}, "helmholtz": {"c": c, "nu": 1.0}}[kind]
+        op = mfop.setup(kind, space=sp_, geom=geom, **kw)
+        bdr = sp_.boundary_dof_set()
+        A = mfop.ConstrainedOperator(op, bdr)
+        pre = solvers.LORPreconditioner(sp_, kind, nu=1.0, c=c, dirichlet_attrs="all")
+        r = np.random.default_rng(99).standard_normal(sp_.ndofs)
+        out[name + "/vcycle_in_seed"] = np.array([99])
+        out[name + "/vcycle"] = pre.apply(r)
+        sm = pre.smoothers[0]
+        out[name + "/ilu_fwd"] = sm.forward(r)
+        out[name + "/ilu_bwd"] = sm.backward(r)
+        out[name + "/lor_nnz"] = np.array([A_.nnz for _, A_ in pre.levels])
+        its = []
+        for seed in seeds:
+            b = np.random.default_rng(seed).standard_normal(sp_.ndofs)
+            b[bdr] = 0.0
+            x, rep = solvers.cg(A, b, precond=pre,
+                                config=solvers.SolverConfig(rel_tol=1e-8, max_iters=300))
+            out[f"{name}/x{seed}"] = x
+            out[f"{name}/hist{seed}"] = np.array(rep.residuals)
+            its.append(rep.iterations)
+        manifest.append(dict(name=name, d=d, counts=counts, perturb=perturb, p=p, kind=kind,
+                             c=c, seeds=list(seeds), iterations=its))
+    # ILU(0) factor values on the cfg1 finest LOR level (kernels/numba_backend.py:64-103)
+    m = mesh.cartesian_mesh((16, 16))
+    sp_ = fespace.FESpace(m, 4)
+    A = lor.lor_matrix(sp_, "stiffness", constrained=sp_.boundary_dof_set())
+    order = solvers._first_touch_ordering(sp_)
+    Ap = A[order][:, order].tocsr()
+    Ap.sort_indices()
+    data = Ap.data.astype(np.float64, copy=True)
+    from flowbench.kernels import ilu0_factor
+    fail = ilu0_factor(Ap.indptr, Ap.indices, data)
+    out["ilu/order"] = order
+    out["ilu/indptr"] = Ap.indptr
+    out["ilu/indices"] = Ap.indices
+    out["ilu/data_in"] = Ap.data
+    out["ilu/data_out"] = data
+    out["ilu/fail"] = np.array([fail])
+    # pure-Neumann Poisson with mean projection (solvers.py:361-362, 384-390)
+    m = mesh.perturb_mesh(mesh.cartesian_mesh((8, 8)), 0.05, seed=11)
+    sp_ = fespace.FESpace(m, 3)
+    geom = mesh.compute_geometric_factors(m, sp_.basis.quad)
+    L = mfop.StiffnessOperator(sp_, geom)
+    pre = solvers.LORPreconditioner(sp_, "stiffness", pure_neumann=True)
+    b = solvers.deflate_mean(np.random.default_rng(5).standard_normal(sp_.ndofs))
+    x, rep = solvers.cg(L, b, precond=pre, project=solvers.MeanProjector(),
+                        config=solvers.SolverConfig(rel_tol=1e-10, max_iters=300))
+    out["neumann/x"] = x
+    manifest.append(dict(name="neumann", iterations=[rep.iterations]))
+    np.savez_compressed(os.path.join(HERE, "solvers.npz"), **out)
+    return {"solvers": manifest}
+
+
+GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers}
 
 
 def main(argv):

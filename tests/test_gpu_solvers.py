@@ -1,0 +1,114 @@
+"""GPU: device Krylov solvers and the device LOR V-cycle against the
+reference's golden iteration counts / vectors (solvers.npz) and the oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import krylov, sumfact
+from tests.cases import build, load, manifest, rel_err
+
+pytestmark = pytest.mark.gpu
+
+SOLVE = {c["name"]: c for c in manifest()["solvers"]}
+CASES = [n for n in SOLVE if n != "neumann"]
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return load("solvers")
+
+
+def _setup(c):
+    from paper_1910_03032_b200 import mfop, solvers
+    m, sp_, geom = build(c["d"], c["counts"], None, c["perturb"], c["p"])
+    kw = {"mass": {}, "stiffness": {"nu": 1.0}, "helmholtz": {"c": c["c"], "nu": 1.0}}[c["kind"]]
+    op = mfop.setup(c["kind"], space=sp_, geom=geom, **kw)
+    bdr = sp_.boundary_dof_set()
+    A = mfop.ConstrainedOperator(op, bdr)
+    pre = solvers.LORPreconditioner(sp_, c["kind"], nu=1.0, c=c["c"], dirichlet_attrs="all")
+    return sp_, geom, A, pre, bdr
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_vcycle_and_ilu_match_reference(name, gold):
+    c = SOLVE[name]
+    sp_, _, _, pre, _ = _setup(c)
+    r = np.random.default_rng(99).standard_normal(sp_.ndofs)
+    assert rel_err(pre.smoothers[0].forward(r), gold[name + "/ilu_fwd"]) < 1e-11
+    assert rel_err(pre.smoothers[0].backward(r), gold[name + "/ilu_bwd"]) < 1e-11
+    assert rel_err(pre.apply(r), gold[name + "/vcycle"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_lor_pcg_iteration_parity(name, gold):
+    from paper_1910_03032_b200 import solvers
+    c = SOLVE[name]
+    sp_, _, A, pre, bdr = _setup(c)
+    for seed, its_ref in zip(c["seeds"], c["iterations"]):
+        b = np.random.default_rng(seed).standard_normal(sp_.ndofs)
+        b[bdr] = 0.0
+        x, rep = solvers.cg(A, b, precond=pre,
+                            config=solvers.SolverConfig(rel_tol=1e-8, max_iters=300))
+        assert rep.converged
+        assert abs(rep.iterations - its_ref) <= 1, (rep.iterations, its_ref)
+        assert rel_err(x, gold[f"{name}/x{seed}"]) < 1e-6
+        hist = gold[f"{name}/hist{seed}"]
+        k = min(len(hist), len(rep.residuals)) - 1
+        assert abs(np.log10(rep.residuals[k]) - np.log10(hist[k])) < 0.1
+
+
+def test_pure_neumann_with_mean_projector(gold):
+    from paper_1910_03032_b200 import geometry, mfop, solvers, spaces
+    m = geometry.perturb_mesh(geometry.cartesian_mesh((8, 8)), 0.05, seed=11)
+    sp_ = spaces.FESpace(m, 3)
+    geom = geometry.compute_geometric_factors(m, sp_.basis.quad)
+    L = mfop.StiffnessOperator(sp_, geom)
+    pre = solvers.LORPreconditioner(sp_, "stiffness", pure_neumann=True)
+    b = solvers.deflate_mean(np.random.default_rng(5).standard_normal(sp_.ndofs))
+    x, rep = solvers.cg(L, b, precond=pre, project=solvers.MeanProjector(),
+                        config=solvers.SolverConfig(rel_tol=1e-10, max_iters=300))
+    assert abs(rep.iterations - SOLVE["neumann"]["iterations"][0]) <= 1
+    assert rel_err(x, gold["neumann/x"]) < 1e-6
+
+
+def test_cg_device_tensors_and_plain_cg_matches_oracle():
+    import torch
+    from paper_1910_03032_b200 import mfop, solvers
+    m, sp_, geom = build(3, (3, 3, 2), None, 0.05, 3)
+    op = mfop.HelmholtzOperator(sp_, geom, 10.0)
+    ref = sumfact.make_square("helmholtz", sp_, geom, c=10.0)
+    b = np.random.default_rng(4).standard_normal(sp_.ndofs)
+    cfg = solvers.SolverConfig(rel_tol=1e-10, max_iters=500)
+    x, rep = solvers.cg(op, b, config=cfg)
+    xo, its, _ = krylov.cg(ref, b, rel_tol=1e-10, max_iters=500)
+    assert abs(rep.iterations - its) <= 1
+    assert rel_err(x, xo) < 1e-8
+    xd, rep2 = solvers.cg(op, torch.from_numpy(b).cuda(), config=cfg)
+    assert xd.is_cuda and rep2.iterations == rep.iterations
+    # diagonal preconditioner path
+    d = solvers.collocated_mass_diagonal(sp_)
+    x3, rep3 = solvers.cg(op, b, precond=solvers.DiagonalPreconditioner(d), config=cfg)
+    x3o, its3, _ = krylov.cg(ref, b, precond=lambda r: r / d, rel_tol=1e-10, max_iters=500)
+    assert abs(rep3.iterations - its3) <= 1
+
+
+def test_fgmres_matches_oracle_and_fixed_iterations():
+    from paper_1910_03032_b200 import mfop, solvers
+    m, sp_, geom = build(2, (6, 5), None, 0.05, 4)
+    op = mfop.HelmholtzOperator(sp_, geom, 1000.0)
+    ref = sumfact.make_square("helmholtz", sp_, geom, c=1000.0)
+    b = np.random.default_rng(8).standard_normal(sp_.ndofs)
+    d = 1000.0 * solvers.collocated_mass_diagonal(sp_)
+    for restart in (50, 7):
+        cfg = solvers.SolverConfig(rel_tol=1e-10, max_iters=400, restart=restart)
+        x, rep = solvers.fgmres(op, b, precond=solvers.DiagonalPreconditioner(d), config=cfg)
+        xo, its = krylov.fgmres(ref, b, precond=lambda r: r / d, rel_tol=1e-10, max_iters=400,
+                                restart=restart)
+        assert rep.converged and its < 400
+        assert abs(rep.iterations - its) <= 1, (restart, rep.iterations, its)
+        assert rel_err(x, xo) < 1e-7
+    # InnerCG: fixed iteration count as a preconditioner (solvers.py:413-425)
+    inner = solvers.InnerCG(op, iterations=3)
+    z = inner.apply(b)
+    zo, its, _ = krylov.cg(ref, b, rel_tol=0.0, max_iters=3)
+    assert rel_err(z, zo) < 1e-10
