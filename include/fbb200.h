@@ -161,6 +161,8 @@ int fb_scalar_div(const double* num_dev, const double* den_dev, double* out_dev,
 /* p = z + beta*p with beta = num/den read on device */
 int fb_xpby_ratio(int64_t n, const double* z_dev, const double* num_dev, const double* den_dev,
                   double* p_dev, void* stream);
+/* y = a * x (a host scalar) */
+int fb_scale(int64_t n, double a, const double* x_dev, double* y_dev, void* stream);
 /* y = x / s (s host scalar; the reference's `r / beta`, fgmres) */
 int fb_div_scalar(int64_t n, const double* x_dev, double s, double* y_dev, void* stream);
 /* y = x - num_dev[0] / den  (mean deflation, solvers.py:60-64) */

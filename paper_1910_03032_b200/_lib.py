@@ -60,6 +60,7 @@ _SIGS = [
     ("fb_xpby_ratio", _int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     ("fb_vmul", _int, [_i64, _vp, _vp, _vp, _vp]),
     ("fb_div_scalar", _int, [_i64, _vp, _dbl, _vp, _vp]),
+    ("fb_scale", _int, [_i64, _dbl, _vp, _vp, _vp]),
     ("fb_shift_ratio", _int, [_i64, _vp, _vp, _dbl, _vp, _vp]),
     ("fb_safe_div", _int, [_vp, _vp, _vp, _vp]),
     ("fb_csr_create", _int, [_i64, _i64, _i64, _vp, _vp, _vp, C.POINTER(_vp)]),

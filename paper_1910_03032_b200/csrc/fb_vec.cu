@@ -99,6 +99,12 @@ __global__ void shift_ratio_kernel(int64_t n, const double* __restrict__ x,
   if (i < n) y[i] = __dsub_rn(x[i], m);
 }
 
+__global__ void scale_kernel(int64_t n, double a, const double* __restrict__ x,
+                             double* __restrict__ y) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __dmul_rn(a, x[i]);
+}
+
 __global__ void safe_div_kernel(const double* num, const double* den, double* out) {
   out[0] = den[0] > 0.0 ? __ddiv_rn(num[0], den[0]) : 0.0;
 }
@@ -192,6 +198,13 @@ int fb_shift_ratio(int64_t n, const double* x, const double* num, double den, do
                    void* stream) {
   if (n <= 0) return FB_OK;
   shift_ratio_kernel<<<ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, x, num, den, y);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+int fb_scale(int64_t n, double a, const double* x, double* y, void* stream) {
+  if (n <= 0) return FB_OK;
+  scale_kernel<<<ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, a, x, y);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }

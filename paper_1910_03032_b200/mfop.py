@@ -410,3 +410,41 @@ def setup(kind, space=None, geom=None, vspace=None, pspace=None, nu=1.0, c=0.0):
     if kind in ("convection", "curlcurl"):
         raise NotImplementedError(f"operator kind {kind!r} is outside the B200 hot path")
     raise ValueError(f"unknown operator kind {kind!r}")
+
+
+# -- right-hand-side formation (host setup; outside the hot path) --------------
+
+def _tensor_t(fq, Bt, d):
+    """(ne, nq^d) -> (ne, n^d): B^T applied along every axis."""
+    ne, q = fq.shape[0], Bt.shape[1]
+    t = fq.reshape((ne,) + (q,) * d)
+    if d == 2:
+        t = np.einsum("ai,eji->eja", Bt, t)
+        t = np.einsum("bj,eja->eba", Bt, t)
+    else:
+        t = np.einsum("ai,ekji->ekja", Bt, t)
+        t = np.einsum("bj,ekja->ekba", Bt, t)
+        t = np.einsum("ck,ekba->ecba", Bt, t)
+    return t.reshape(ne, -1)
+
+
+def load_vector(space, geom, f):
+    """Weak forcing b_i = (f, phi_i) with f sampled at the quadrature points
+    (the reference's load_vector, mfop.py:600-620)."""
+    _check_rule_match(space, geom)
+    B, _ = _eval_matrices(space, np.asarray(geom.rule.points))
+    wdet = geom.detj * geom.w[None, :]
+    xq = geom.xq.reshape(-1, space.dim)
+    vals = np.asarray(f(xq), dtype=np.float64)
+    if vals.ndim == 1:
+        vals = vals[:, None]
+    if vals.shape != (xq.shape[0], space.vdim):
+        raise ValueError(f"forcing returned shape {vals.shape}, expected ({xq.shape[0]}, {space.vdim})")
+    ne, nq = geom.detj.shape
+    ns = space.ndofs_scalar
+    out = np.empty(space.ndofs)
+    for c in range(space.vdim):
+        loc = _tensor_t(vals[:, c].reshape(ne, nq) * wdet, B.T, space.dim)
+        out[c * ns:(c + 1) * ns] = np.bincount(space.element_dofs.ravel(), weights=loc.ravel(),
+                                                minlength=ns)
+    return out

@@ -85,6 +85,12 @@ def xpby_ratio(z, num, den, p, stream=None):
     return p
 
 
+def scale(a, x, y, stream=None):
+    """y = a * x."""
+    _lib.check(_lib.lib.fb_scale(x.shape[0], float(a), x.data_ptr(), y.data_ptr(), _st(stream)))
+    return y
+
+
 def div_scalar(x, s, y, stream=None):
     """y = x / s."""
     _lib.check(_lib.lib.fb_div_scalar(x.shape[0], x.data_ptr(), float(s), y.data_ptr(), _st(stream)))
@@ -104,7 +110,8 @@ def vmul(d, x, y, stream=None):
 
 
 def copy(x, y, stream=None):
-    _lib.check(_lib.lib.fb_axpby(y.shape[0], 1.0, x.data_ptr(), 0.0, y.data_ptr(), _st(stream)))
+    """y = x (a 1.0 * x scale: never reads y, so uninitialised y is fine)."""
+    _lib.check(_lib.lib.fb_scale(x.shape[0], 1.0, x.data_ptr(), y.data_ptr(), _st(stream)))
     return y
 
 

@@ -201,7 +201,46 @@ def make_solvers():
     return {"solvers": manifest}
 
 
-GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers}
+# (name, d, counts, p, alpha_dt)
+STOKES_CASES = [
+    ("cav2d_p2", 2, (8, 8), 2, None),
+    ("cav2d_p4", 2, (8, 8), 4, None),
+    ("cav2d_p6", 2, (8, 8), 6, None),
+    ("cav3d_p2", 3, (3, 3, 3), 2, None),
+    ("cav2d_p3_unsteady", 2, (8, 8), 3, 0.01),
+]
+
+
+def lid(X):
+    d = X.shape[1]
+    out = np.zeros_like(X)
+    out[np.abs(X[:, 1] - 1.0) < 1e-12, 0] = 1.0
+    return out
+
+
+def make_stokes():
+    mesh, fespace, mfop, solvers, _, stokes = ref_modules()
+    out, manifest = {}, []
+    for (name, d, counts, p, adt) in STOKES_CASES:
+        m = mesh.cartesian_mesh(counts)
+        vs = fespace.FESpace(m, p, vdim=d)
+        ps = fespace.FESpace(m, p - 1)
+        geom = mesh.compute_geometric_factors(m, vs.basis.quad)
+        S = stokes.StokesSystem(vs, ps, geom, nu=1.0, alpha_dt=adt)
+        u, pr, rep = S.solve(g=lid, config=solvers.SolverConfig(rel_tol=1e-8, max_iters=200))
+        out[name + "/u"] = u
+        out[name + "/p"] = pr
+        # one application of K and of the block preconditioner
+        x = np.random.default_rng(3).standard_normal(S.K.shape[0])
+        out[name + "/Kx"] = S.K.apply(x)
+        out[name + "/Px"] = S.P.apply(x)
+        manifest.append(dict(name=name, d=d, counts=counts, p=p, alpha_dt=adt,
+                             iterations=rep.iterations))
+    np.savez_compressed(os.path.join(HERE, "stokes.npz"), **out)
+    return {"stokes": manifest}
+
+
+GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers, "stokes": make_stokes}
 
 
 def main(argv):
