@@ -134,13 +134,11 @@ def build_problem(p, target=TARGET_DOFS, seed=1):
 
 # ----------------------------------------------------------------------------- CPU legs
 
-def cpu_sample(threads, reps=1, target=CPU_SAMPLE_DOFS):
-    """Oracle port of the reference apply on ~target DoFs per degree.
-    Returns (GDoF/s, seconds, description)."""
+def cpu_problems(threads, target=CPU_SAMPLE_DOFS):
+    """Oracle-port runners (reference apply restated in numpy) per degree."""
     from oracle import cpu_apply
     from paper_1910_03032_b200 import geometry, spaces
-    tot_dofs = 0
-    tot_t = 0.0
+    out = []
     for p in DEGREES:
         n = mesh_cells(p, target)
         m = geometry.perturb_mesh(geometry.cartesian_mesh((n, n, n)), 0.05, seed=1)
@@ -149,31 +147,52 @@ def cpu_sample(threads, reps=1, target=CPU_SAMPLE_DOFS):
         runner = cpu_apply.HelmholtzCPU(sp, geom, C_HELM, NU, threads=threads)
         x = np.random.default_rng(0).standard_normal(sp.ndofs)
         runner(x)  # warm
+        out.append((runner, x, sp.ndofs))
+    return out
+
+
+def cpu_time(problems, reps=1):
+    tot_dofs, tot_t = 0, 0.0
+    for runner, x, n in problems:
         t0 = time.perf_counter()
         for _ in range(reps):
             runner(x)
         tot_t += time.perf_counter() - t0
-        tot_dofs += reps * sp.ndofs
-        runner.close()
+        tot_dofs += reps * n
+    return tot_dofs / tot_t / 1e9, tot_t
+
+
+def cpu_sample(threads, reps=1, target=CPU_SAMPLE_DOFS):
+    """Returns (GDoF/s, timed seconds, description)."""
+    probs = cpu_problems(threads, target)
+    v, t = cpu_time(probs, reps)
+    for r, _, _ in probs:
+        r.close()
     desc = (f"3D Helmholtz apply, p=1..8, ~{target/1e3:.0f}k DoFs per degree "
-            f"(perturbed cube), {reps} timed rep(s) after 1 warm-up, oracle numpy port")
-    return tot_dofs / tot_t / 1e9, tot_t, desc
+            f"(perturbed cube), {reps} timed rep(s) after 1 warm-up, oracle numpy port, "
+            f"{threads} thread(s)")
+    return v, t, desc
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    vals = []
+    probs = cpu_problems(threads)
     for _ in range(args.warmup):
-        cpu_sample(threads, reps=1)
-    desc = ""
+        cpu_time(probs)
+    vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, _, desc = cpu_sample(threads, reps=1)
+        v, _ = cpu_time(probs)
         vals.append(v)
     el = time.perf_counter() - t0
+    for r, _, _ in probs:
+        r.close()
     value = float(np.mean(vals))
+    desc = (f"3D Helmholtz apply, p=1..8, ~{CPU_SAMPLE_DOFS/1e3:.0f}k DoFs per degree "
+            f"(perturbed cube), one apply per degree per step, oracle numpy port of the "
+            f"reference contractions on {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -186,6 +205,44 @@ def run_reference(args, rank, world):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def lor_pcg(cases=((4, 25), (7, 14)), c=C_HELM):
+    """LOR-preconditioned CG time-to-solve, 3D Helmholtz (cfg3 shape at ~1M
+    DoFs): device operator + device V-cycle, rel_tol 1e-8."""
+    import torch
+    from paper_1910_03032_b200 import geometry, mfop, solvers, spaces
+    out = {}
+    for p, n in cases:
+        t0 = time.perf_counter()
+        m = geometry.cartesian_mesh((n, n, n))
+        sp = spaces.FESpace(m, p)
+        geom = geometry.DeviceGeometry(m, sp.basis.quad)
+        op = mfop.HelmholtzOperator(sp, geom, c)
+        bdr = sp.boundary_dof_set()
+        A = mfop.ConstrainedOperator(op, bdr)
+        pre = solvers.LORPreconditioner(sp, "helmholtz", c=c, dirichlet_attrs="all")
+        setup = time.perf_counter() - t0
+        b = np.random.default_rng(0).standard_normal(sp.ndofs)
+        b[bdr] = 0.0
+        bd = torch.from_numpy(b).cuda()
+        cfg = solvers.SolverConfig(rel_tol=1e-8, max_iters=300)
+        solvers.cg(A, bd, precond=pre, config=cfg)  # warm
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x, rep = solvers.cg(A, bd, precond=pre, config=cfg)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        out[f"p{p}_{n}^3"] = {"dofs": sp.ndofs, "iterations": rep.iterations,
+                              "converged": rep.converged, "solve_ms": round(ms, 2),
+                              "ms_per_iteration": round(ms / max(rep.iterations, 1), 3),
+                              "host_setup_s": round(setup, 2),
+                              "reference_cpu_solve_s": {4: 41.7, 7: 53.0}.get(p),
+                              "reference_iterations": {4: 30, 7: 36}.get(p)}
+    return out
 
 
 METRIC = "fp64 GDoF/s of sum-factorized Helmholtz apply vs p (3D, p=1..8, ~10M DoFs each)"
@@ -223,17 +280,20 @@ def run_ours(args, rank, world):
             if timed_events is not None:
                 timed_events[i][1].record(st)
 
-    for _ in range(args.warmup):
+    clocks = ClockSampler(local)
+    clocks.start()
+    tw = time.perf_counter()
+    nw = 0
+    while nw < args.warmup or time.perf_counter() - tw < 1.0:  # >= W warm-up steps, >= 1 s loaded
         step()
-    torch.cuda.synchronize()
+        nw += 1
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in probs] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
-    clocks.start()
     l0 = _lib.lib.fb_launch_count()
     torch.cuda.synchronize()
     t_start.record(st)
@@ -333,7 +393,10 @@ def run_ours(args, rank, world):
                         "inside the timed region"},
         "gpu_launches": int(launches),
         "clocks": clk,
+        "warmup_steps_run": nw,
     }
+    if not args.no_pcg:
+        line["lor_pcg"] = lor_pcg()
     if not args.no_cpu:
         v, secs, desc = cpu_sample(1, reps=3)
         line["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": 1, "kind": "port",
@@ -348,6 +411,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pcg", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
