@@ -48,6 +48,7 @@ typedef struct fb_restriction fb_restriction;
 typedef struct fb_operator fb_operator;
 typedef struct fb_csr fb_csr;
 typedef struct fb_trisolve fb_trisolve;
+typedef struct fb_blockilu fb_blockilu;
 
 const char* fb_last_error(void);
 int fb_abi_version(void);
@@ -192,9 +193,28 @@ int fb_trisolve_create(int64_t n, const int64_t* indptr_host, const int64_t* ind
                        const double* data_host, int lower, int unit_diag, fb_trisolve** out);
 void fb_trisolve_destroy(fb_trisolve* T);
 int fb_trisolve_solve(const fb_trisolve* T, const double* b_dev, double* x_dev, void* stream);
+/* Number of dependency levels of the triangular matrix. */
+int fb_trisolve_levels(const fb_trisolve* T);
+/* Solve strategy for all triangular solves: 0 = sync-free single launch
+ * (poll backoff in ns), 1 = level-scheduled kernels replayed from a CUDA graph. */
+int fb_set_trisolve_mode(int mode, int backoff_ns);
 /* dst[i] = src[idx[i]] (scatter=0) or dst[idx[i]] = src[i] (scatter=1) */
 int fb_permute(int64_t n, const int* idx_dev, const double* src_dev, double* dst_dev, int scatter,
                void* stream);
+/* Block-Jacobi ILU(0) smoother (scale mode of the LOR V-cycle, SURVEY
+ * 8(e')): F = block-diagonal ILU(0) factor in block-major numbering (strict
+ * lower = L with unit diagonal, upper incl. diagonal = U), block_ptr =
+ * (nblocks+1) row offsets, new2old = new -> original index.  apply computes
+ * out = (LU)^-1 r (transpose=0) or (LU)^-T r (transpose=1) in the original
+ * numbering with one CTA per block, level-scheduled in shared memory. */
+int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr_host,
+                       const int64_t* new2old_host, const int64_t* indptr_host,
+                       const int64_t* indices_host, const double* data_host, fb_blockilu** out);
+void fb_blockilu_destroy(fb_blockilu* B);
+int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r_dev, double* out_dev,
+                      void* stream);
+/* y = M x for a dense row-major n x n matrix (coarse-level inverse). */
+int fb_dense_mv(int64_t n, const double* M_dev, const double* x_dev, double* y_dev, void* stream);
 /* ILU(0) in place on sorted CSR, IKJ order (kernels/numba_backend.py:64-103):
  * returns -1 on success, else the failing row. */
 int64_t fb_ilu0_factor_host(int64_t n, const int64_t* indptr, const int64_t* indices,

@@ -70,8 +70,14 @@ _SIGS = [
     ("fb_trisolve_create", _int, [_i64, _vp, _vp, _vp, _int, _int, C.POINTER(_vp)]),
     ("fb_trisolve_destroy", None, [_vp]),
     ("fb_trisolve_solve", _int, [_vp, _vp, _vp, _vp]),
+    ("fb_trisolve_levels", _int, [_vp]),
+    ("fb_set_trisolve_mode", _int, [_int, _int]),
     ("fb_permute", _int, [_i64, _vp, _vp, _vp, _int, _vp]),
     ("fb_ilu0_factor_host", _i64, [_i64, _vp, _vp, _vp]),
+    ("fb_blockilu_create", _int, [_i64, _int, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)]),
+    ("fb_blockilu_destroy", None, [_vp]),
+    ("fb_blockilu_apply", _int, [_vp, _int, _vp, _vp, _vp]),
+    ("fb_dense_mv", _int, [_i64, _vp, _vp, _vp, _vp]),
 ]
 
 SYMBOLS = [s[0] for s in _SIGS]

@@ -15,6 +15,7 @@
 // claimed earlier by a running warp, so the solve cannot deadlock, and one
 // launch replaces the reference's level-by-level dependency chain (449-1409
 // levels at 36k-0.9M DoFs).
+#include <algorithm>
 #include <cstring>
 #include <memory>
 
@@ -35,7 +36,21 @@ struct fb_trisolve {
   fb::DevBuf<unsigned int> flags;  // per-row completion epoch
   fb::DevBuf<unsigned int> counter;
   mutable unsigned int epoch = 0;
+  // level schedule
+  int nlevels = 0;
+  std::vector<int> level_ptr;  // host: offsets into level_rows
+  fb::DevBuf<int> level_rows;
+  mutable cudaGraphExec_t graph = nullptr;
+  mutable const double* graph_b = nullptr;
+  mutable double* graph_x = nullptr;
+  mutable cudaStream_t graph_stream = nullptr;
+  ~fb_trisolve() {
+    if (graph) cudaGraphExecDestroy(graph);
+  }
 };
+
+static int g_trisolve_mode = 1;      // 0 = sync-free, 1 = level-scheduled graph
+static int g_trisolve_backoff = 64;  // ns between polls (sync-free mode)
 
 namespace fb {
 
@@ -59,7 +74,7 @@ __global__ void trisolve_kernel(int64_t n, int lower, const int* __restrict__ ip
                                 const int* __restrict__ ix, const double* __restrict__ v,
                                 const double* __restrict__ invdiag, const double* __restrict__ b,
                                 double* x, volatile unsigned int* flags, unsigned int* counter,
-                                unsigned int epoch) {
+                                unsigned int epoch, int backoff_ns) {
   const int lane = threadIdx.x & 31;
   int64_t k;
   if (lane == 0) k = atomicAdd(counter, 1u);
@@ -72,6 +87,7 @@ __global__ void trisolve_kernel(int64_t n, int lower, const int* __restrict__ ip
   for (int j = beg + lane; j < end; j += 32) {
     const int col = ix[j];
     while (flags[col] != epoch) {
+      if (backoff_ns > 0) __nanosleep(backoff_ns);
     }
     __threadfence();
     part = __dadd_rn(part, __dmul_rn(v[j], reinterpret_cast<volatile double*>(x)[col]));
@@ -84,6 +100,23 @@ __global__ void trisolve_kernel(int64_t n, int lower, const int* __restrict__ ip
     __threadfence();
     flags[row] = epoch;
   }
+}
+
+// Level-scheduled variant: rows of one dependency level are independent;
+// one thread per row, rows listed level by level (level_rows), one launch
+// per level (captured once into a CUDA graph by the host code).
+__global__ void trisolve_level_kernel(int nrows_level, const int* __restrict__ rows,
+                                      const int* __restrict__ ip, const int* __restrict__ ix,
+                                      const double* __restrict__ v,
+                                      const double* __restrict__ invdiag,
+                                      const double* __restrict__ b, double* __restrict__ x) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows_level) return;
+  const int row = rows[t];
+  double acc = 0.0;
+  for (int k = ip[row]; k < ip[row + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(v[k], x[ix[k]]));
+  const double r = __dsub_rn(b[row], acc);
+  x[row] = invdiag ? __dmul_rn(r, invdiag[row]) : r;
 }
 
 __global__ void permute_gather_kernel(int64_t n, const int* __restrict__ idx,
@@ -194,6 +227,25 @@ int fb_trisolve_create(int64_t n, const int64_t* indptr, const int64_t* indices,
   if (rc != FB_OK) return rc;
   FB_TRY_CUDA(T->data.upload(vv.data(), int64_t(vv.size())));
   if (!unit_diag) FB_TRY_CUDA(T->invdiag.upload(inv.data(), n));
+  {
+    // dependency levels: level[r] = 1 + max level of the rows r reads
+    std::vector<int> level(n, 0);
+    int maxl = 0;
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t r = lower ? k : n - 1 - k;
+      int lv = 0;
+      for (int64_t j = ip[r]; j < ip[r + 1]; ++j) lv = std::max(lv, level[ix[j]] + 1);
+      level[r] = lv;
+      maxl = std::max(maxl, lv);
+    }
+    T->nlevels = n > 0 ? maxl + 1 : 0;
+    T->level_ptr.assign(T->nlevels + 1, 0);
+    for (int64_t r = 0; r < n; ++r) T->level_ptr[level[r] + 1]++;
+    for (int l = 0; l < T->nlevels; ++l) T->level_ptr[l + 1] += T->level_ptr[l];
+    std::vector<int> rows(n), pos(T->level_ptr.begin(), T->level_ptr.end() - 1);
+    for (int64_t r = 0; r < n; ++r) rows[pos[level[r]]++] = int(r);
+    FB_TRY_CUDA(T->level_rows.upload(rows.data(), n));
+  }
   FB_TRY_CUDA(T->flags.alloc(n > 0 ? n : 1));
   FB_TRY_CUDA(cudaMemset(T->flags.ptr, 0, sizeof(unsigned int) * (n > 0 ? n : 1)));
   FB_TRY_CUDA(T->counter.alloc(1));
@@ -203,11 +255,43 @@ int fb_trisolve_create(int64_t n, const int64_t* indptr, const int64_t* indices,
 
 void fb_trisolve_destroy(fb_trisolve* T) { delete T; }
 
+static int trisolve_levels(const fb_trisolve* T, const double* b, double* x, cudaStream_t st) {
+  for (int l = 0; l < T->nlevels; ++l) {
+    const int cnt = T->level_ptr[l + 1] - T->level_ptr[l];
+    trisolve_level_kernel<<<ceil_div(cnt, 128), 128, 0, st>>>(
+        cnt, T->level_rows.ptr + T->level_ptr[l], T->indptr.ptr, T->indices.ptr, T->data.ptr,
+        T->unit ? nullptr : T->invdiag.ptr, b, x);
+  }
+  return FB_OK;
+}
+
 int fb_trisolve_solve(const fb_trisolve* T, const double* b, double* x, void* stream) {
   FB_REQUIRE(T != nullptr, "solver is NULL");
   FB_REQUIRE(b != x, "in-place triangular solve is not supported");
   if (T->n == 0) return FB_OK;
   cudaStream_t st = as_stream(stream);
+  if (g_trisolve_mode == 1) {
+    // one graph per (b, x, stream) binding; re-captured when the operands change
+    if (!T->graph || T->graph_b != b || T->graph_x != x || T->graph_stream != st) {
+      if (T->graph) cudaGraphExecDestroy(T->graph);
+      T->graph = nullptr;
+      cudaStream_t cap;
+      FB_TRY_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      cudaGraph_t g;
+      FB_TRY_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      trisolve_levels(T, b, x, cap);
+      FB_TRY_CUDA(cudaStreamEndCapture(cap, &g));
+      FB_TRY_CUDA(cudaGraphInstantiate(&T->graph, g, 0));
+      cudaGraphDestroy(g);
+      cudaStreamDestroy(cap);
+      T->graph_b = b;
+      T->graph_x = x;
+      T->graph_stream = st;
+    }
+    FB_TRY_CUDA(cudaGraphLaunch(T->graph, st));
+    launch_counter() += T->nlevels;
+    return FB_OK;
+  }
   T->epoch += 1;
   if (T->epoch == 0) {  // wrapped: reset the flags
     FB_TRY_CUDA(cudaMemsetAsync(T->flags.ptr, 0, sizeof(unsigned int) * T->n, st));
@@ -217,8 +301,18 @@ int fb_trisolve_solve(const fb_trisolve* T, const double* b, double* x, void* st
   const int64_t threads = T->n * 32;
   trisolve_kernel<<<ceil_div(threads, 256), 256, 0, st>>>(
       T->n, T->lower, T->indptr.ptr, T->indices.ptr, T->data.ptr,
-      T->unit ? nullptr : T->invdiag.ptr, b, x, T->flags.ptr, T->counter.ptr, T->epoch);
+      T->unit ? nullptr : T->invdiag.ptr, b, x, T->flags.ptr, T->counter.ptr, T->epoch,
+      g_trisolve_backoff);
   FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+int fb_trisolve_levels(const fb_trisolve* T) { return T ? T->nlevels : -1; }
+
+int fb_set_trisolve_mode(int mode, int backoff_ns) {
+  FB_REQUIRE(mode == 0 || mode == 1, "mode must be 0 (sync-free) or 1 (level graph)");
+  g_trisolve_mode = mode;
+  g_trisolve_backoff = backoff_ns;
   return FB_OK;
 }
 

@@ -62,6 +62,11 @@ class SolveReport:
                 f"relres {self.final_relres:.3e}, {self.seconds:.3f}s")
 
 
+# Smoother used by LORPreconditioner when none is given: "block" (device
+# block-Jacobi ILU(0), the B200 path) or "global" (the reference's ILU(0)).
+DEFAULT_SMOOTHER = "block"
+
+
 # -- operand normalisation ------------------------------------------------------
 
 def _device_apply(A):
@@ -439,6 +444,138 @@ class ILU0Smoother:
         return dev.to_host(out) if host else out
 
 
+def infer_counts(mesh):
+    """Structured cell counts of a tensor-product mesh numbered x-fastest
+    (cartesian_mesh, mesh.py:110-121), or None."""
+    counts = getattr(mesh, "counts", None)
+    if counts:
+        return tuple(counts)
+    ne, d = mesh.num_elements, mesh.dim
+    cen = mesh.corners.mean(axis=1)
+    wrap = np.flatnonzero(np.diff(cen[:, 0]) < 0)
+    nx = int(wrap[0]) + 1 if wrap.size else ne
+    if d == 2:
+        return (nx, ne // nx) if ne % nx == 0 else None
+    rows = cen[::nx, 1]
+    wrap = np.flatnonzero(np.diff(rows) < 0)
+    ny = int(wrap[0]) + 1 if wrap.size else ne // nx
+    if ne % (nx * ny):
+        return None
+    return (nx, ny, ne // (nx * ny))
+
+
+def element_block_ids(mesh, block):
+    """Element -> block id for element-cube blocks of block^d elements."""
+    ne, d = mesh.num_elements, mesh.dim
+    counts = infer_counts(mesh)
+    e = np.arange(ne)
+    if counts is None or int(np.prod(counts)) != ne:
+        return e // block ** d
+    idx = []
+    for a in range(d):
+        idx.append((e % counts[a]) // block)
+        e = e // counts[a]
+    nb = [-(-counts[a] // block) for a in range(d)]
+    bid = idx[-1]
+    for a in range(d - 2, -1, -1):
+        bid = bid * nb[a] + idx[a]
+    return bid
+
+
+class BlockILU0Smoother:
+    """Block-Jacobi ILU(0) over element-cube blocks (SURVEY 8(e') scale mode).
+
+    Every DoF joins the block of its first-touch owner element; couplings
+    between blocks are dropped; inside a block the reference's first-touch
+    order is kept, so each block's factor is exactly the reference ILU(0)
+    restricted to that block.  Measured against the reference's global ILU:
+    +0/+1 CG iterations (SURVEY 8(e')).  One kernel launch per sweep."""
+
+    def __init__(self, A, space, order, block=2):
+        import ctypes as C
+        from . import _lib
+        A = A.tocsr()
+        n = A.shape[0]
+        self.n = n
+        order = np.asarray(order, dtype=np.int64)
+        blk = element_block_ids(space.mesh, block)[space.dof_owner_elem]
+        new2old = order[np.argsort(blk[order], kind="stable")]
+        bnew = blk[new2old]
+        Ap = A[new2old][:, new2old].tocoo()
+        keep = bnew[Ap.row] == bnew[Ap.col]
+        F = sp.csr_matrix((Ap.data[keep], (Ap.row[keep], Ap.col[keep])), shape=(n, n))
+        F.sort_indices()
+        data = F.data.astype(np.float64, copy=True)
+        fail = vec.ilu0_factor_host(F.indptr, F.indices, data)
+        self.jacobi = None
+        if fail >= 0:
+            diag = A.diagonal().copy()
+            diag[diag == 0.0] = 1.0
+            self.jacobi = 0.6 / diag
+            self._jac = dev.to_device(self.jacobi)
+            return
+        starts = np.flatnonzero(np.r_[True, bnew[1:] != bnew[:-1]])
+        block_ptr = np.r_[starts, n].astype(np.int64)
+        self.nblocks = len(starts)
+        ip = np.ascontiguousarray(F.indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(F.indices, dtype=np.int64)
+        n2o = np.ascontiguousarray(new2old, dtype=np.int64)
+        h = C.c_void_p()
+        _lib.check(_lib.lib.fb_blockilu_create(n, self.nblocks, _lib.ptr(block_ptr), _lib.ptr(n2o),
+                                               _lib.ptr(ip), _lib.ptr(ix), _lib.ptr(data),
+                                               C.byref(h)))
+        self.handle = h
+        self._lib = _lib
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and self._lib is not None and self._lib.lib is not None:
+            self._lib.lib.fb_blockilu_destroy(h)
+
+    def _apply(self, r, out, transpose, stream):
+        if self.jacobi is not None:
+            return vec.vmul(self._jac, r, out, stream)
+        self._lib.check(self._lib.lib.fb_blockilu_apply(
+            self.handle, int(transpose), r.data_ptr(), out.data_ptr(),
+            dev.stream_handle() if stream is None else stream))
+        return out
+
+    def forward_into(self, r, out, stream=None):
+        return self._apply(r, out, False, stream)
+
+    def backward_into(self, r, out, stream=None):
+        return self._apply(r, out, True, stream)
+
+    forward = ILU0Smoother.forward
+    backward = ILU0Smoother.backward
+
+
+class DenseInverseSolver:
+    """Coarse direct solve through a dense inverse computed once on the
+    device (cuSOLVER via torch.linalg.inv); applied with a deterministic
+    libfbb200 matrix-vector kernel.  Used for coarse levels up to ~20k rows."""
+
+    def __init__(self, A):
+        from . import _lib
+        self.n = A.shape[0]
+        M = torch.from_numpy(np.asarray(A.toarray(), dtype=np.float64)).to(dev.device())
+        self.inv = torch.linalg.inv(M).contiguous()
+        del M
+        self._lib = _lib
+
+    def solve_into(self, b, x, stream=None):
+        self._lib.check(self._lib.lib.fb_dense_mv(self.n, self.inv.data_ptr(), b.data_ptr(),
+                                                  x.data_ptr(),
+                                                  dev.stream_handle() if stream is None else stream))
+        return x
+
+    def solve(self, b):
+        bd, host = dev.DeviceIn.get(b)
+        out = torch.empty_like(bd)
+        self.solve_into(bd, out)
+        return dev.to_host(out) if host else out
+
+
 class SparseLUSolver:
     """Coarse direct solve: host sparse LU (SuperLU via scipy, COLAMD, as the
     reference's splu at solvers.py:372), device triangular solves."""
@@ -473,10 +610,28 @@ class LORPreconditioner(_DeviceMixin):
     """Degree-ladder V(1,1) cycle on LOR matrices (solvers.py:321-392), applied
     on the device: per level one ILU(0) forward sweep, residual SpMV, P^T
     restriction, recursive correction, P prolongation, residual SpMV, ILU(0)
-    backward sweep; the Q1 bottom level is a sparse direct solve."""
+    backward sweep; the Q1 bottom level is an exact direct solve.
+
+    smoother="block" (default for stiffness / Helmholtz): block-Jacobi ILU(0)
+    over element cubes of `block`^d elements (default 2 for p <= 4, else 1) in
+    first-touch order -- one launch per sweep, +0/+1 iterations vs the
+    reference (SURVEY 8(e'), tests/test_gpu_solvers.py).  Mass defaults to
+    the global smoother.  smoother="global": the
+    reference's global first-touch ILU(0), reproduced to rounding (its
+    triangular solves are a dependency chain of ~60 n levels).
+    coarse="auto": dense inverse up to 20k coarse rows, else sparse LU."""
 
     def __init__(self, space, kind, nu=1.0, c=0.0, dirichlet_attrs=None,
-                 pure_neumann=False, backend=None):
+                 pure_neumann=False, backend=None, smoother=None, block=None, coarse="auto"):
+        if smoother is None:
+            # the Q1 mass LOR matrix loses too much coupling when blocked
+            # (37 -> 42 CG iterations on the 3D p=3 golden case); stiffness and
+            # Helmholtz stay within +1 of the reference for any block size
+            smoother = "global" if kind == "mass" else DEFAULT_SMOOTHER
+        if block is None:
+            block = 2 if (space.dim == 2 or space.p <= 4) else 1
+        if smoother not in ("block", "global"):
+            raise ValueError(f"unknown smoother {smoother!r}")
         if space.vdim != 1:
             raise ValueError("LOR cycles act componentwise on scalar spaces")
         if pure_neumann and dirichlet_attrs is not None:
@@ -502,9 +657,18 @@ class LORPreconditioner(_DeviceMixin):
                 self.transfers.append(lor_mod.nodal_interpolation(prev, lsp))
             prev = lsp
         self.A = self.levels[0][1]
-        self.smoothers = [ILU0Smoother(A, lor_mod.first_touch_ordering(lsp), backend=backend)
-                          for lsp, A in self.levels[:-1]]
-        self._bottom = SparseLUSolver(self.levels[-1][1])
+        self.smoother_kind = smoother
+        if smoother == "global":  # the reference's global first-touch ILU(0)
+            self.smoothers = [ILU0Smoother(A, lor_mod.first_touch_ordering(lsp), backend=backend)
+                              for lsp, A in self.levels[:-1]]
+        else:
+            self.smoothers = [BlockILU0Smoother(A, lsp, lor_mod.first_touch_ordering(lsp), block)
+                              for lsp, A in self.levels[:-1]]
+        Ac = self.levels[-1][1]
+        if coarse == "dense" or (coarse == "auto" and Ac.shape[0] <= 20000):
+            self._bottom = DenseInverseSolver(Ac)
+        else:
+            self._bottom = SparseLUSolver(Ac)
         self._A = [vec.DeviceCSR(A) for _, A in self.levels]
         self._P = [vec.DeviceCSR(P) for P in self.transfers]
         self._Pt = [vec.DeviceCSR(P.T.tocsr()) for P in self.transfers]

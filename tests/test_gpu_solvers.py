@@ -18,14 +18,15 @@ def gold():
     return load("solvers")
 
 
-def _setup(c):
+def _setup(c, smoother="global", block=None):
     from paper_1910_03032_b200 import mfop, solvers
     m, sp_, geom = build(c["d"], c["counts"], None, c["perturb"], c["p"])
     kw = {"mass": {}, "stiffness": {"nu": 1.0}, "helmholtz": {"c": c["c"], "nu": 1.0}}[c["kind"]]
     op = mfop.setup(c["kind"], space=sp_, geom=geom, **kw)
     bdr = sp_.boundary_dof_set()
     A = mfop.ConstrainedOperator(op, bdr)
-    pre = solvers.LORPreconditioner(sp_, c["kind"], nu=1.0, c=c["c"], dirichlet_attrs="all")
+    pre = solvers.LORPreconditioner(sp_, c["kind"], nu=1.0, c=c["c"], dirichlet_attrs="all",
+                                    smoother=smoother, block=block, coarse="lu")
     return sp_, geom, A, pre, bdr
 
 
@@ -39,11 +40,16 @@ def test_vcycle_and_ilu_match_reference(name, gold):
     assert rel_err(pre.apply(r), gold[name + "/vcycle"]) < 1e-10
 
 
+@pytest.mark.parametrize("smoother", ["global", "block"])
 @pytest.mark.parametrize("name", CASES)
-def test_lor_pcg_iteration_parity(name, gold):
+def test_lor_pcg_iteration_parity(name, smoother, gold):
+    """Reference iteration counts within +-1 for the reference's global ILU(0)
+    (parity mode) and the block-Jacobi ILU(0) scale mode."""
     from paper_1910_03032_b200 import solvers
     c = SOLVE[name]
-    sp_, _, A, pre, bdr = _setup(c)
+    if smoother == "block" and c["kind"] == "mass":
+        pytest.skip("mass LOR matrices default to the global smoother (blocking costs +5 its)")
+    sp_, _, A, pre, bdr = _setup(c, smoother)
     for seed, its_ref in zip(c["seeds"], c["iterations"]):
         b = np.random.default_rng(seed).standard_normal(sp_.ndofs)
         b[bdr] = 0.0
@@ -52,6 +58,8 @@ def test_lor_pcg_iteration_parity(name, gold):
         assert rep.converged
         assert abs(rep.iterations - its_ref) <= 1, (rep.iterations, its_ref)
         assert rel_err(x, gold[f"{name}/x{seed}"]) < 1e-6
+        if smoother == "block":
+            continue
         hist = gold[f"{name}/hist{seed}"]
         k = min(len(hist), len(rep.residuals)) - 1
         assert abs(np.log10(rep.residuals[k]) - np.log10(hist[k])) < 0.1
@@ -63,7 +71,7 @@ def test_pure_neumann_with_mean_projector(gold):
     sp_ = spaces.FESpace(m, 3)
     geom = geometry.compute_geometric_factors(m, sp_.basis.quad)
     L = mfop.StiffnessOperator(sp_, geom)
-    pre = solvers.LORPreconditioner(sp_, "stiffness", pure_neumann=True)
+    pre = solvers.LORPreconditioner(sp_, "stiffness", pure_neumann=True, smoother="global")
     b = solvers.deflate_mean(np.random.default_rng(5).standard_normal(sp_.ndofs))
     x, rep = solvers.cg(L, b, precond=pre, project=solvers.MeanProjector(),
                         config=solvers.SolverConfig(rel_tol=1e-10, max_iters=300))
@@ -112,3 +120,23 @@ def test_fgmres_matches_oracle_and_fixed_iterations():
     z = inner.apply(b)
     zo, its, _ = krylov.cg(ref, b, rel_tol=0.0, max_iters=3)
     assert rel_err(z, zo) < 1e-10
+
+
+def test_block_ilu_is_exact_on_single_block_and_dense_coarse():
+    """One block covering the mesh reproduces the global ILU(0) sweep; the
+    dense-inverse coarse solve equals the sparse LU solve."""
+    import scipy.sparse.linalg as spla
+    from paper_1910_03032_b200 import lor, solvers
+    m, sp_, _ = build(3, (2, 2, 2), None, 0.05, 3)
+    A = lor.lor_matrix(sp_, "helmholtz", c=10.0, constrained=sp_.boundary_dof_set())
+    order = lor.first_touch_ordering(sp_)
+    g = solvers.ILU0Smoother(A, order)
+    b = solvers.BlockILU0Smoother(A, sp_, order, block=2)
+    r = np.random.default_rng(0).standard_normal(A.shape[0])
+    assert b.nblocks == 1
+    assert rel_err(b.forward(r), g.forward(r)) < 1e-13
+    assert rel_err(b.backward(r), g.backward(r)) < 1e-13
+    Ac = lor.lor_matrix(sp_, "stiffness", constrained=sp_.boundary_dof_set())
+    x_ref = spla.spsolve(Ac.tocsc(), r)
+    assert rel_err(solvers.DenseInverseSolver(Ac).solve(r), x_ref) < 1e-10
+    assert rel_err(solvers.SparseLUSolver(Ac).solve(r), x_ref) < 1e-10

@@ -22,9 +22,11 @@ def gold():
     return load("stokes")
 
 
+@pytest.mark.parametrize("smoother", ["global", "block"])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_lid_cavity_matches_reference(name, gold):
+def test_lid_cavity_matches_reference(name, smoother, gold, monkeypatch):
     from paper_1910_03032_b200 import geometry, solvers, spaces, stokes
+    monkeypatch.setattr(solvers, "DEFAULT_SMOOTHER", smoother)
     c = CASES[name]
     m = geometry.cartesian_mesh(tuple(c["counts"]))
     vs = spaces.FESpace(m, c["p"], vdim=c["d"])
@@ -33,7 +35,8 @@ def test_lid_cavity_matches_reference(name, gold):
     S = stokes.StokesSystem(vs, ps, geom, nu=1.0, alpha_dt=c["alpha_dt"])
     x = np.random.default_rng(3).standard_normal(S.K.shape[0])
     assert rel_err(S.K.apply(x), gold[name + "/Kx"]) < 1e-12
-    assert rel_err(S.P.apply(x), gold[name + "/Px"]) < 1e-9
+    if smoother == "global":  # the reference's cycle, reproduced to rounding
+        assert rel_err(S.P.apply(x), gold[name + "/Px"]) < 1e-9
     u, p, rep = S.solve(g=lid, config=solvers.SolverConfig(rel_tol=1e-8, max_iters=200))
     assert rep.converged
     assert abs(rep.iterations - c["iterations"]) <= 1, (rep.iterations, c["iterations"])
