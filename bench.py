@@ -119,17 +119,26 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- problems
 
-def build_problem(p, target=TARGET_DOFS, seed=1):
-    from paper_1910_03032_b200 import geometry, mfop, spaces
+def build_problem(p, target=TARGET_DOFS, seed=1, rank=0, world=1):
+    """One degree's problem.  world > 1: this rank's z-slab (n x n x n
+    elements) of an n x n x (world*n) box, with a cut-plane halo exchange
+    (weak scaling: ~target DoFs per GPU)."""
+    from paper_1910_03032_b200 import geometry, mfop, partition, spaces
     n = mesh_cells(p, target)
-    m = geometry.perturb_mesh(geometry.cartesian_mesh((n, n, n)), 0.05, seed=seed)
-    sp = spaces.FESpace(m, p)
+    halo = None
+    if world == 1:
+        m = geometry.perturb_mesh(geometry.cartesian_mesh((n, n, n)), 0.05, seed=seed)
+        sp = spaces.FESpace(m, p)
+    else:
+        slab = partition.StructuredSlab((n, n), n, p, rank, world, perturb=0.05, seed=seed)
+        m, sp = slab.mesh, slab.space
+        halo = partition.HaloExchange(slab, device="cuda")
     g = geometry.DeviceGeometry(m, sp.basis.quad)
     op = mfop.HelmholtzOperator(sp, g, C_HELM, nu=NU)
     ne = m.num_elements
     N = sp.ndofs
     del m
-    return dict(p=p, n=n, ne=ne, N=N, op=op)
+    return dict(p=p, n=n, ne=ne, N=N, op=op, halo=halo)
 
 
 # ----------------------------------------------------------------------------- CPU legs
@@ -252,7 +261,8 @@ def config_block(world):
     return {"workload": "cfg2-shape 3D Helmholtz apply sweep p=1..8, ~10M DoFs per degree, "
                         "perturbed unit-cube hex mesh, n_q=p+2 Gauss-Legendre, stored factors",
             "c": C_HELM, "nu": NU, "degrees": DEGREES, "target_dofs_per_degree": TARGET_DOFS,
-            "parallelism": f"replica x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"z-slab x{world} (weak scaling: n x n x n elements per GPU, "
+                            f"NCCL cut-plane halo sum per apply)") if world > 1 else "single GPU",
             "l2_policy": "per-apply working set >= 1 GB (factors) >> 126 MB L2; no flush needed"}
 
 
@@ -265,7 +275,7 @@ def run_ours(args, rank, world):
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    probs = [build_problem(p) for p in DEGREES]
+    probs = [build_problem(p, rank=rank, world=world) for p in DEGREES]
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     for pr in probs:
         pr["x"] = torch.randn(pr["N"], dtype=torch.float64, device="cuda", generator=gen)
@@ -277,6 +287,8 @@ def run_ours(args, rank, world):
             if timed_events is not None:
                 timed_events[i][0].record(st)
             pr["op"].apply_into(pr["x"], pr["y"])
+            if pr["halo"] is not None:
+                pr["halo"].sum(pr["y"])
             if timed_events is not None:
                 timed_events[i][1].record(st)
 
@@ -337,6 +349,8 @@ def run_ours(args, rank, world):
         for i, pr in enumerate(probs):
             pr["x"].copy_(hx[i], non_blocking=True)
             pr["op"].apply_into(pr["x"], pr["y"])
+            if pr["halo"] is not None:
+                pr["halo"].sum(pr["y"])
             hy[i].copy_(pr["y"], non_blocking=True)
 
     e2e_step()
@@ -395,7 +409,7 @@ def run_ours(args, rank, world):
         "clocks": clk,
         "warmup_steps_run": nw,
     }
-    if not args.no_pcg:
+    if not args.no_pcg and world == 1:
         line["lor_pcg"] = lor_pcg()
     if not args.no_cpu:
         v, secs, desc = cpu_sample(1, reps=3)
