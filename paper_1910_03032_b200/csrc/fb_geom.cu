@@ -21,6 +21,7 @@ struct GeomParams {
   int64_t ne;
   int dim, nq, kind, nfac;
   int64_t fstride;
+  int lanes;  // 0: element-blocked; 32: [ne/32][K][nq][32] interleaved
   double c, nu;
   double pts[32];
   double w1[32];
@@ -82,10 +83,13 @@ __global__ void factor_kernel(const __grid_constant__ GeomParams P) {
   double w = 1.0;
   for (int a = d - 1; a >= 0; --a) w = __dmul_rn(w, P.w1[qi[a]]);
   const double wdet = __dmul_rn(detj, w);
-  double* out = P.fac + e * P.fstride + q;
+  const int64_t kstride = P.lanes ? int64_t(nqd) * P.lanes : nqd;
+  double* out = P.lanes ? P.fac + (e / P.lanes) * P.nfac * kstride + int64_t(q) * P.lanes +
+                              (e % P.lanes)
+                        : P.fac + e * P.fstride + q;
   int k = 0;
   if (P.kind == FB_MASS || P.kind == FB_HELMHOLTZ) {
-    out[int64_t(k++) * nqd] = P.kind == FB_HELMHOLTZ ? __dmul_rn(P.c, wdet) : wdet;
+    out[int64_t(k++) * kstride] = P.kind == FB_HELMHOLTZ ? __dmul_rn(P.c, wdet) : wdet;
   }
   if (P.kind == FB_STIFFNESS || P.kind == FB_HELMHOLTZ) {
     const double nw = __dmul_rn(P.nu, wdet);
@@ -93,18 +97,19 @@ __global__ void factor_kernel(const __grid_constant__ GeomParams P) {
       for (int b = a; b < d; ++b) {
         double sacc = 0.0;
         for (int mm = 0; mm < d; ++mm) sacc = __dadd_rn(sacc, __dmul_rn(jinv[a][mm], jinv[b][mm]));
-        out[int64_t(k++) * nqd] = __dmul_rn(nw, sacc);
+        out[int64_t(k++) * kstride] = __dmul_rn(nw, sacc);
       }
   }
   if (P.kind == FB_GRADIENT || P.kind == FB_DIVERGENCE) {
     for (int cc = 0; cc < d; ++cc)
-      for (int mm = 0; mm < d; ++mm) out[int64_t(cc * d + mm) * nqd] = __dmul_rn(wdet, jinv[mm][cc]);
+      for (int mm = 0; mm < d; ++mm) out[int64_t(cc * d + mm) * kstride] = __dmul_rn(wdet, jinv[mm][cc]);
   }
 }
 
 int build_factors_device(int dim, int64_t ne, const double* corners_dev, int nq,
                          const double* pts, const double* w1, int kind, double c, double nu,
-                         double* fac_dev, int nfac, int64_t fstride, cudaStream_t st) {
+                         double* fac_dev, int nfac, int64_t fstride, int lanes,
+                         cudaStream_t st) {
   GeomParams P;
   P.corners = corners_dev;
   P.fac = fac_dev;
@@ -114,6 +119,7 @@ int build_factors_device(int dim, int64_t ne, const double* corners_dev, int nq,
   P.kind = kind;
   P.nfac = nfac;
   P.fstride = fstride;
+  P.lanes = lanes;
   P.c = c;
   P.nu = nu;
   for (int i = 0; i < nq && i < 32; ++i) {

@@ -8,13 +8,14 @@
 
 #include "fb_common.cuh"
 #include "sf3_fast.cuh"
+#include "sf3_q1.cuh"
 #include "sf_general.cuh"
 
 namespace fb {
 
 int build_factors_device(int dim, int64_t ne, const double* corners_dev, int nq,
                          const double* pts, const double* w1, int kind, double c, double nu,
-                         double* fac_dev, int nfac, int64_t fstride, cudaStream_t st);
+                         double* fac_dev, int nfac, int64_t fstride, int lanes, cudaStream_t st);
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -75,7 +76,9 @@ struct fb_operator {
   const fb_restriction* rv = nullptr;
   const fb_restriction* rp = nullptr;
   bool fast = false;
-  SF3Params fp;  // host copy of the fast-path parameters
+  bool q1 = false;  // trilinear thread-per-element kernel, interleaved factors
+  SF3Params fp;     // host copy of the fast-path parameters
+  Q1Params qp;
   DevBuf<double> fac;
   DevBuf<double> mats;
   DevBuf<double> S;  // shared-entry buffer / E-vector scratch
@@ -116,13 +119,13 @@ void diff_matrix(const double* x, int n, double* D) {
   }
 }
 
-template <int N, int Q, int KIND, int NE, int NT, int MINB>
+template <int N, int Q, int KIND, int NE, int NT, int MINB, bool ZL>
 int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
-  constexpr size_t smem = SF3Shape<N, Q, KIND, NE>::SMEM;
+  constexpr size_t smem = SF3Shape<N, Q, KIND, NE, ZL>::SMEM;
   // persistent grid: as many CTAs as can be resident at once
   static int resident = 0;
   if (resident == 0) {
-    auto kern = sf3_fast_kernel<N, Q, KIND, NE, NT, MINB>;
+    auto kern = sf3_fast_kernel<N, Q, KIND, NE, NT, MINB, ZL>;
     FB_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(smem)));
     int dev = 0, sms = 0, per_sm = 0;
@@ -136,17 +139,17 @@ int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_
   p.y = y;
   p.nbatch = ceil_div(op->rv->ne, NE);
   const int grid = p.nbatch < resident ? p.nbatch : resident;
-  sf3_fast_kernel<N, Q, KIND, NE, NT, MINB><<<grid, NT, smem, st>>>(p);
+  sf3_fast_kernel<N, Q, KIND, NE, NT, MINB, ZL><<<grid, NT, smem, st>>>(p);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
 
-template <int N, int Q, int NE, int NT, int MINB>
+template <int N, int Q, int NE, int NT, int MINB, bool ZL = false>
 int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   switch (op->kind) {
-    case FB_MASS: return launch_fast_t<N, Q, kMass, NE, NT, MINB>(op, x, y, st);
-    case FB_STIFFNESS: return launch_fast_t<N, Q, kStiff, NE, NT, MINB>(op, x, y, st);
-    default: return launch_fast_t<N, Q, kHelm, NE, NT, MINB>(op, x, y, st);
+    case FB_MASS: return launch_fast_t<N, Q, kMass, NE, NT, MINB, ZL>(op, x, y, st);
+    case FB_STIFFNESS: return launch_fast_t<N, Q, kStiff, NE, NT, MINB, ZL>(op, x, y, st);
+    default: return launch_fast_t<N, Q, kHelm, NE, NT, MINB, ZL>(op, x, y, st);
   }
 }
 
@@ -155,9 +158,9 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // element (34-52 KB); the grid is persistent (all CTAs resident).
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   switch (op->rv->p) {
-    case 1: return launch_fast_kind<2, 3, 32, 288, 3>(op, x, y, st);
-    case 2: return launch_fast_kind<3, 4, 16, 256, 3>(op, x, y, st);
-    case 3: return launch_fast_kind<4, 5, 8, 256, 3>(op, x, y, st);
+    case 1: return launch_fast_kind<2, 3, 32, 288, 3>(op, x, y, st);  // (p=1 uses sf3_q1)
+    case 2: return launch_fast_kind<3, 4, 16, 256, 3, true>(op, x, y, st);
+    case 3: return launch_fast_kind<4, 5, 8, 256, 3, true>(op, x, y, st);
     case 4: return launch_fast_kind<5, 6, 4, 160, 5>(op, x, y, st);
     case 5: return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
     case 6: return launch_fast_kind<7, 8, 2, 192, 4>(op, x, y, st);
@@ -180,13 +183,28 @@ int scatter_rows(const fb_restriction* r, bool split, const double* S, int64_t S
   return FB_OK;
 }
 
-// AoS (ne, nq, k) -> element-blocked (ne, [k, nq] padded to fstride)
+// AoS (ne, nq, k) -> element-blocked (ne, [k, nq] padded to fstride), or for
+// lanes = 32 the interleaved layout [ne/32][ktot][nq][32].
 void relayout(const double* src, int64_t ne, int nqd, int k, double* dst, int64_t fstride,
-              int koff) {
+              int koff, int lanes = 0, int ktot = 0) {
   for (int64_t e = 0; e < ne; ++e)
     for (int c = 0; c < k; ++c)
-      for (int q = 0; q < nqd; ++q)
-        dst[e * fstride + int64_t(koff + c) * nqd + q] = src[(e * nqd + q) * k + c];
+      for (int q = 0; q < nqd; ++q) {
+        const double v = src[(e * nqd + q) * k + c];
+        if (lanes)
+          dst[((e / lanes) * ktot + koff + c) * int64_t(nqd) * lanes + int64_t(q) * lanes +
+              (e % lanes)] = v;
+        else
+          dst[e * fstride + int64_t(koff + c) * nqd + q] = v;
+      }
+}
+
+bool use_q1(int kind, int dim, int p, int nq1, const fb_restriction* rv) {
+  return kind <= FB_HELMHOLTZ && dim == 3 && p == 1 && nq1 == 3 && rv->split_ok;
+}
+
+int64_t factor_count(bool q1, int64_t ne, int nfac, int nqd, int64_t fstride) {
+  return q1 ? (ne + 31) / 32 * 32 * int64_t(nfac) * nqd : ne * fstride;
 }
 
 }  // namespace
@@ -202,7 +220,28 @@ static int finish_operator(fb_operator* op, const double* points, const double* 
   const int p = rv->p;
   op->fast = (kind <= FB_HELMHOLTZ) && dim == 3 && nq1 == p + 2 && p >= 1 && p <= 8 &&
              rv->split_ok;
-  if (op->fast) {
+  op->q1 = op->fast && use_q1(kind, dim, p, nq1, rv);
+  if (op->q1) {
+    Q1Params& qp = op->qp;
+    std::memset(&qp, 0, sizeof(qp));
+    for (int q = 0; q < 3; ++q)
+      for (int i = 0; i < 2; ++i) qp.B[q][i] = B[q * 2 + i];
+    std::vector<double> Dq(9);
+    diff_matrix(points, 3, Dq.data());
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) qp.Dq[a][b] = Dq[a * 3 + b];
+    FB_REQUIRE(rv->nlocp == 8 && rv->nbp == 8, "unexpected p=1 map layout");
+    qp.map = rv->map_pad.ptr;
+    qp.spos = rv->s_pos.ptr;
+    qp.fac = op->fac.ptr;
+    qp.ne = ne;
+    qp.x_comp_stride = rv->ndofs;
+    qp.S_comp_stride = ne * rv->nb;
+    qp.vdim = vdim;
+    op->S_comp_stride = ne * rv->nb;
+    FB_TRY_CUDA(op->S.alloc(op->S_comp_stride * vdim));
+    qp.S = op->S.ptr;
+  } else if (op->fast) {
     SF3Params& fp = op->fp;
     std::memset(&fp, 0, sizeof(fp));
     const int n = rv->n;
@@ -401,13 +440,16 @@ int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction*
     if (kind != FB_MASS) FB_REQUIRE(stiff != nullptr, "stiffness factor required");
     op->nfac = (kind == FB_MASS) ? 1 : (kind == FB_STIFFNESS ? ksym : ksym + 1);
     op->fstride = (int64_t(op->nfac) * nqd + 1) / 2 * 2;
-    fac.assign(size_t(ne) * op->fstride, 0.0);
+    const bool q1 = use_q1(kind, dim, rv->p, nq1, rv);
+    const int lanes = q1 ? 32 : 0;
+    fac.assign(size_t(factor_count(q1, ne, op->nfac, nqd, op->fstride)), 0.0);
     int koff = 0;
     if (kind != FB_STIFFNESS) {
-      relayout(wdet, ne, nqd, 1, fac.data(), op->fstride, 0);
+      relayout(wdet, ne, nqd, 1, fac.data(), op->fstride, 0, lanes, op->nfac);
       koff = 1;
     }
-    if (kind != FB_MASS) relayout(stiff, ne, nqd, ksym, fac.data(), op->fstride, koff);
+    if (kind != FB_MASS)
+      relayout(stiff, ne, nqd, ksym, fac.data(), op->fstride, koff, lanes, op->nfac);
   } else {
     FB_REQUIRE(rp != nullptr, "pressure restriction is NULL");
     FB_REQUIRE(rp->ne == ne && rp->dim == dim, "velocity/pressure spaces disagree");
@@ -461,13 +503,14 @@ int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restric
     op->nfac = dim * dim;
   }
   op->fstride = (int64_t(op->nfac) * nqd + 1) / 2 * 2;
-  FB_TRY_CUDA(op->fac.alloc(ne * op->fstride));
+  const bool q1 = use_q1(kind, dim, rv->p, nq1, rv);
+  FB_TRY_CUDA(op->fac.alloc(factor_count(q1, ne, op->nfac, nqd, op->fstride)));
   FB_TRY_CUDA(cudaMemset(op->fac.ptr, 0, op->fac.bytes()));
   {
     DevBuf<double> cd;
     FB_TRY_CUDA(cd.upload(corners, ne * (int64_t(1) << dim) * dim));
     int rc = build_factors_device(dim, ne, cd.ptr, nq1, points, weights, kind, c, nu,
-                                  op->fac.ptr, op->nfac, op->fstride, 0);
+                                  op->fac.ptr, op->nfac, op->fstride, q1 ? 32 : 0, 0);
     if (rc != FB_OK) return rc;
     FB_TRY_CUDA(cudaDeviceSynchronize());
   }
@@ -545,8 +588,28 @@ int fb_operator_apply_part(const fb_operator* op, const double* x, double* y, in
   cudaStream_t st = as_stream(stream);
   if (op->fast) {
     if (op->rv->ne > 0 && part != 2) {
-      int rc = launch_fast(op, x, y, st);
-      if (rc != FB_OK) return rc;
+      if (op->q1) {
+        Q1Params qp = op->qp;
+        qp.x = x;
+        const int grid = ceil_div(op->rv->ne, kQ1Threads);
+        static bool q1_configured = false;
+        if (!q1_configured) {
+          FB_TRY_CUDA(cudaFuncSetAttribute(sf3_q1_kernel<kMass>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kQ1Smem));
+          FB_TRY_CUDA(cudaFuncSetAttribute(sf3_q1_kernel<kStiff>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kQ1Smem));
+          FB_TRY_CUDA(cudaFuncSetAttribute(sf3_q1_kernel<kHelm>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kQ1Smem));
+          q1_configured = true;
+        }
+        if (op->kind == FB_MASS) sf3_q1_kernel<kMass><<<grid, kQ1Threads, kQ1Smem, st>>>(qp);
+        else if (op->kind == FB_STIFFNESS) sf3_q1_kernel<kStiff><<<grid, kQ1Threads, kQ1Smem, st>>>(qp);
+        else sf3_q1_kernel<kHelm><<<grid, kQ1Threads, kQ1Smem, st>>>(qp);
+        FB_CHECK_LAUNCH();
+      } else {
+        int rc = launch_fast(op, x, y, st);
+        if (rc != FB_OK) return rc;
+      }
     }
     if (part == 1) return FB_OK;
     return scatter_rows(op->rv, true, op->S.ptr, op->S_comp_stride, y, op->rv->ndofs,

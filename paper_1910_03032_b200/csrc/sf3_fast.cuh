@@ -85,7 +85,7 @@ struct KindInfo<kHelm> {
 __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 // Compile-time geometry of one instantiation.
-template <int N, int Q, int KIND, int NE>
+template <int N, int Q, int KIND, int NE, bool ZL = false>
 struct SF3Shape {
   static constexpr int QP = Q | 1;        // odd x-pitch
   static constexpr int BUF = Q * Q * QP;  // one q^3 buffer (padded)
@@ -97,7 +97,8 @@ struct SF3Shape {
   static constexpr int FACP = round_up(NK * Q3, 2);
   static constexpr int NB = (N <= 2) ? NLOC : NLOC - (N - 2) * (N - 2) * (N - 2);
   static constexpr int NBP = round_up(NB, 4);
-  static constexpr int NBUF = (KIND == kMass) ? 2 : 4;  // work buffers per element
+  // work buffers per element: the z-line schedule (ZL) keeps G_z in registers
+  static constexpr int NBUF = (KIND == kMass) ? 2 : (ZL ? 3 : 4);
   static constexpr int XBUF = N * N * (N | 1);          // gathered x_e (odd pitch)
   // shared-memory plan (bytes):
   //   [3 mbarriers | 3 x (map | slots) | gather buffer | work buffers]
@@ -178,9 +179,9 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-template <int N, int Q, int KIND, int NE, int NT, int MINB>
+template <int N, int Q, int KIND, int NE, int NT, int MINB, bool ZL>
 __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constant__ SF3Params P) {
-  using Sh = SF3Shape<N, Q, KIND, NE>;
+  using Sh = SF3Shape<N, Q, KIND, NE, ZL>;
   constexpr int QP = Sh::QP, BUF = Sh::BUF, NLOC = Sh::NLOC, NLOCP = Sh::NLOCP;
   constexpr int Q2 = Sh::Q2, Q3 = Sh::Q3, FACP = Sh::FACP, NBP = Sh::NBP, NBUF = Sh::NBUF;
   constexpr int NQX = N | 1;  // x pitch of the gather buffer
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       }
       __syncthreads();
 
+      if constexpr (!ZL) {
       // ---- P3: z-lines (b,a): b0 -> U (b0 in place), Gz = Dq_z U (b3) -------
 #pragma unroll 1
       for (int L = tid; L < NE * Q2; L += NT) {
@@ -482,6 +484,172 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         __syncthreads();
       }
 
+      } else {
+      // ---- P3: z-lines (b,a): b0 -> U (b0 in place) ---------------------------
+#pragma unroll 1
+      for (int L = tid; L < NE * Q2; L += NT) {
+        const int el = L / Q2, r = L - el * Q2;
+        const int b = r / Q, a = r - b * Q;
+        double* base = smem + el * NBUF * BUF;
+        double v[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = base[IX(k, b, a)];
+        double u[Q];
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc = fma(P.B[c][k], v[k], acc);
+          u[c] = acc;
+        }
+        if (KIND == kMass) {
+          // mass: scale by wdet and contract back along z right here
+          const double* __restrict__ f = P.fac + (e0 + el) * FACP + b * Q + a;
+          const bool live = el < nel;
+#pragma unroll
+          for (int c = 0; c < Q; ++c) u[c] = (live ? __ldg(f + c * Q2) : 0.0) * u[c];
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], u[c], acc);
+            base[IX(k, b, a)] = acc;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < Q; ++c) base[IX(c, b, a)] = u[c];
+        }
+      }
+      __syncthreads();
+
+      if (KIND != kMass) {
+        // ---- P4: derivative lines: x (c,b) b0 -> b1; y (c,a) b0 -> b2 -----
+#pragma unroll 1
+        for (int L = tid; L < NE * Q2; L += NT) {
+          const int el = L / Q2, r = L - el * Q2;
+          const int c = r / Q, t = r - c * Q;
+          double* base = smem + el * NBUF * BUF;
+          // the x-line (c, b=t) and the y-line (c, a=t) share Dq coefficients
+          const double* inx = base + IX(c, t, 0);
+          const double* iny = base + IX(c, 0, t);
+          double vx[Q], vy[Q];
+#pragma unroll
+          for (int s2 = 0; s2 < Q; ++s2) {
+            vx[s2] = inx[s2];
+            vy[s2] = iny[s2 * QP];
+          }
+          double* ox = base + BUF + IX(c, t, 0);
+          double* oy = base + 2 * BUF + IX(c, 0, t);
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            double ax = 0.0, ay = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < Q; ++s2) {
+              ax = fma(P.Dq[a][s2], vx[s2], ax);
+              ay = fma(P.Dq[a][s2], vy[s2], ay);
+            }
+            ox[a] = ax;
+            oy[a * QP] = ay;
+          }
+        }
+        __syncthreads();
+
+        // ---- P5: z-line pointwise stage (b,a), factors from L2:
+        //   G_z = Dq_z U in registers; per point f = W g (g0, g1 from b1, b2);
+        //   f0 -> b1, f1 -> b2; V = f_u + Dq_z^T f_z -> b0 (replaces U)
+        constexpr int o = (KIND == kHelm) ? 1 : 0;
+#pragma unroll 1
+        for (int L = tid; L < nel * Q2; L += NT) {
+          const int el = L / Q2, ba = L - el * Q2;
+          const int b = ba / Q, a = ba - b * Q;
+          double* col = smem + el * NBUF * BUF + IX(0, b, a);
+          const double* __restrict__ f = P.fac + (e0 + el) * FACP + ba;
+          double u[Q], g[Q];
+#pragma unroll
+          for (int c = 0; c < Q; ++c) u[c] = col[c * Q * QP];
+#pragma unroll
+          for (int c = 0; c < Q; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < Q; ++s2) acc = fma(P.Dq[c][s2], u[s2], acc);
+            g[c] = acc;
+          }
+#pragma unroll
+          for (int c = 0; c < Q; ++c) {
+            const double* fc = f + c * Q2;
+            const double w00 = __ldg(fc + (o + 0) * Q3), w01 = __ldg(fc + (o + 1) * Q3);
+            const double w02 = __ldg(fc + (o + 2) * Q3), w11 = __ldg(fc + (o + 3) * Q3);
+            const double w12 = __ldg(fc + (o + 4) * Q3), w22 = __ldg(fc + (o + 5) * Q3);
+            double* pt = col + c * Q * QP;
+            const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = g[c];
+            pt[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
+            pt[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
+            g[c] = w02 * g0 + w12 * g1 + w22 * g2;
+            u[c] = (KIND == kHelm) ? __ldg(fc) * u[c] : 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < Q; ++c) {
+            double acc = u[c];
+#pragma unroll
+            for (int s2 = 0; s2 < Q; ++s2) acc = fma(P.Dq[s2][c], g[s2], acc);
+            col[c * Q * QP] = acc;
+          }
+        }
+        __syncthreads();
+
+        // ---- P6: transposed derivative lines, in place: x b1, y b2 ---------
+#pragma unroll 1
+        for (int L = tid; L < NE * Q2; L += NT) {
+          const int el = L / Q2, r = L - el * Q2;
+          const int c = r / Q, t = r - c * Q;
+          double* base = smem + el * NBUF * BUF;
+          double* io0 = base + BUF + IX(c, t, 0);
+          double* io1 = base + 2 * BUF + IX(c, 0, t);
+          double v0[Q], v1[Q];
+#pragma unroll
+          for (int s2 = 0; s2 < Q; ++s2) {
+            v0[s2] = io0[s2];
+            v1[s2] = io1[s2 * QP];
+          }
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < Q; ++s2) {
+              const double dd = P.Dq[s2][a];
+              a0 = fma(dd, v0[s2], a0);
+              a1 = fma(dd, v1[s2], a1);
+            }
+            io0[a] = a0;
+            io1[a * QP] = a1;
+          }
+        }
+        __syncthreads();
+
+        // ---- P7: transposed z-lines (b,a): (b0+b1+b2) -> b0[k<N] -----------
+#pragma unroll 1
+        for (int L = tid; L < NE * Q2; L += NT) {
+          const int el = L / Q2, r = L - el * Q2;
+          const int b = r / Q, a = r - b * Q;
+          double* base = smem + el * NBUF * BUF;
+          double v[Q];
+#pragma unroll
+          for (int c = 0; c < Q; ++c) {
+            const int ix = IX(c, b, a);
+            v[c] = (base[ix] + base[BUF + ix]) + base[2 * BUF + ix];
+          }
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], v[c], acc);
+            base[IX(k, b, a)] = acc;
+          }
+        }
+        __syncthreads();
+      }
+
+      }
       // ---- P8: transposed y-lines (k,a): b0[k][b<Q][a] -> b1[k][j<N][a] ----
 #pragma unroll 1
       for (int L = tid; L < NE * N * Q; L += NT) {
