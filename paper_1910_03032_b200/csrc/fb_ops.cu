@@ -36,13 +36,40 @@ __global__ void scatter_rows_kernel(int64_t nrows, const int* __restrict__ row_d
   const double* Sc = S + comp * S_comp_stride;
   const int b = __ldg(off + r), e = __ldg(off + r + 1);
   double acc = 0.0;
-  if (ent) {
-    for (int k = b; k < e; ++k) acc += __ldg(Sc + __ldg(ent + k));
-  } else {  // slots already in row order (fused path)
-    for (int k = b; k < e; ++k) acc += __ldg(Sc + k);
-  }
+  for (int k = b; k < e; ++k) acc += __ldg(Sc + __ldg(ent + k));
   const int64_t dof = row_dof ? int64_t(__ldg(row_dof + r)) : r;
   y[comp * y_comp_stride + dof] = acc;
+}
+
+// Slot-ordered variant (fused path): each thread sums RPT consecutive rows
+// whose slots are contiguous, so the offsets come in one vector load and all
+// slot loads of the thread are independent (memory-level parallelism).
+constexpr int kRPT = 4;
+__global__ void scatter_slots_kernel(int64_t nrows, const int* __restrict__ row_dof,
+                                     const int* __restrict__ off, const double* __restrict__ S,
+                                     int64_t S_comp_stride, double* __restrict__ y,
+                                     int64_t y_comp_stride) {
+  const int64_t r0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kRPT;
+  if (r0 >= nrows) return;
+  const int comp = blockIdx.y;
+  const double* __restrict__ Sc = S + comp * S_comp_stride;
+  double* __restrict__ yc = y + comp * y_comp_stride;
+  int o[kRPT + 1], d[kRPT];
+  const int nr = (nrows - r0) < kRPT ? int(nrows - r0) : kRPT;
+#pragma unroll
+  for (int i = 0; i <= kRPT; ++i) o[i] = i <= nr ? __ldg(off + r0 + i) : 0;
+#pragma unroll
+  for (int i = 0; i < kRPT; ++i) d[i] = i < nr ? __ldg(row_dof + r0 + i) : 0;
+  double acc[kRPT];
+#pragma unroll
+  for (int i = 0; i < kRPT; ++i) {
+    acc[i] = 0.0;
+    if (i < nr)
+      for (int k = o[i]; k < o[i + 1]; ++k) acc[i] += __ldg(Sc + k);
+  }
+#pragma unroll
+  for (int i = 0; i < kRPT; ++i)
+    if (i < nr) yc[d[i]] = acc[i];
 }
 
 __global__ void gather_kernel(int64_t total, const int* __restrict__ map,
@@ -174,11 +201,15 @@ int scatter_rows(const fb_restriction* r, bool split, const double* S, int64_t S
                  double* y, int64_t y_comp_stride, int ncomp, cudaStream_t st) {
   const int64_t nrows = split ? r->nsrows : r->ndofs;
   if (nrows == 0) return FB_OK;
-  dim3 grid(ceil_div(nrows, 256), ncomp);
-  scatter_rows_kernel<<<grid, 256, 0, st>>>(nrows, split ? r->s_row.ptr : nullptr,
-                                            split ? r->s_off.ptr : r->full_off.ptr,
-                                            split ? nullptr : r->full_ent.ptr, S,
-                                            S_comp_stride, y, y_comp_stride);
+  if (split) {
+    dim3 grid(ceil_div(ceil_div(nrows, kRPT), 256), ncomp);
+    scatter_slots_kernel<<<grid, 256, 0, st>>>(nrows, r->s_row.ptr, r->s_off.ptr, S,
+                                               S_comp_stride, y, y_comp_stride);
+  } else {
+    dim3 grid(ceil_div(nrows, 256), ncomp);
+    scatter_rows_kernel<<<grid, 256, 0, st>>>(nrows, nullptr, r->full_off.ptr, r->full_ent.ptr,
+                                              S, S_comp_stride, y, y_comp_stride);
+  }
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
