@@ -110,6 +110,9 @@ int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restric
                             const double* D_host, const double* Bp_host, const double* Dp_host,
                             const double* corners_host, double c, double nu,
                             fb_operator** out);
+/* Select one of the compiled launch shapes of the fused kernel for degree p
+ * (0 = default); used by tools/tune_fast.py. */
+int fb_set_fast_config(int p, int variant);
 /* Element-blocked factors (ne, K, nq1^dim) back to host, for verification. */
 int64_t fb_operator_factor_count(const fb_operator* op);
 int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count);

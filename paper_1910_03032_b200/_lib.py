@@ -42,6 +42,7 @@ _SIGS = [
     ("fb_operator_create_geom", _int, [_int, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp,
                                        _vp, _dbl, _dbl, C.POINTER(_vp)]),
     ("fb_operator_factor_count", _i64, [_vp]),
+    ("fb_set_fast_config", _int, [_int, _int]),
     ("fb_operator_factors", _int, [_vp, _vp, _i64]),
     ("fb_operator_destroy", None, [_vp]),
     ("fb_operator_apply", _int, [_vp, _vp, _vp, _vp]),

@@ -183,16 +183,41 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // (N, Q, elements per CTA, threads, min CTAs/SM) per degree; shared memory
 // per CTA: double-buffered map/slot stage, gather buffer, 4 work buffers per
 // element (34-52 KB); the grid is persistent (all CTAs resident).
+// Runtime-selectable launch shapes (tuning): g_fast_cfg[p] picks a variant.
+static int g_fast_cfg[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
+  const int v = g_fast_cfg[op->rv->p < 9 ? op->rv->p : 0];
   switch (op->rv->p) {
     case 1: return launch_fast_kind<2, 3, 32, 288, 3>(op, x, y, st);  // (p=1 uses sf3_q1)
-    case 2: return launch_fast_kind<3, 4, 16, 256, 3, true>(op, x, y, st);
-    case 3: return launch_fast_kind<4, 5, 8, 256, 3, true>(op, x, y, st);
-    case 4: return launch_fast_kind<5, 6, 4, 160, 5>(op, x, y, st);
-    case 5: return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
-    case 6: return launch_fast_kind<7, 8, 2, 192, 4>(op, x, y, st);
-    case 7: return launch_fast_kind<8, 9, 1, 128, 4>(op, x, y, st);
-    case 8: return launch_fast_kind<9, 10, 1, 128, 4>(op, x, y, st);
+    case 2:
+      if (v == 1) return launch_fast_kind<3, 4, 16, 256, 3, true>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<3, 4, 8, 128, 6, false>(op, x, y, st);
+      return launch_fast_kind<3, 4, 4, 64, 10, true>(op, x, y, st);
+    case 3:
+      if (v == 1) return launch_fast_kind<4, 5, 8, 256, 3, true>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<4, 5, 4, 128, 6, false>(op, x, y, st);
+      return launch_fast_kind<4, 5, 2, 64, 10, true>(op, x, y, st);
+    case 4:
+      if (v == 1) return launch_fast_kind<5, 6, 4, 160, 5>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<5, 6, 1, 64, 12>(op, x, y, st);
+      return launch_fast_kind<5, 6, 2, 96, 8>(op, x, y, st);
+    case 5:
+      if (v == 1) return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<6, 7, 2, 128, 6>(op, x, y, st);
+      return launch_fast_kind<6, 7, 1, 64, 10>(op, x, y, st);
+    case 6:
+      if (v == 1) return launch_fast_kind<7, 8, 2, 128, 6>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<7, 8, 2, 192, 4>(op, x, y, st);
+      return launch_fast_kind<7, 8, 1, 96, 8>(op, x, y, st);
+    case 7:
+      if (v == 1) return launch_fast_kind<8, 9, 2, 192, 3>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<8, 9, 1, 96, 6>(op, x, y, st);
+      return launch_fast_kind<8, 9, 1, 128, 4>(op, x, y, st);
+    case 8:
+      if (v == 1) return launch_fast_kind<9, 10, 1, 96, 5>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<9, 10, 2, 224, 2>(op, x, y, st);
+      return launch_fast_kind<9, 10, 1, 128, 4>(op, x, y, st);
     default: set_error("fast path not built for this degree"); return FB_ERR_UNSUPPORTED;
   }
 }
@@ -560,6 +585,12 @@ int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count) 
 }
 
 int64_t fb_operator_factor_count(const fb_operator* op) { return op ? op->fac.n : 0; }
+
+int fb_set_fast_config(int p, int variant) {
+  FB_REQUIRE(p >= 1 && p <= 8 && variant >= 0 && variant <= 2, "bad fast-path config");
+  g_fast_cfg[p] = variant;
+  return FB_OK;
+}
 
 void fb_operator_destroy(fb_operator* op) { delete op; }
 

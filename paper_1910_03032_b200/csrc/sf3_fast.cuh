@@ -84,11 +84,24 @@ struct KindInfo<kHelm> {
 
 __host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
+// Work-buffer pitches (x-row pitch QP, z-plane pitch YP, element pad) chosen
+// by a wavefront model of every pass's shared-memory accesses
+// (tools/bank_model.py): dense x-rows with a padded plane pitch remove the
+// 2-way conflicts an odd x-pitch causes in the y- and z-line passes.
+template <int Q>
+struct SF3Pitch {
+  static constexpr int QP = (Q == 8) ? 9 : Q;
+  static constexpr int YP = (Q == 4) ? 19 : (Q == 5) ? 25 : (Q == 6) ? 38 : (Q == 7) ? 52
+                          : (Q == 8) ? 72 : (Q == 9) ? 81 : (Q == 10) ? 101 : Q * (Q | 1);
+  static constexpr int PAD = (Q == 4) ? 4 : (Q == 5) ? 2 : (Q == 6) ? 4 : (Q == 7) ? 1 : 0;
+};
+
 // Compile-time geometry of one instantiation.
 template <int N, int Q, int KIND, int NE, bool ZL = false>
 struct SF3Shape {
-  static constexpr int QP = Q | 1;        // odd x-pitch
-  static constexpr int BUF = Q * Q * QP;  // one q^3 buffer (padded)
+  static constexpr int QP = SF3Pitch<Q>::QP;  // x-row pitch
+  static constexpr int YP = SF3Pitch<Q>::YP;  // z-plane pitch
+  static constexpr int BUF = Q * YP;          // one q^3 buffer (padded)
   static constexpr int NLOC = N * N * N;
   static constexpr int NLOCP = round_up(NLOC, 4);
   static constexpr int Q2 = Q * Q;
@@ -107,7 +120,8 @@ struct SF3Shape {
   static constexpr int OFF_STAGE = 32;
   static constexpr int OFF_X = OFF_STAGE + NSTAGE * STAGE;
   static constexpr int OFF_WORK = round_up(OFF_X + NE * XBUF * 8, 16);
-  static constexpr int SMEM = OFF_WORK + NE * NBUF * BUF * 8;
+  static constexpr int ES = NBUF * BUF + SF3Pitch<Q>::PAD;  // element stride (doubles)
+  static constexpr int SMEM = OFF_WORK + NE * ES * 8;
 };
 
 // rank of lattice position (k,j,i) among the element-boundary positions of
@@ -183,7 +197,8 @@ template <int N, int Q, int KIND, int NE, int NT, int MINB, bool ZL>
 __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constant__ SF3Params P) {
   using Sh = SF3Shape<N, Q, KIND, NE, ZL>;
   constexpr int QP = Sh::QP, BUF = Sh::BUF, NLOC = Sh::NLOC, NLOCP = Sh::NLOCP;
-  constexpr int Q2 = Sh::Q2, Q3 = Sh::Q3, FACP = Sh::FACP, NBP = Sh::NBP, NBUF = Sh::NBUF;
+  constexpr int Q2 = Sh::Q2, Q3 = Sh::Q3, FACP = Sh::FACP, NBP = Sh::NBP;
+  constexpr int YP = Sh::YP, ES = Sh::ES;
   constexpr int NQX = N | 1;  // x pitch of the gather buffer
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -203,7 +218,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
   const int nbatch = P.nbatch;
   const int vdim = P.vdim;
 
-  auto IX = [](int z, int yy, int xx) { return (z * Q + yy) * QP + xx; };
+  auto IX = [](int z, int yy, int xx) { return z * YP + yy * QP + xx; };
   auto XI = [](int z, int yy, int xx) { return (z * N + yy) * NQX + xx; };
   auto nel_of = [&](int batch) {
     const int64_t e0 = int64_t(batch) * NE;
@@ -286,7 +301,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         const int el = L / (N * N), r = L - el * N * N;
         const int k = r / N, j = r - k * N;
         const double* in = sx + el * Sh::XBUF + XI(k, j, 0);
-        double* out = smem + el * NBUF * BUF + BUF + IX(k, j, 0);
+        double* out = smem + el * ES + BUF + IX(k, j, 0);
         double v[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) v[i] = in[i];
@@ -313,8 +328,8 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       for (int L = tid; L < NE * N * Q; L += NT) {
         const int el = L / (N * Q), r = L - el * N * Q;
         const int k = r / Q, a = r - k * Q;
-        const double* in = smem + el * NBUF * BUF + BUF + IX(k, 0, a);
-        double* out = smem + el * NBUF * BUF + IX(k, 0, a);
+        const double* in = smem + el * ES + BUF + IX(k, 0, a);
+        double* out = smem + el * ES + IX(k, 0, a);
         double v[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) v[j] = in[j * QP];
@@ -334,7 +349,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       for (int L = tid; L < NE * Q2; L += NT) {
         const int el = L / Q2, r = L - el * Q2;
         const int b = r / Q, a = r - b * Q;
-        double* base = smem + el * NBUF * BUF;
+        double* base = smem + el * ES;
         double v[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) v[k] = base[IX(k, b, a)];
@@ -378,7 +393,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         for (int L = tid; L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int c = r / Q, t = r - c * Q;
-          double* base = smem + el * NBUF * BUF;
+          double* base = smem + el * ES;
           // the x-line (c, b=t) and the y-line (c, a=t) share Dq coefficients
           const double* inx = base + IX(c, t, 0);
           const double* iny = base + IX(c, 0, t);
@@ -404,25 +419,29 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         }
         __syncthreads();
 
-        // ---- P5: pointwise quadrature-point factors (point-parallel, from L2)
+        // ---- P5: pointwise quadrature-point factors, one z-column per thread
+        //   (points (c, b, a), c = 0..Q-1: constant strides, coalesced L2 reads)
         //   b0: U -> f_u,  b1: G0 -> f0,  b2: G1 -> f1,  b3: G2 -> f2
         constexpr int o = (KIND == kHelm) ? 1 : 0;
+#pragma unroll 1
+        for (int L = tid; L < nel * Q2; L += NT) {
+          const int el = L / Q2, ba = L - el * Q2;
+          double* col = smem + el * ES + IX(0, ba / Q, ba % Q);
+          const double* __restrict__ f = P.fac + (e0 + el) * FACP + ba;
 #pragma unroll 2
-        for (int idx = tid; idx < nel * Q3; idx += NT) {
-          const int el = idx / Q3, qp = idx - el * Q3;
-          const int c = qp / Q2, ba = qp - c * Q2;
-          const int b = ba / Q, a = ba - b * Q;
-          double* pt = smem + el * NBUF * BUF + IX(c, b, a);
-          const double* __restrict__ f = P.fac + (e0 + el) * FACP + qp;
-          const double w00 = __ldg(f + (o + 0) * Q3), w01 = __ldg(f + (o + 1) * Q3);
-          const double w02 = __ldg(f + (o + 2) * Q3), w11 = __ldg(f + (o + 3) * Q3);
-          const double w12 = __ldg(f + (o + 4) * Q3), w22 = __ldg(f + (o + 5) * Q3);
-          const double wm = (KIND == kHelm) ? __ldg(f) : 0.0;
-          const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = pt[3 * BUF];
-          pt[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
-          pt[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
-          pt[3 * BUF] = w02 * g0 + w12 * g1 + w22 * g2;
-          if (KIND == kHelm) pt[0] = wm * pt[0];
+          for (int c = 0; c < Q; ++c) {
+            const double* fc = f + c * Q2;
+            double* pt = col + c * YP;
+            const double w00 = __ldg(fc + (o + 0) * Q3), w01 = __ldg(fc + (o + 1) * Q3);
+            const double w02 = __ldg(fc + (o + 2) * Q3), w11 = __ldg(fc + (o + 3) * Q3);
+            const double w12 = __ldg(fc + (o + 4) * Q3), w22 = __ldg(fc + (o + 5) * Q3);
+            const double wm = (KIND == kHelm) ? __ldg(fc) : 0.0;
+            const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = pt[3 * BUF];
+            pt[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
+            pt[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
+            pt[3 * BUF] = w02 * g0 + w12 * g1 + w22 * g2;
+            if (KIND == kHelm) pt[0] = wm * pt[0];
+          }
         }
         __syncthreads();
 
@@ -431,7 +450,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         for (int L = tid; L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int c = r / Q, t = r - c * Q;
-          double* base = smem + el * NBUF * BUF;
+          double* base = smem + el * ES;
           // x-line (c, b=t), y-line (c, a=t), z-line (b=c, a=t): same Dq^T
           double* io0 = base + BUF + IX(c, t, 0);
           double* io1 = base + 2 * BUF + IX(c, 0, t);
@@ -441,7 +460,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           for (int s2 = 0; s2 < Q; ++s2) {
             v0[s2] = io0[s2];
             v1[s2] = io1[s2 * QP];
-            v2[s2] = io2[s2 * Q * QP];
+            v2[s2] = io2[s2 * YP];
           }
 #pragma unroll
           for (int a = 0; a < Q; ++a) {
@@ -455,7 +474,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
             }
             io0[a] = a0;
             io1[a * QP] = a1;
-            io2[a * Q * QP] = a2;
+            io2[a * YP] = a2;
           }
         }
         __syncthreads();
@@ -465,7 +484,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         for (int L = tid; L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int b = r / Q, a = r - b * Q;
-          double* base = smem + el * NBUF * BUF;
+          double* base = smem + el * ES;
           double v[Q];
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
@@ -490,7 +509,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       for (int L = tid; L < NE * Q2; L += NT) {
         const int el = L / Q2, r = L - el * Q2;
         const int b = r / Q, a = r - b * Q;
-        double* base = smem + el * NBUF * BUF;
+        double* base = smem + el * ES;
         double v[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) v[k] = base[IX(k, b, a)];
@@ -528,7 +547,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         for (int L = tid; L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int c = r / Q, t = r - c * Q;
-          double* base = smem + el * NBUF * BUF;
+          double* base = smem + el * ES;
           // the x-line (c, b=t) and the y-line (c, a=t) share Dq coefficients
           const double* inx = base + IX(c, t, 0);
           const double* iny = base + IX(c, 0, t);
@@ -562,11 +581,11 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         for (int L = tid; L < nel * Q2; L += NT) {
           const int el = L / Q2, ba = L - el * Q2;
           const int b = ba / Q, a = ba - b * Q;
-          double* col = smem + el * NBUF * BUF + IX(0, b, a);
+          double* col = smem + el * ES + IX(0, b, a);
           const double* __restrict__ f = P.fac + (e0 + el) * FACP + ba;
           double u[Q], g[Q];
 #pragma unroll
-          for (int c = 0; c < Q; ++c) u[c] = col[c * Q * QP];
+          for (int c = 0; c < Q; ++c) u[c] = col[c * YP];
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
             double acc = 0.0;
@@ -580,7 +599,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
             const double w00 = __ldg(fc + (o + 0) * Q3), w01 = __ldg(fc + (o + 1) * Q3);
             const double w02 = __ldg(fc + (o + 2) * Q3), w11 = __ldg(fc + (o + 3) * Q3);
             const double w12 = __ldg(fc + (o + 4) * Q3), w22 = __ldg(fc + (o + 5) * Q3);
-            double* pt = col + c * Q * QP;
+            double* pt = col + c * YP;
             const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = g[c];
             pt[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
             pt[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
@@ -592,7 +611,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
             double acc = u[c];
 #pragma unroll
             for (int s2 = 0; s2 < Q; ++s2) acc = fma(P.Dq[s2][c], g[s2], acc);
-            col[c * Q * QP] = acc;
+            col[c * YP] = acc;
           }
         }
         __syncthreads();
@@ -602,7 +621,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         for (int L = tid; L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int c = r / Q, t = r - c * Q;
-          double* base = smem + el * NBUF * BUF;
+          double* base = smem + el * ES;
           double* io0 = base + BUF + IX(c, t, 0);
           double* io1 = base + 2 * BUF + IX(c, 0, t);
           double v0[Q], v1[Q];
@@ -631,7 +650,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         for (int L = tid; L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int b = r / Q, a = r - b * Q;
-          double* base = smem + el * NBUF * BUF;
+          double* base = smem + el * ES;
           double v[Q];
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
@@ -655,8 +674,8 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       for (int L = tid; L < NE * N * Q; L += NT) {
         const int el = L / (N * Q), r = L - el * N * Q;
         const int k = r / Q, a = r - k * Q;
-        const double* in = smem + el * NBUF * BUF + IX(k, 0, a);
-        double* out = smem + el * NBUF * BUF + BUF + IX(k, 0, a);
+        const double* in = smem + el * ES + IX(k, 0, a);
+        double* out = smem + el * ES + BUF + IX(k, 0, a);
         double v[Q];
 #pragma unroll
         for (int b = 0; b < Q; ++b) v[b] = in[b * QP];
@@ -675,7 +694,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       for (int L = tid; L < nel * N * N; L += NT) {
         const int el = L / (N * N), r = L - el * N * N;
         const int k = r / N, j = r - k * N;
-        const double* in = smem + el * NBUF * BUF + BUF + IX(k, j, 0);
+        const double* in = smem + el * ES + BUF + IX(k, j, 0);
         double v[Q];
 #pragma unroll
         for (int a = 0; a < Q; ++a) v[a] = in[a];
