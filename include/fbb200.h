@@ -218,6 +218,17 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r_dev, 
                       void* stream);
 /* y = M x for a dense row-major n x n matrix (coarse-level inverse). */
 int fb_dense_mv(int64_t n, const double* M_dev, const double* x_dev, double* y_dev, void* stream);
+/* LOR matrix of a degree-p space on its nodal sub-cell mesh (lor.py:61-99):
+ * Q1 kind (FB_MASS / FB_STIFFNESS / FB_HELMHOLTZ) with 2-point Gauss, rows
+ * in CSR with sorted columns, constrained rows/columns zeroed in-pattern with
+ * a unit diagonal.  corners: (ne, 2^dim, dim); nodes: the p+1 GLL nodes.
+ * Outputs are malloc'ed; release them with fb_host_free.  Returns nnz or
+ * minus a status code. */
+int64_t fb_lor_assemble_host(int dim, int p, int64_t ne, int64_t ndofs, const int64_t* element_dofs,
+                             const double* corners, const double* nodes, int kind, double nu,
+                             double c, int64_t ncons, const int64_t* constrained,
+                             int64_t** indptr_out, int64_t** indices_out, double** data_out);
+void fb_host_free(void* p);
 /* ILU(0) in place on sorted CSR, IKJ order (kernels/numba_backend.py:64-103):
  * returns -1 on success, else the failing row. */
 int64_t fb_ilu0_factor_host(int64_t n, const int64_t* indptr, const int64_t* indices,

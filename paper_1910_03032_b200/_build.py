@@ -23,6 +23,7 @@ LIB = os.path.join(HERE, "libfbb200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+              "-Xcompiler", "-fopenmp",
               "--expt-relaxed-constexpr", "-I", INCLUDE]
 
 
@@ -74,7 +75,7 @@ def build(verbose=False, force=False):
             list(ex.map(lambda j: _compile(j[0], j[1], verbose), jobs))
     if force or jobs or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        cmd = [_nvcc()] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        cmd = [_nvcc()] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread", "-lgomp"]
         if verbose:
             print(" ".join(cmd), flush=True)
         res = subprocess.run(cmd, capture_output=True, text=True)

@@ -75,6 +75,9 @@ _SIGS = [
     ("fb_set_trisolve_mode", _int, [_int, _int]),
     ("fb_permute", _int, [_i64, _vp, _vp, _vp, _int, _vp]),
     ("fb_ilu0_factor_host", _i64, [_i64, _vp, _vp, _vp]),
+    ("fb_lor_assemble_host", _i64, [_int, _int, _i64, _i64, _vp, _vp, _vp, _int, _dbl, _dbl, _i64,
+                                    _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
+    ("fb_host_free", None, [_vp]),
     ("fb_blockilu_create", _int, [_i64, _int, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)]),
     ("fb_blockilu_destroy", None, [_vp]),
     ("fb_blockilu_apply", _int, [_vp, _int, _vp, _vp, _vp]),

@@ -50,6 +50,9 @@ __global__ void __launch_bounds__(kQ1Threads, 4) sf3_q1_kernel(const __grid_cons
   if (e >= P.ne) return;  // no block-level barriers below
   const int lane = int(e & 31);
   const double* __restrict__ f = P.fac + (e >> 5) * (int64_t(NK) * 27 * 32) + lane;
+  // one lane per warp streams the warp's interleaved factor block into L2
+  // (bulk prefetch) while the warp gathers x and runs the forward passes
+  if (lane == 0) bulk_prefetch_l2(f, int64_t(NK) * 27 * 32 * 8);
   double* U = su + tid;
   double* V = sv + tid;
   int m[8], sl[8];

@@ -74,7 +74,40 @@ def _q1_local_matrices(kind, corners, nu, c):
 
 
 def lor_matrix(space, kind, nu=1.0, c=0.0, constrained=None):
-    """Q1 mass/stiffness/helmholtz matrix on the nodal sub-cell mesh."""
+    """Q1 mass/stiffness/helmholtz matrix on the nodal sub-cell mesh,
+    assembled in C++ (fb_lor_assemble_host) directly into CSR."""
+    if kind not in ("mass", "stiffness", "helmholtz"):
+        raise ValueError(f"unsupported LOR kind {kind!r}")
+    if space.vdim != 1:
+        raise ValueError("LOR meshes are built from scalar spaces")
+    import ctypes as C
+    from . import _lib
+    ed = np.ascontiguousarray(space.element_dofs, dtype=np.int64)
+    corners = np.ascontiguousarray(space.mesh.corners, dtype=np.float64)
+    nodes = np.ascontiguousarray(space.basis.nodes, dtype=np.float64)
+    cons = np.ascontiguousarray(np.zeros(0) if constrained is None else constrained,
+                                dtype=np.int64)
+    ns = space.ndofs_scalar
+    pi, px, pd = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    nnz = _lib.lib.fb_lor_assemble_host(space.dim, space.p, ed.shape[0], ns, _lib.ptr(ed),
+                                        _lib.ptr(corners), _lib.ptr(nodes), _lib.KIND[kind],
+                                        float(nu), float(c), cons.size, _lib.ptr(cons),
+                                        C.byref(pi), C.byref(px), C.byref(pd))
+    if nnz < 0:
+        _lib.check(int(-nnz))
+    try:
+        indptr = np.ctypeslib.as_array(C.cast(pi, C.POINTER(C.c_int64)), shape=(ns + 1,)).copy()
+        indices = np.ctypeslib.as_array(C.cast(px, C.POINTER(C.c_int64)), shape=(max(nnz, 1),))[:nnz].copy()
+        data = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_double)), shape=(max(nnz, 1),))[:nnz].copy()
+    finally:
+        for ptr_ in (pi, px, pd):
+            _lib.lib.fb_host_free(ptr_)
+    return sp.csr_matrix((data, indices, indptr), shape=(ns, ns))
+
+
+def lor_matrix_numpy(space, kind, nu=1.0, c=0.0, constrained=None):
+    """numpy assembly of the same matrix (reference-shaped; kept as a
+    cross-check of the C++ assembler, tests/test_solvers_cpu.py)."""
     if kind not in ("mass", "stiffness", "helmholtz"):
         raise ValueError(f"unsupported LOR kind {kind!r}")
     if space.vdim != 1:
