@@ -613,7 +613,7 @@ class LORPreconditioner(_DeviceMixin):
     backward sweep; the Q1 bottom level is an exact direct solve.
 
     smoother="block" (default for stiffness / Helmholtz): block-Jacobi ILU(0)
-    over element cubes of `block`^d elements (default 2 for p <= 4, else 1) in
+    over element cubes of `block`^d elements (default 2) in
     first-touch order -- one launch per sweep, +0/+1 iterations vs the
     reference (SURVEY 8(e'), tests/test_gpu_solvers.py).  Mass defaults to
     the global smoother.  smoother="global": the
@@ -629,7 +629,9 @@ class LORPreconditioner(_DeviceMixin):
             # Helmholtz stay within +1 of the reference for any block size
             smoother = "global" if kind == "mass" else DEFAULT_SMOOTHER
         if block is None:
-            block = 2 if (space.dim == 2 or space.p <= 4) else 1
+            # 2^d-element blocks: +0/+1 iterations at p = 4 and 7 on 1M DoFs
+            # (tools/blk_sweep.py); single-element blocks cost +1/+2
+            block = 2
         if smoother not in ("block", "global"):
             raise ValueError(f"unknown smoother {smoother!r}")
         if space.vdim != 1:
