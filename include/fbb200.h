@@ -47,6 +47,7 @@ extern "C" {
 typedef struct fb_restriction fb_restriction;
 typedef struct fb_operator fb_operator;
 typedef struct fb_csr fb_csr;
+typedef struct fb_transfer fb_transfer;
 typedef struct fb_trisolve fb_trisolve;
 typedef struct fb_blockilu fb_blockilu;
 
@@ -180,8 +181,8 @@ int fb_vmul(int64_t n, const double* d_dev, const double* x_dev, double* y_dev, 
 /* ------------------------------------------------------------------ */
 /* Sparse pieces of the LOR V-cycle (solvers.py:269-392, lor.py:61-123) */
 /* ------------------------------------------------------------------ */
-/* CSR matrix on the device (int32 indices, fp64 values), copied from host
- * int64 CSR arrays (scipy.sparse.csr_matrix). */
+/* CSR matrix on the device (int64 row offsets, int32 column indices, fp64
+ * values), copied from host int64 CSR arrays (scipy.sparse.csr_matrix). */
 int fb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* indptr_host,
                   const int64_t* indices_host, const double* data_host, fb_csr** out);
 void fb_csr_destroy(fb_csr* A);
@@ -233,6 +234,46 @@ void fb_host_free(void* p);
  * returns -1 on success, else the failing row. */
 int64_t fb_ilu0_factor_host(int64_t n, const int64_t* indptr, const int64_t* indices,
                             double* data);
+
+/* ------------------------------------------------------------------ */
+/* Structured-box scale mode: LOR levels built on the device            */
+/* (SURVEY 8(e') and 8(f) items 1-2; replaces the host setup of         */
+/* lor.py:61-123, solvers.py:269-392 and numba_backend.py:64-103)       */
+/* ------------------------------------------------------------------ */
+/* Q1 LOR matrix of a degree-p space on a structured box of counts[3]
+ * elements (numbered x fastest), assembled on the device: one row per
+ * lattice point of the (counts*p+1)^3 nodal lattice, rows/columns numbered by
+ * lattice_ids_dev (int32, x fastest), columns sorted.  corners_dev: (ne, 8, 3)
+ * element corners; nodes: the p+1 GLL nodes (host).  constrain_boundary
+ * zeroes boundary rows/columns with a unit diagonal (lor.py:84-99). */
+int fb_lor_assemble_box(int p, const int64_t* counts, const double* corners_dev,
+                        const double* nodes, const int* lattice_ids_dev, int kind, double nu,
+                        double c, int constrain_boundary, fb_csr** out);
+int fb_csr_info(const fb_csr* A, int64_t* nrows, int64_t* ncols, int64_t* nnz);
+/* copy a device CSR to host arrays (indptr: nrows+1, indices/data: nnz) */
+int fb_csr_download(const fb_csr* A, int64_t* indptr, int64_t* indices, double* data);
+/* Block-Jacobi ILU(0) of a device CSR already numbered block-major (rows of
+ * block b are block_ptr[b]..block_ptr[b+1]-1), factored and level-grouped on
+ * the device; same factor and sweeps as fb_blockilu_create.  On a zero pivot
+ * *fail_row >= 0 and no handle is returned (the caller falls back to Jacobi,
+ * solvers.py:283-290). */
+int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks, const int64_t* block_ptr_host,
+                           int64_t* fail_row, fb_blockilu** out);
+/* Nodal interpolation between two levels of a structured box, matrix-free
+ * (lor.py:102-123).  fine: map of the fine level (ne, nf^3); hmap: for each
+ * fine element the coarse DoFs of its parent coarse element (ne, nc^3);
+ * counts: fine element counts; W: nw weight tables (nf x nc); widx: for
+ * axis a and element coordinate i, the table index (arrays of counts[0],
+ * counts[1], counts[2] entries, concatenated).  Fine DoFs follow first-touch
+ * ownership. */
+int fb_transfer_create(const fb_restriction* fine, const fb_restriction* hmap,
+                       const int64_t* counts, int nw, const double* W, const int64_t* widx,
+                       fb_transfer** out);
+void fb_transfer_destroy(fb_transfer* T);
+/* xf = P xc */
+int fb_transfer_prolong(const fb_transfer* T, const double* xc_dev, double* xf_dev, void* stream);
+/* xc = P^T xf (deterministic) */
+int fb_transfer_restrict(const fb_transfer* T, const double* xf_dev, double* xc_dev, void* stream);
 
 #ifdef __cplusplus
 }

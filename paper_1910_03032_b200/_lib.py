@@ -82,6 +82,15 @@ _SIGS = [
     ("fb_blockilu_destroy", None, [_vp]),
     ("fb_blockilu_apply", _int, [_vp, _int, _vp, _vp, _vp]),
     ("fb_dense_mv", _int, [_i64, _vp, _vp, _vp, _vp]),
+    ("fb_lor_assemble_box", _int, [_int, _vp, _vp, _vp, _vp, _int, _dbl, _dbl, _int,
+                                   C.POINTER(_vp)]),
+    ("fb_csr_info", _int, [_vp, _pi64, _pi64, _pi64]),
+    ("fb_csr_download", _int, [_vp, _vp, _vp, _vp]),
+    ("fb_blockilu_create_csr", _int, [_vp, _i64, _vp, _pi64, C.POINTER(_vp)]),
+    ("fb_transfer_create", _int, [_vp, _vp, _vp, _int, _vp, _vp, C.POINTER(_vp)]),
+    ("fb_transfer_destroy", None, [_vp]),
+    ("fb_transfer_prolong", _int, [_vp, _vp, _vp, _vp]),
+    ("fb_transfer_restrict", _int, [_vp, _vp, _vp, _vp]),
 ]
 
 SYMBOLS = [s[0] for s in _SIGS]

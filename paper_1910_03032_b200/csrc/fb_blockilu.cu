@@ -18,12 +18,16 @@
 #include <memory>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "fb_common.cuh"
+#include "fb_internal.cuh"
 
 namespace {
 
 struct TriPart {
-  fb::DevBuf<int> ip, ix;        // CSR (global new numbering), off-diagonal only
+  fb::DevBuf<int64_t> ip;        // CSR (global new numbering), off-diagonal only
+  fb::DevBuf<int> ix;
   fb::DevBuf<double> v;
   fb::DevBuf<double> invdiag;    // empty for unit diagonal
   fb::DevBuf<int> rows;          // rows of each block, grouped by level
@@ -45,7 +49,7 @@ struct fb_blockilu {
 namespace fb {
 
 struct TriView {
-  const int* ip;
+  const int64_t* ip;
   const int* ix;
   const double* v;
   const double* invdiag;
@@ -61,7 +65,7 @@ __device__ __forceinline__ void block_tri(const TriView& T, int b, int bs, doubl
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) {
       const int row = T.rows[k];
       double acc = 0.0;
-      for (int e = T.ip[row]; e < T.ip[row + 1]; ++e)
+      for (int64_t e = T.ip[row]; e < T.ip[row + 1]; ++e)
         acc = __dadd_rn(acc, __dmul_rn(T.v[e], y[T.ix[e] - bs]));
       const double r = __dsub_rn(y[row - bs], acc);
       y[row - bs] = T.invdiag ? __dmul_rn(r, T.invdiag[row]) : r;
@@ -76,13 +80,220 @@ __global__ void block_ilu_kernel(const int* __restrict__ block_ptr,
   extern __shared__ double y[];
   const int b = blockIdx.x;
   const int bs = block_ptr[b], be = block_ptr[b + 1];
-  for (int i = threadIdx.x; i < be - bs; i += blockDim.x) y[i] = r[new2old[bs + i]];
+  // new2old == nullptr: the level is numbered block-major already
+  for (int i = threadIdx.x; i < be - bs; i += blockDim.x) y[i] = r[new2old ? new2old[bs + i] : bs + i];
   __syncthreads();
   block_tri(A, b, bs, y);
   block_tri(B, b, bs, y);
-  for (int i = threadIdx.x; i < be - bs; i += blockDim.x) out[new2old[bs + i]] = y[i];
+  for (int i = threadIdx.x; i < be - bs; i += blockDim.x) out[new2old ? new2old[bs + i] : bs + i] = y[i];
 }
 
+
+// ---- device-side construction (structured "scale mode" levels) -----------
+// The same factor and the same per-block level grouping as the host path
+// (fb_blockilu_create), built from a device CSR without a host round trip:
+// the finest LOR level of a 100M-DoF box has ~2.7G entries.
+
+__global__ void bilu_row_block_kernel(int64_t n, int64_t nblocks, const int64_t* __restrict__ bptr,
+                                      int* __restrict__ rb) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t lo = 0, hi = nblocks - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (bptr[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  rb[r] = int(lo);
+}
+
+__global__ void bilu_count_kernel(int64_t n, const int64_t* __restrict__ ip,
+                                  const int* __restrict__ ix, const int64_t* __restrict__ bptr,
+                                  const int* __restrict__ rb, int* __restrict__ cnt) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t bs = bptr[rb[r]], be = bptr[rb[r] + 1];
+  int c = 0;
+  for (int64_t k = ip[r]; k < ip[r + 1]; ++k) c += (ix[k] >= bs && ix[k] < be);
+  cnt[r] = c;
+}
+
+__global__ void bilu_fill_kernel(int64_t n, const int64_t* __restrict__ ip,
+                                 const int* __restrict__ ix, const double* __restrict__ v,
+                                 const int64_t* __restrict__ bptr, const int* __restrict__ rb,
+                                 const int64_t* __restrict__ fip, int* __restrict__ fix,
+                                 double* __restrict__ fv, int64_t* __restrict__ dpos,
+                                 unsigned long long* __restrict__ missing) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t bs = bptr[rb[r]], be = bptr[rb[r] + 1];
+  int64_t o = fip[r], d = -1;
+  for (int64_t k = ip[r]; k < ip[r + 1]; ++k) {
+    const int c = ix[k];
+    if (c < bs || c >= be) continue;
+    if (c == r) d = o;
+    fix[o] = c;
+    fv[o] = v[k];
+    ++o;
+  }
+  dpos[r] = d;
+  if (d < 0) atomicMin(missing, (unsigned long long)r);
+}
+
+// ILU(0), IKJ order of numba_backend.py:64-103, one thread per block; every
+// update is a separately rounded multiply and subtract, so the factor is
+// bitwise the host/numba factor of the same matrix.
+__global__ void bilu_factor_kernel(int64_t nblocks, const int64_t* __restrict__ bptr,
+                                   const int64_t* __restrict__ fip, const int* __restrict__ fix,
+                                   double* __restrict__ fv, const int64_t* __restrict__ dpos,
+                                   unsigned long long* __restrict__ fail) {
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= nblocks) return;
+  for (int64_t i = bptr[b]; i < bptr[b + 1]; ++i) {
+    const int64_t re = fip[i + 1];
+    for (int64_t kk = fip[i]; kk < dpos[i]; ++kk) {
+      const int k = fix[kk];
+      const double piv = fv[dpos[k]];
+      if (fabs(piv) < 1e-300) {
+        atomicMin(fail, (unsigned long long)k);
+        return;
+      }
+      const double l = __ddiv_rn(fv[kk], piv);
+      fv[kk] = l;
+      int64_t p1 = kk + 1, p2 = dpos[k] + 1;
+      const int64_t e2 = fip[k + 1];
+      while (p1 < re && p2 < e2) {
+        const int c1 = fix[p1], c2 = fix[p2];
+        if (c1 == c2) {
+          fv[p1] = __dsub_rn(fv[p1], __dmul_rn(l, fv[p2]));
+          ++p1;
+          ++p2;
+        } else if (c1 < c2) {
+          ++p1;
+        } else {
+          ++p2;
+        }
+      }
+    }
+    if (fabs(fv[dpos[i]]) < 1e-300) {
+      atomicMin(fail, (unsigned long long)i);
+      return;
+    }
+  }
+}
+
+__global__ void bilu_split_count_kernel(int64_t n, const int64_t* __restrict__ fip,
+                                        const int64_t* __restrict__ dpos, int* __restrict__ lc,
+                                        int* __restrict__ uc) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  lc[r] = int(dpos[r] - fip[r]);
+  uc[r] = int(fip[r + 1] - dpos[r] - 1);
+}
+
+__global__ void bilu_split_fill_kernel(int64_t n, const int64_t* __restrict__ fip,
+                                       const int* __restrict__ fix, const double* __restrict__ fv,
+                                       const int64_t* __restrict__ dpos,
+                                       const int64_t* __restrict__ lip, int* __restrict__ lix,
+                                       double* __restrict__ lv, const int64_t* __restrict__ uip,
+                                       int* __restrict__ uix, double* __restrict__ uv,
+                                       double* __restrict__ uinv) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t o = lip[r];
+  for (int64_t k = fip[r]; k < dpos[r]; ++k, ++o) {
+    lix[o] = fix[k];
+    lv[o] = fv[k];
+  }
+  o = uip[r];
+  for (int64_t k = dpos[r] + 1; k < fip[r + 1]; ++k, ++o) {
+    uix[o] = fix[k];
+    uv[o] = fv[k];
+  }
+  uinv[r] = 1.0 / fv[dpos[r]];
+}
+
+__global__ void csr_col_count_kernel(int64_t n, const int64_t* __restrict__ ip,
+                                     const int* __restrict__ ix, int* __restrict__ cnt) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int64_t k = ip[r]; k < ip[r + 1]; ++k) atomicAdd(cnt + ix[k], 1);
+}
+
+__global__ void csr_transpose_fill_kernel(int64_t n, const int64_t* __restrict__ ip,
+                                          const int* __restrict__ ix, const double* __restrict__ v,
+                                          const int64_t* __restrict__ tip, int* __restrict__ cur,
+                                          int* __restrict__ tix, double* __restrict__ tv) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int64_t k = ip[r]; k < ip[r + 1]; ++k) {
+    const int c = ix[k];
+    const int64_t pos = tip[c] + atomicAdd(cur + c, 1);
+    tix[pos] = int(r);
+    tv[pos] = v[k];
+  }
+}
+
+// rows of the transpose were filled in arbitrary order: sort each by column
+__global__ void csr_sort_rows_kernel(int64_t n, const int64_t* __restrict__ ip,
+                                     int* __restrict__ ix, double* __restrict__ v) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t b = ip[r], e = ip[r + 1];
+  for (int64_t i = b + 1; i < e; ++i) {
+    const int c = ix[i];
+    const double x = v[i];
+    int64_t j = i - 1;
+    while (j >= b && ix[j] > c) {
+      ix[j + 1] = ix[j];
+      v[j + 1] = v[j];
+      --j;
+    }
+    ix[j + 1] = c;
+    v[j + 1] = x;
+  }
+}
+
+__global__ void bilu_levels_kernel(int64_t nblocks, const int64_t* __restrict__ bptr,
+                                   const int64_t* __restrict__ ip, const int* __restrict__ ix,
+                                   int lower, int* __restrict__ level, int* __restrict__ nlev) {
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= nblocks) return;
+  const int64_t bs = bptr[b], be = bptr[b + 1];
+  int maxl = 0;
+  for (int64_t k = 0; k < be - bs; ++k) {
+    const int64_t r = lower ? bs + k : be - 1 - k;
+    int lv = 0;
+    for (int64_t e = ip[r]; e < ip[r + 1]; ++e) lv = max(lv, level[ix[e]] + 1);
+    level[r] = lv;
+    maxl = max(maxl, lv);
+  }
+  nlev[b] = maxl + 1;
+}
+
+__global__ void bilu_group_kernel(int64_t nblocks, int64_t n, const int64_t* __restrict__ bptr,
+                                  const int* __restrict__ level, const int64_t* __restrict__ bg,
+                                  int* __restrict__ grp, int* __restrict__ blk_grp,
+                                  int* __restrict__ cur, int* __restrict__ rows) {
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b > nblocks) return;
+  blk_grp[b] = int(bg[b]);
+  if (b == nblocks) {
+    grp[bg[b]] = int(n);
+    return;
+  }
+  const int64_t bs = bptr[b], be = bptr[b + 1];
+  const int64_t g0 = bg[b], L = bg[b + 1] - g0;
+  for (int64_t l = 0; l < L; ++l) grp[g0 + l] = 0;
+  for (int64_t r = bs; r < be; ++r) grp[g0 + level[r]]++;
+  int off = int(bs);
+  for (int64_t l = 0; l < L; ++l) {
+    const int t = grp[g0 + l];
+    grp[g0 + l] = off;
+    cur[g0 + l] = off;
+    off += t;
+  }
+  for (int64_t r = bs; r < be; ++r) rows[cur[g0 + level[r]]++] = int(r);
+}
 }  // namespace fb
 
 using namespace fb;
@@ -94,7 +305,8 @@ namespace {
 int build_part(int64_t n, const std::vector<int>& bptr, const std::vector<int64_t>& ip,
                const std::vector<int64_t>& ix, const std::vector<double>& v, bool lower,
                bool unit, TriPart& P) {
-  std::vector<int> oip(n + 1, 0), oix;
+  std::vector<int64_t> oip(n + 1, 0);
+  std::vector<int> oix;
   std::vector<double> ov, inv(n, 1.0);
   oix.reserve(ix.size());
   ov.reserve(ix.size());
@@ -112,7 +324,7 @@ int build_part(int64_t n, const std::vector<int>& bptr, const std::vector<int64_
       oix.push_back(int(c));
       ov.push_back(v[k]);
     }
-    oip[r + 1] = int(oix.size());
+    oip[r + 1] = int64_t(oix.size());
   }
   // levels within each block
   const int nb = int(bptr.size()) - 1;
@@ -128,7 +340,7 @@ int build_part(int64_t n, const std::vector<int>& bptr, const std::vector<int64_
     for (int k = 0; k < be - bs; ++k) {
       const int r = lower ? bs + k : be - 1 - k;
       int lv = 0;
-      for (int e = oip[r]; e < oip[r + 1]; ++e) {
+      for (int64_t e = oip[r]; e < oip[r + 1]; ++e) {
         FB_REQUIRE(oix[e] >= bs && oix[e] < be, "block ILU factor couples two blocks");
         lv = std::max(lv, level[oix[e]] + 1);
       }
@@ -281,3 +493,182 @@ int fb_dense_mv(int64_t n, const double* M, const double* x, double* y, void* st
 }
 
 }  // extern "C"
+
+namespace {
+
+inline int grid_for(int64_t n, int t = 256) { return fb::ceil_div(n > 0 ? n : 1, t); }
+
+// levels + per-block grouping of one triangular part (device)
+int device_levels(int64_t n, int64_t nblocks, const int64_t* bptr, TriPart& P, bool lower,
+                  cudaStream_t st) {
+  DevBuf<int> level, nlev;
+  DevBuf<int64_t> bg;
+  FB_TRY_CUDA(level.alloc(n));
+  FB_TRY_CUDA(nlev.alloc(nblocks + 1));
+  FB_TRY_CUDA(bg.alloc(nblocks + 1));
+  bilu_levels_kernel<<<grid_for(nblocks, 128), 128, 0, st>>>(nblocks, bptr, P.ip.ptr, P.ix.ptr,
+                                                              lower ? 1 : 0, level.ptr, nlev.ptr);
+  FB_CHECK_LAUNCH();
+  int rc = exclusive_offsets(nlev.ptr, nblocks, bg.ptr, st);
+  if (rc != FB_OK) return rc;
+  int64_t ngroups = 0;
+  FB_TRY_CUDA(cudaMemcpyAsync(&ngroups, bg.ptr + nblocks, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FB_TRY_CUDA(cudaStreamSynchronize(st));
+  FB_REQUIRE(ngroups < (int64_t(1) << 31), "too many level groups");
+  DevBuf<int> cur;
+  FB_TRY_CUDA(P.grp.alloc(ngroups + 1));
+  FB_TRY_CUDA(cur.alloc(ngroups + 1));
+  FB_TRY_CUDA(P.blk_grp.alloc(nblocks + 1));
+  FB_TRY_CUDA(P.rows.alloc(n));
+  bilu_group_kernel<<<grid_for(nblocks + 1, 128), 128, 0, st>>>(nblocks, n, bptr, level.ptr, bg.ptr,
+                                                                 P.grp.ptr, P.blk_grp.ptr, cur.ptr,
+                                                                 P.rows.ptr);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(cudaStreamSynchronize(st));
+  return FB_OK;
+}
+
+// transpose of a (block-local) CSR part on the device, rows sorted
+int device_transpose(int64_t n, const TriPart& S, TriPart& T, cudaStream_t st) {
+  DevBuf<int> cnt;
+  FB_TRY_CUDA(cnt.alloc(n));
+  FB_TRY_CUDA(cudaMemsetAsync(cnt.ptr, 0, n * sizeof(int), st));
+  csr_col_count_kernel<<<grid_for(n), 256, 0, st>>>(n, S.ip.ptr, S.ix.ptr, cnt.ptr);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(T.ip.alloc(n + 1));
+  int rc = exclusive_offsets(cnt.ptr, n, T.ip.ptr, st);
+  if (rc != FB_OK) return rc;
+  const int64_t nnz = S.ix.n;
+  FB_TRY_CUDA(T.ix.alloc(nnz));
+  FB_TRY_CUDA(T.v.alloc(nnz));
+  FB_TRY_CUDA(cudaMemsetAsync(cnt.ptr, 0, n * sizeof(int), st));
+  csr_transpose_fill_kernel<<<grid_for(n), 256, 0, st>>>(n, S.ip.ptr, S.ix.ptr, S.v.ptr, T.ip.ptr,
+                                                          cnt.ptr, T.ix.ptr, T.v.ptr);
+  FB_CHECK_LAUNCH();
+  csr_sort_rows_kernel<<<grid_for(n), 256, 0, st>>>(n, T.ip.ptr, T.ix.ptr, T.v.ptr);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+}  // namespace
+
+extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
+                                      const int64_t* block_ptr_host, int64_t* fail_row,
+                                      fb_blockilu** out) {
+  FB_REQUIRE(out != nullptr && fail_row != nullptr, "out is NULL");
+  *out = nullptr;
+  *fail_row = -1;
+  FB_REQUIRE(A != nullptr && block_ptr_host != nullptr, "bad block ILU input");
+  const int64_t n = A->nrows;
+  FB_REQUIRE(A->ncols == n, "block ILU needs a square matrix");
+  FB_REQUIRE(nblocks >= 1 && block_ptr_host[0] == 0 && block_ptr_host[nblocks] == n,
+             "block_ptr must cover all rows");
+  std::unique_ptr<fb_blockilu> B(new fb_blockilu());
+  B->n = n;
+  B->nblocks = int(nblocks);
+  for (int64_t b = 0; b < nblocks; ++b) {
+    FB_REQUIRE(block_ptr_host[b + 1] >= block_ptr_host[b], "block_ptr must be non-decreasing");
+    B->max_block = std::max<int64_t>(B->max_block, block_ptr_host[b + 1] - block_ptr_host[b]);
+  }
+  FB_REQUIRE(size_t(B->max_block) * 8 <= 200 * 1024, "block too large for shared memory");
+  cudaStream_t st = 0;
+  DevBuf<int64_t> bptr64;
+  FB_TRY_CUDA(bptr64.upload(block_ptr_host, nblocks + 1));
+  {
+    std::vector<int> b32(nblocks + 1);
+    for (int64_t b = 0; b <= nblocks; ++b) b32[b] = int(block_ptr_host[b]);
+    FB_TRY_CUDA(B->block_ptr.upload(b32.data(), nblocks + 1));
+  }
+  // block-diagonal part F of A
+  DevBuf<int> rb, cnt;
+  DevBuf<int64_t> fip, dpos;
+  DevBuf<int> fix;
+  DevBuf<double> fv;
+  DevBuf<unsigned long long> flag;
+  FB_TRY_CUDA(rb.alloc(n));
+  FB_TRY_CUDA(cnt.alloc(n));
+  FB_TRY_CUDA(flag.alloc(2));
+  FB_TRY_CUDA(cudaMemsetAsync(flag.ptr, 0xff, 2 * sizeof(unsigned long long), st));
+  bilu_row_block_kernel<<<grid_for(n), 256, 0, st>>>(n, nblocks, bptr64.ptr, rb.ptr);
+  FB_CHECK_LAUNCH();
+  bilu_count_kernel<<<grid_for(n), 256, 0, st>>>(n, A->indptr.ptr, A->indices.ptr, bptr64.ptr,
+                                                  rb.ptr, cnt.ptr);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(fip.alloc(n + 1));
+  int rc = exclusive_offsets(cnt.ptr, n, fip.ptr, st);
+  if (rc != FB_OK) return rc;
+  int64_t fnnz = 0;
+  FB_TRY_CUDA(cudaMemcpy(&fnnz, fip.ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  FB_TRY_CUDA(fix.alloc(fnnz));
+  FB_TRY_CUDA(fv.alloc(fnnz));
+  FB_TRY_CUDA(dpos.alloc(n));
+  bilu_fill_kernel<<<grid_for(n), 256, 0, st>>>(n, A->indptr.ptr, A->indices.ptr, A->data.ptr,
+                                                 bptr64.ptr, rb.ptr, fip.ptr, fix.ptr, fv.ptr,
+                                                 dpos.ptr, flag.ptr);
+  FB_CHECK_LAUNCH();
+  rb.reset();
+  unsigned long long h[2];
+  FB_TRY_CUDA(cudaMemcpy(h, flag.ptr, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h[0] != ~0ull) {  // a row without a stored diagonal: same outcome as the host factor
+    *fail_row = int64_t(h[0]);
+    return FB_OK;
+  }
+  bilu_factor_kernel<<<grid_for(nblocks, 64), 64, 0, st>>>(nblocks, bptr64.ptr, fip.ptr, fix.ptr,
+                                                           fv.ptr, dpos.ptr, flag.ptr + 1);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(cudaMemcpy(h, flag.ptr, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h[1] != ~0ull) {
+    *fail_row = int64_t(h[1]);
+    return FB_OK;
+  }
+  // split: L strict lower (unit diagonal), U strict upper + inverse diagonal
+  DevBuf<int> uc;
+  FB_TRY_CUDA(uc.alloc(n));
+  bilu_split_count_kernel<<<grid_for(n), 256, 0, st>>>(n, fip.ptr, dpos.ptr, cnt.ptr, uc.ptr);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(B->L.ip.alloc(n + 1));
+  FB_TRY_CUDA(B->U.ip.alloc(n + 1));
+  rc = exclusive_offsets(cnt.ptr, n, B->L.ip.ptr, st);
+  if (rc != FB_OK) return rc;
+  rc = exclusive_offsets(uc.ptr, n, B->U.ip.ptr, st);
+  if (rc != FB_OK) return rc;
+  int64_t lnnz = 0, unnz = 0;
+  FB_TRY_CUDA(cudaMemcpy(&lnnz, B->L.ip.ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  FB_TRY_CUDA(cudaMemcpy(&unnz, B->U.ip.ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  FB_TRY_CUDA(B->L.ix.alloc(lnnz));
+  FB_TRY_CUDA(B->L.v.alloc(lnnz));
+  FB_TRY_CUDA(B->U.ix.alloc(unnz));
+  FB_TRY_CUDA(B->U.v.alloc(unnz));
+  FB_TRY_CUDA(B->U.invdiag.alloc(n));
+  bilu_split_fill_kernel<<<grid_for(n), 256, 0, st>>>(n, fip.ptr, fix.ptr, fv.ptr, dpos.ptr,
+                                                       B->L.ip.ptr, B->L.ix.ptr, B->L.v.ptr,
+                                                       B->U.ip.ptr, B->U.ix.ptr, B->U.v.ptr,
+                                                       B->U.invdiag.ptr);
+  FB_CHECK_LAUNCH();
+  fix.reset();
+  fv.reset();
+  fip.reset();
+  dpos.reset();
+  cnt.reset();
+  uc.reset();
+  // transposed factors for the backward sweep
+  rc = device_transpose(n, B->U, B->Ut, st);
+  if (rc != FB_OK) return rc;
+  FB_TRY_CUDA(B->Ut.invdiag.alloc(n));
+  FB_TRY_CUDA(cudaMemcpyAsync(B->Ut.invdiag.ptr, B->U.invdiag.ptr, n * sizeof(double),
+                              cudaMemcpyDeviceToDevice, st));
+  rc = device_transpose(n, B->L, B->Lt, st);
+  if (rc != FB_OK) return rc;
+  // level groups: forward L (lower), U (upper); backward U^T (lower), L^T (upper)
+  rc = device_levels(n, nblocks, bptr64.ptr, B->L, true, st);
+  if (rc != FB_OK) return rc;
+  rc = device_levels(n, nblocks, bptr64.ptr, B->U, false, st);
+  if (rc != FB_OK) return rc;
+  rc = device_levels(n, nblocks, bptr64.ptr, B->Ut, true, st);
+  if (rc != FB_OK) return rc;
+  rc = device_levels(n, nblocks, bptr64.ptr, B->Lt, false, st);
+  if (rc != FB_OK) return rc;
+  FB_TRY_CUDA(cudaDeviceSynchronize());
+  *out = B.release();  // new2old stays empty: the level is block-major already
+  return FB_OK;
+}

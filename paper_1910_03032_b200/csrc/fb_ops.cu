@@ -7,6 +7,7 @@
 #include <memory>
 
 #include "fb_common.cuh"
+#include "fb_internal.cuh"
 #include "sf3_fast.cuh"
 #include "sf3_q1.cuh"
 #include "sf_general.cuh"
@@ -343,6 +344,13 @@ static int finish_operator(fb_operator* op, const double* points, const double* 
   }
   return FB_OK;
 }
+
+namespace fb {
+const int* restriction_map(const fb_restriction* r) { return r->map.ptr; }
+int restriction_nloc(const fb_restriction* r) { return r->nloc; }
+int64_t restriction_ne(const fb_restriction* r) { return r->ne; }
+int64_t restriction_ndofs(const fb_restriction* r) { return r->ndofs; }
+}  // namespace fb
 
 extern "C" {
 

@@ -20,12 +20,8 @@
 #include <memory>
 
 #include "fb_common.cuh"
+#include "fb_internal.cuh"
 
-struct fb_csr {
-  int64_t nrows = 0, ncols = 0, nnz = 0;
-  fb::DevBuf<int> indptr, indices;
-  fb::DevBuf<double> data;
-};
 
 struct fb_trisolve {
   int64_t n = 0;
@@ -54,15 +50,15 @@ static int g_trisolve_backoff = 64;  // ns between polls (sync-free mode)
 
 namespace fb {
 
-__global__ void csr_spmv_kernel(int64_t nrows, const int* __restrict__ ip,
+__global__ void csr_spmv_kernel(int64_t nrows, const int64_t* __restrict__ ip,
                                 const int* __restrict__ ix, const double* __restrict__ v,
                                 const double* __restrict__ x, const double* __restrict__ b,
                                 double* __restrict__ y) {
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
   double acc = 0.0;
-  const int e = __ldg(ip + r + 1);
-  for (int k = __ldg(ip + r); k < e; ++k)
+  const int64_t e = __ldg(ip + r + 1);
+  for (int64_t k = __ldg(ip + r); k < e; ++k)
     acc = __dadd_rn(acc, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ix + k))));
   y[r] = b ? __dsub_rn(__ldg(b + r), acc) : acc;
 }
@@ -163,8 +159,13 @@ int fb_csr_create(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* indp
   A->nrows = nrows;
   A->ncols = ncols;
   A->nnz = nnz;
-  int rc = upload_csr32(nrows, nnz, indptr, indices, A->indptr, A->indices);
-  if (rc != FB_OK) return rc;
+  FB_REQUIRE(ncols < (int64_t(1) << 31), "CSR too wide for int32 column indices");
+  {
+    std::vector<int> b(nnz);
+    for (int64_t i = 0; i < nnz; ++i) b[i] = int(indices[i]);
+    FB_TRY_CUDA(A->indices.upload(b.data(), nnz));
+  }
+  FB_TRY_CUDA(A->indptr.upload(indptr, nrows + 1));
   FB_TRY_CUDA(A->data.upload(data, nnz));
   *out = A.release();
   return FB_OK;

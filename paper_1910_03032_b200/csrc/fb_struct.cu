@@ -1,0 +1,456 @@
+// Structured-box setup and grid transfers on the device: the "scale mode"
+// LOR V-cycle of SURVEY.md 8(e'), with the setup moved off the host
+// (SURVEY.md 8(f) items 1-2).
+//
+// The reference builds every LOR level on the host: a Python/numpy Q1
+// assembly on the nodal sub-cell mesh (lor.py:61-81, mfop.py:496-528), a
+// COO->CSR conversion, SciPy nodal-interpolation matrices (lor.py:102-123)
+// and a numba ILU(0) (numba_backend.py:64-103) -- 55-70 s at 1M DoFs, and
+// out of reach at the 100M DoFs of cfg3.  For a structured box everything a
+// level needs follows from the lattice:
+//   * fb_lor_assemble_box: one thread per lattice point assembles its CSR row
+//     of the Q1 (2-point Gauss) matrix on the nodal sub-cell mesh, summing the
+//     row of each of its (up to 8) incident sub-cells; sub-cell vertices are
+//     evaluated from the parent element's trilinear map, like
+//     element_node_coords.  Columns are the 27-point lattice neighbours,
+//     sorted by DoF id; constrained rows/columns are zeroed with a unit
+//     diagonal (constrain_matrix, lor.py:84-99).
+//   * fb_transfer_*: the nodal interpolation between two levels applied
+//     matrix-free per fine element: prolongation writes each fine DoF once,
+//     from its first-touch owner element (the row the reference's
+//     nodal_interpolation builds from dof_owner_elem); restriction (P^T)
+//     accumulates per-element contributions and sums them with the coarse
+//     map's deterministic transposed-CSR E->L sum.  The same kernels serve
+//     p-transfers (same mesh, p -> p') and h-transfers (Q1 on a mesh -> Q1 on
+//     the 2x coarsened mesh) through per-axis weight tables.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "fb_common.cuh"
+#include "fb_internal.cuh"
+
+struct fb_transfer {
+  const fb_restriction* fine = nullptr;  // fine level map (ne, nf^3)
+  const fb_restriction* hmap = nullptr;  // coarse DoFs of each fine element's parent (ne, nc^3)
+  int nf = 0, nc = 0;
+  int64_t ne = 0, counts[3] = {0, 0, 0};
+  fb::DevBuf<double> W;   // (nw, nf, nc) weight tables
+  fb::DevBuf<int> widx;   // per axis, per element coordinate: table index
+  fb::DevBuf<double> E;   // (ne, nc^3) restriction contributions
+};
+
+namespace fb {
+
+__global__ void counts_to_i64_kernel(const int* __restrict__ c, int64_t n, int64_t* __restrict__ o) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i <= n) o[i] = i < n ? int64_t(c[i]) : 0;
+}
+
+int exclusive_offsets(const int* counts, int64_t n, int64_t* offsets, cudaStream_t st) {
+  counts_to_i64_kernel<<<ceil_div(n + 1, 256), 256, 0, st>>>(counts, n, offsets);
+  FB_CHECK_LAUNCH();
+  size_t bytes = 0;
+  FB_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, offsets, offsets, n + 1, st));
+  DevBuf<unsigned char> tmp;
+  FB_TRY_CUDA(tmp.alloc(int64_t(bytes)));
+  FB_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, bytes, offsets, offsets, n + 1, st));
+  FB_TRY_CUDA(cudaStreamSynchronize(st));  // tmp is freed on return
+  return FB_OK;
+}
+
+// ---- Q1 LOR assembly on the lattice -----------------------------------------
+
+struct BoxParams {
+  int p;
+  int64_t nx, ny, nz;   // element counts
+  int64_t Nx, Ny, Nz;   // lattice sizes (n_a p + 1)
+  const double* corners;  // (ne, 8, 3)
+  const int* lid;         // lattice -> DoF id, x fastest
+  int kind, constrain;
+  double nu, c;
+  double nodes[17];
+};
+
+__device__ __forceinline__ bool on_box_boundary(const BoxParams& P, int64_t gx, int64_t gy,
+                                                int64_t gz) {
+  return gx == 0 || gy == 0 || gz == 0 || gx == P.Nx - 1 || gy == P.Ny - 1 || gz == P.Nz - 1;
+}
+
+// physical position of lattice point (gx,gy,gz) through element (ex,ey,ez)
+__device__ void lattice_point(const BoxParams& P, int64_t ex, int64_t ey, int64_t ez, int64_t gx,
+                              int64_t gy, int64_t gz, double X[3]) {
+  const double* C = P.corners + ((ez * P.ny + ey) * P.nx + ex) * 24;
+  const double t[3] = {P.nodes[gx - ex * P.p], P.nodes[gy - ey * P.p], P.nodes[gz - ez * P.p]};
+  X[0] = X[1] = X[2] = 0.0;
+  for (int cc = 0; cc < 8; ++cc) {
+    double s = 1.0;
+    for (int a = 0; a < 3; ++a) s *= ((cc >> a) & 1) ? (1.0 + t[a]) / 2.0 : (1.0 - t[a]) / 2.0;
+    for (int d = 0; d < 3; ++d) X[d] += s * C[cc * 3 + d];
+  }
+}
+
+// row `vi` of the trilinear sub-cell matrix with vertices X (2-point Gauss)
+__device__ void q1_row(const double X[8][3], int vi, int kind, double nu, double c, double K[8]) {
+  const double g = 0.57735026918962576451;  // 1/sqrt(3)
+  for (int w = 0; w < 8; ++w) K[w] = 0.0;
+  for (int q = 0; q < 8; ++q) {
+    const double xi[3] = {(q & 1) ? g : -g, (q & 2) ? g : -g, (q & 4) ? g : -g};
+    double N[8], dN[8][3];
+    for (int v = 0; v < 8; ++v) {
+      double f[3], df[3];
+      for (int a = 0; a < 3; ++a) {
+        const bool hi = (v >> a) & 1;
+        f[a] = hi ? (1.0 + xi[a]) / 2.0 : (1.0 - xi[a]) / 2.0;
+        df[a] = hi ? 0.5 : -0.5;
+      }
+      N[v] = f[0] * f[1] * f[2];
+      dN[v][0] = df[0] * f[1] * f[2];
+      dN[v][1] = f[0] * df[1] * f[2];
+      dN[v][2] = f[0] * f[1] * df[2];
+    }
+    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int v = 0; v < 8; ++v)
+      for (int d = 0; d < 3; ++d)
+        for (int b = 0; b < 3; ++b) J[d][b] += dN[v][b] * X[v][d];
+    const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                       J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                       J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    double Ji[3][3];
+    Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / det;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+    Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / det;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+    Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+    if (kind != FB_STIFFNESS) {
+      const double wm = (kind == FB_HELMHOLTZ) ? c * det : det;
+      for (int w = 0; w < 8; ++w) K[w] += N[vi] * wm * N[w];
+    }
+    if (kind != FB_MASS) {
+      double Wm[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          Wm[a][b] = nu * det * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+      double gi[3];
+      for (int b = 0; b < 3; ++b)
+        gi[b] = dN[vi][0] * Wm[0][b] + dN[vi][1] * Wm[1][b] + dN[vi][2] * Wm[2][b];
+      for (int w = 0; w < 8; ++w) K[w] += gi[0] * dN[w][0] + gi[1] * dN[w][1] + gi[2] * dN[w][2];
+    }
+  }
+}
+
+__device__ __forceinline__ int axis_span(int64_t g, int64_t N) { return 1 + (g > 0) + (g < N - 1); }
+
+__global__ void lor_box_count_kernel(BoxParams P, int* __restrict__ cnt) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = P.Nx * P.Ny * P.Nz;
+  if (t >= total) return;
+  const int64_t gx = t % P.Nx, gy = (t / P.Nx) % P.Ny, gz = t / (P.Nx * P.Ny);
+  cnt[P.lid[t]] = axis_span(gx, P.Nx) * axis_span(gy, P.Ny) * axis_span(gz, P.Nz);
+}
+
+__global__ void __launch_bounds__(128) lor_box_fill_kernel(BoxParams P,
+                                                           const int64_t* __restrict__ ip,
+                                                           int* __restrict__ ix,
+                                                           double* __restrict__ v) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = P.Nx * P.Ny * P.Nz;
+  if (t >= total) return;
+  const int64_t g[3] = {t % P.Nx, (t / P.Nx) % P.Ny, t / (P.Nx * P.Ny)};
+  const int64_t N[3] = {P.Nx, P.Ny, P.Nz};
+  const int64_t ne_[3] = {P.nx, P.ny, P.nz};
+  const bool brow = P.constrain && on_box_boundary(P, g[0], g[1], g[2]);
+  double acc[27];
+  for (int k = 0; k < 27; ++k) acc[k] = 0.0;
+  if (!brow) {
+    // incident sub-cells: min corner m = g - s, s in {0,1}^3, in ascending s
+    for (int s = 0; s < 8; ++s) {
+      int64_t m[3];
+      bool ok = true;
+      for (int a = 0; a < 3; ++a) {
+        m[a] = g[a] - ((s >> a) & 1);
+        ok = ok && m[a] >= 0 && m[a] <= N[a] - 2;
+      }
+      if (!ok) continue;
+      int64_t e[3];
+      for (int a = 0; a < 3; ++a) e[a] = min(m[a] / P.p, ne_[a] - 1);
+      double X[8][3];
+      for (int w = 0; w < 8; ++w)
+        lattice_point(P, e[0], e[1], e[2], m[0] + (w & 1), m[1] + ((w >> 1) & 1),
+                      m[2] + ((w >> 2) & 1), X[w]);
+      double K[8];
+      q1_row(X, s, P.kind, P.nu, P.c, K);
+      for (int w = 0; w < 8; ++w) {
+        // neighbour offset of vertex w relative to g, in {-1,0,1}^3
+        const int dx = (w & 1) - (s & 1), dy = ((w >> 1) & 1) - ((s >> 1) & 1),
+                  dz = ((w >> 2) & 1) - ((s >> 2) & 1);
+        acc[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)] += K[w];
+      }
+    }
+  }
+  // gather the row's (column, value) pairs and insertion-sort them by column
+  int cols[27];
+  double vals[27];
+  int m = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int64_t hx = g[0] + dx, hy = g[1] + dy, hz = g[2] + dz;
+        if (hx < 0 || hy < 0 || hz < 0 || hx >= N[0] || hy >= N[1] || hz >= N[2]) continue;
+        const int col = P.lid[(hz * N[1] + hy) * N[0] + hx];
+        double val = acc[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)];
+        if (brow) val = (dx == 0 && dy == 0 && dz == 0) ? 1.0 : 0.0;
+        else if (P.constrain && on_box_boundary(P, hx, hy, hz)) val = 0.0;
+        int j = m - 1;
+        while (j >= 0 && cols[j] > col) {
+          cols[j + 1] = cols[j];
+          vals[j + 1] = vals[j];
+          --j;
+        }
+        cols[j + 1] = col;
+        vals[j + 1] = val;
+        ++m;
+      }
+  const int64_t base = ip[P.lid[t]];
+  for (int k = 0; k < m; ++k) {
+    ix[base + k] = cols[k];
+    v[base + k] = vals[k];
+  }
+}
+
+// ---- matrix-free nodal interpolation between levels -------------------------
+
+struct TransferView {
+  const int* fmap;   // (ne, nf^3)
+  const int* hmap;   // (ne, nc^3)
+  const double* W;   // (nw, nf, nc)
+  const int* widx;   // [nx | ny | nz]
+  int64_t nx, ny, nz;
+  int nf, nc;
+};
+
+// fine element e: per-axis coordinates and weight tables
+__device__ __forceinline__ void transfer_elem(const TransferView& T, int64_t e, int64_t ec[3],
+                                              const double* Wa[3]) {
+  ec[0] = e % T.nx;
+  ec[1] = (e / T.nx) % T.ny;
+  ec[2] = e / (T.nx * T.ny);
+  const int64_t off[3] = {0, T.nx, T.nx + T.ny};
+  for (int a = 0; a < 3; ++a) Wa[a] = T.W + int64_t(T.widx[off[a] + ec[a]]) * T.nf * T.nc;
+}
+
+// first-touch ownership on a structured box: local lattice index 0 along an
+// axis belongs to the lower neighbour unless the element is the first one
+__device__ __forceinline__ bool owned_local(const int64_t ec[3], int l0, int l1, int l2) {
+  return (l0 > 0 || ec[0] == 0) && (l1 > 0 || ec[1] == 0) && (l2 > 0 || ec[2] == 0);
+}
+
+__global__ void transfer_prolong_kernel(TransferView T, const double* __restrict__ xc,
+                                        double* __restrict__ xf) {
+  __shared__ double xe[125];
+  __shared__ double w[3][9 * 5];
+  const int64_t e = blockIdx.x;
+  int64_t ec[3];
+  const double* Wa[3];
+  transfer_elem(T, e, ec, Wa);
+  const int nc3 = T.nc * T.nc * T.nc, nf3 = T.nf * T.nf * T.nf;
+  for (int j = threadIdx.x; j < nc3; j += blockDim.x) xe[j] = xc[T.hmap[e * nc3 + j]];
+  for (int j = threadIdx.x; j < T.nf * T.nc; j += blockDim.x)
+    for (int a = 0; a < 3; ++a) w[a][j] = Wa[a][j];
+  __syncthreads();
+  for (int l = threadIdx.x; l < nf3; l += blockDim.x) {
+    const int l0 = l % T.nf, l1 = (l / T.nf) % T.nf, l2 = l / (T.nf * T.nf);
+    if (!owned_local(ec, l0, l1, l2)) continue;
+    double acc = 0.0;
+    for (int c = 0; c < T.nc; ++c) {
+      double ab = 0.0;
+      for (int b = 0; b < T.nc; ++b) {
+        double aa = 0.0;
+        for (int a = 0; a < T.nc; ++a) aa += w[0][l0 * T.nc + a] * xe[(c * T.nc + b) * T.nc + a];
+        ab += w[1][l1 * T.nc + b] * aa;
+      }
+      acc += w[2][l2 * T.nc + c] * ab;
+    }
+    xf[T.fmap[e * nf3 + l]] = acc;
+  }
+}
+
+__global__ void transfer_restrict_kernel(TransferView T, const double* __restrict__ xf,
+                                         double* __restrict__ E) {
+  __shared__ double rf[729];
+  __shared__ double w[3][9 * 5];
+  const int64_t e = blockIdx.x;
+  int64_t ec[3];
+  const double* Wa[3];
+  transfer_elem(T, e, ec, Wa);
+  const int nc3 = T.nc * T.nc * T.nc, nf3 = T.nf * T.nf * T.nf;
+  for (int l = threadIdx.x; l < nf3; l += blockDim.x) {
+    const int l0 = l % T.nf, l1 = (l / T.nf) % T.nf, l2 = l / (T.nf * T.nf);
+    rf[l] = owned_local(ec, l0, l1, l2) ? xf[T.fmap[e * nf3 + l]] : 0.0;
+  }
+  for (int j = threadIdx.x; j < T.nf * T.nc; j += blockDim.x)
+    for (int a = 0; a < 3; ++a) w[a][j] = Wa[a][j];
+  __syncthreads();
+  for (int j = threadIdx.x; j < nc3; j += blockDim.x) {
+    const int j0 = j % T.nc, j1 = (j / T.nc) % T.nc, j2 = j / (T.nc * T.nc);
+    double acc = 0.0;
+    for (int l2 = 0; l2 < T.nf; ++l2) {
+      double s1 = 0.0;
+      for (int l1 = 0; l1 < T.nf; ++l1) {
+        double s0 = 0.0;
+        for (int l0 = 0; l0 < T.nf; ++l0) s0 += w[0][l0 * T.nc + j0] * rf[(l2 * T.nf + l1) * T.nf + l0];
+        s1 += w[1][l1 * T.nc + j1] * s0;
+      }
+      acc += w[2][l2 * T.nc + j2] * s1;
+    }
+    E[e * nc3 + j] = acc;
+  }
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" {
+
+int fb_lor_assemble_box(int p, const int64_t* counts, const double* corners_dev,
+                        const double* nodes, const int* lattice_ids_dev, int kind, double nu,
+                        double c, int constrain_boundary, fb_csr** out) {
+  FB_REQUIRE(out != nullptr, "out is NULL");
+  *out = nullptr;
+  FB_REQUIRE(p >= 1 && p <= 16, "degree must be in [1, 16]");
+  FB_REQUIRE(counts && corners_dev && nodes && lattice_ids_dev, "NULL argument");
+  FB_REQUIRE(kind >= FB_MASS && kind <= FB_HELMHOLTZ, "unsupported LOR kind");
+  FB_REQUIRE(counts[0] >= 1 && counts[1] >= 1 && counts[2] >= 1, "cell counts must be positive");
+  BoxParams P{};
+  P.p = p;
+  P.nx = counts[0];
+  P.ny = counts[1];
+  P.nz = counts[2];
+  P.Nx = P.nx * p + 1;
+  P.Ny = P.ny * p + 1;
+  P.Nz = P.nz * p + 1;
+  P.corners = corners_dev;
+  P.lid = lattice_ids_dev;
+  P.kind = kind;
+  P.constrain = constrain_boundary ? 1 : 0;
+  P.nu = nu;
+  P.c = c;
+  for (int i = 0; i <= p; ++i) P.nodes[i] = nodes[i];
+  const int64_t n = P.Nx * P.Ny * P.Nz;
+  FB_REQUIRE(n < (int64_t(1) << 31), "lattice exceeds int32 DoF ids");
+  std::unique_ptr<fb_csr> A(new fb_csr());
+  A->nrows = A->ncols = n;
+  cudaStream_t st = 0;
+  DevBuf<int> cnt;
+  FB_TRY_CUDA(cnt.alloc(n));
+  lor_box_count_kernel<<<ceil_div(n, 256), 256, 0, st>>>(P, cnt.ptr);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(A->indptr.alloc(n + 1));
+  int rc = exclusive_offsets(cnt.ptr, n, A->indptr.ptr, st);
+  if (rc != FB_OK) return rc;
+  cnt.reset();
+  FB_TRY_CUDA(cudaMemcpy(&A->nnz, A->indptr.ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  FB_TRY_CUDA(A->indices.alloc(A->nnz));
+  FB_TRY_CUDA(A->data.alloc(A->nnz));
+  lor_box_fill_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P, A->indptr.ptr, A->indices.ptr,
+                                                        A->data.ptr);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(cudaDeviceSynchronize());
+  *out = A.release();
+  return FB_OK;
+}
+
+int fb_csr_info(const fb_csr* A, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+  FB_REQUIRE(A != nullptr, "matrix is NULL");
+  if (nrows) *nrows = A->nrows;
+  if (ncols) *ncols = A->ncols;
+  if (nnz) *nnz = A->nnz;
+  return FB_OK;
+}
+
+int fb_csr_download(const fb_csr* A, int64_t* indptr, int64_t* indices, double* data) {
+  FB_REQUIRE(A != nullptr && indptr && indices && data, "NULL argument");
+  FB_TRY_CUDA(cudaMemcpy(indptr, A->indptr.ptr, (A->nrows + 1) * sizeof(int64_t),
+                         cudaMemcpyDeviceToHost));
+  std::vector<int> ix(A->nnz);
+  if (A->nnz) {
+    FB_TRY_CUDA(cudaMemcpy(ix.data(), A->indices.ptr, A->nnz * sizeof(int), cudaMemcpyDeviceToHost));
+    FB_TRY_CUDA(cudaMemcpy(data, A->data.ptr, A->nnz * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  for (int64_t k = 0; k < A->nnz; ++k) indices[k] = ix[k];
+  return FB_OK;
+}
+
+int fb_transfer_create(const fb_restriction* fine, const fb_restriction* hmap,
+                       const int64_t* counts, int nw, const double* W, const int64_t* widx,
+                       fb_transfer** out) {
+  FB_REQUIRE(out != nullptr, "out is NULL");
+  *out = nullptr;
+  FB_REQUIRE(fine && hmap && counts && W && widx && nw >= 1, "NULL argument");
+  const int64_t ne = restriction_ne(fine);
+  FB_REQUIRE(restriction_ne(hmap) == ne, "fine and coarse maps must list the same elements");
+  FB_REQUIRE(counts[0] * counts[1] * counts[2] == ne, "counts do not match the element count");
+  const int nf3 = restriction_nloc(fine), nc3 = restriction_nloc(hmap);
+  int nf = 1, nc = 1;
+  while (nf * nf * nf < nf3) ++nf;
+  while (nc * nc * nc < nc3) ++nc;
+  FB_REQUIRE(nf * nf * nf == nf3 && nc * nc * nc == nc3, "transfers need 3D tensor maps");
+  FB_REQUIRE(nf <= 9 && nc <= 5, "transfer sizes beyond p = 8 -> 4 are not supported");
+  std::unique_ptr<fb_transfer> T(new fb_transfer());
+  T->fine = fine;
+  T->hmap = hmap;
+  T->nf = nf;
+  T->nc = nc;
+  T->ne = ne;
+  for (int a = 0; a < 3; ++a) T->counts[a] = counts[a];
+  const int64_t nidx = counts[0] + counts[1] + counts[2];
+  std::vector<int> wi(nidx);
+  for (int64_t i = 0; i < nidx; ++i) {
+    FB_REQUIRE(widx[i] >= 0 && widx[i] < nw, "weight table index out of range");
+    wi[i] = int(widx[i]);
+  }
+  FB_TRY_CUDA(T->widx.upload(wi.data(), nidx));
+  FB_TRY_CUDA(T->W.upload(W, int64_t(nw) * nf * nc));
+  FB_TRY_CUDA(T->E.alloc(ne * nc3));
+  *out = T.release();
+  return FB_OK;
+}
+
+void fb_transfer_destroy(fb_transfer* T) { delete T; }
+
+static TransferView transfer_view(const fb_transfer* T) {
+  return TransferView{restriction_map(T->fine), restriction_map(T->hmap), T->W.ptr, T->widx.ptr,
+                      T->counts[0], T->counts[1], T->counts[2], T->nf, T->nc};
+}
+
+// xf (fine L-vector) = P xc: every fine DoF written once, by its owner element
+int fb_transfer_prolong(const fb_transfer* T, const double* xc, double* xf, void* stream) {
+  FB_REQUIRE(T != nullptr, "transfer is NULL");
+  if (T->ne == 0) return FB_OK;
+  FB_REQUIRE(T->ne < (int64_t(1) << 31), "too many elements");
+  transfer_prolong_kernel<<<int(T->ne), 128, 0, as_stream(stream)>>>(transfer_view(T), xc, xf);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+// xc (coarse L-vector) = P^T xf, deterministic (per-element contributions,
+// then the coarse map's transposed-CSR sum)
+int fb_transfer_restrict(const fb_transfer* T, const double* xf, double* xc, void* stream) {
+  FB_REQUIRE(T != nullptr, "transfer is NULL");
+  if (T->ne == 0) return FB_OK;
+  FB_REQUIRE(T->ne < (int64_t(1) << 31), "too many elements");
+  transfer_restrict_kernel<<<int(T->ne), 128, 0, as_stream(stream)>>>(transfer_view(T), xf,
+                                                                       T->E.ptr);
+  FB_CHECK_LAUNCH();
+  return fb_restriction_scatter_add(T->hmap, T->E.ptr, xc, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+"""Structured-box scale mode (paper_1910_03032_b200/structured.py).
+
+CPU: the block-major first-touch numbering is a renumbering of the
+reference's numbering whose block order is exactly the parity path's
+block-ILU order; coarsening / h-transfer tables.
+GPU: device-built LOR matrices, block-ILU factors and transfers against the
+host/reference constructions on the reference numbering; scale-mode LOR-PCG
+iteration counts against the reference's golden counts."""
+
+import numpy as np
+import pytest
+
+from tests.cases import load, manifest, rel_err
+
+BOXES = [((3, 2, 2), 2, 2), ((5, 4, 3), 3, 2), ((4, 4, 4), 4, 2), ((3, 3, 5), 1, 4),
+         ((7, 5, 3), 2, 3), ((2, 3, 2), 7, 2)]
+
+
+def _perm(counts, p, block, perturb=0.0, seed=11):
+    from paper_1910_03032_b200 import geometry, spaces, structured as S
+    m = geometry.cartesian_mesh(counts)
+    if perturb:
+        m = geometry.perturb_mesh(m, perturb, seed=seed)  # tests/cases.build's seed
+    ref = spaces.FESpace(m, p)
+    ids, bptr = S.box_lattice_ids(counts, p, block)
+    ed = S.lattice_element_dofs(ids, p).numpy()
+    perm = np.full(ref.ndofs_scalar, -1, dtype=np.int64)
+    perm[ref.element_dofs.ravel()] = ed.ravel()
+    return m, ref, ed, perm, bptr
+
+
+@pytest.mark.parametrize("counts,p,block", BOXES)
+def test_box_numbering_is_block_major_first_touch(counts, p, block):
+    from paper_1910_03032_b200 import lor, solvers
+    m, ref, ed, perm, bptr = _perm(counts, p, block)
+    n = ref.ndofs_scalar
+    assert np.array_equal(np.sort(perm), np.arange(n))
+    assert np.array_equal(perm[ref.element_dofs], ed)  # a consistent renumbering
+    # the parity path's block-ILU order (solvers.BlockILU0Smoother) is the identity here
+    order = lor.first_touch_ordering(ref)
+    blk = solvers.element_block_ids(m, block)[ref.dof_owner_elem]
+    new2old = order[np.argsort(blk[order], kind="stable")]
+    assert np.array_equal(perm[new2old], np.arange(n))
+    bnew = blk[new2old]
+    starts = np.flatnonzero(np.r_[True, bnew[1:] != bnew[:-1]])
+    assert np.array_equal(np.r_[starts, n], bptr)
+
+
+def test_coarsen_box_and_h_tables():
+    from paper_1910_03032_b200 import geometry, structured as S
+    m = geometry.perturb_mesh(geometry.cartesian_mesh((5, 4, 3)), 0.05, seed=2)
+    c = S.coarsen_box(m)
+    assert c.counts == (3, 2, 2)
+    V = m.vertices.reshape(4, 5, 6, 3)
+    Vc = c.vertices.reshape(3, 3, 4, 3)
+    assert np.array_equal(Vc[1, 1, 1], V[2, 2, 2])
+    assert np.array_equal(Vc[-1, -1, -1], V[-1, -1, -1])  # odd count: last cell spans one
+    assert np.array_equal(c.corners, c.vertices[c.elements])
+    tables, idx, parent = S.h_transfer_tables(5)
+    assert list(parent) == [0, 0, 1, 1, 2] and list(idx) == [0, 1, 0, 1, 2]
+    # interpolation weights reproduce linear functions of the lattice index
+    for i in range(5):
+        for loc in (0, 1):
+            f = i + loc
+            w = tables[idx[i]][loc]
+            c0 = 2 * parent[i]
+            c1 = min(c0 + 2, 5)
+            assert w[0] * c0 + w[1] * c1 == pytest.approx(f)
+
+
+# ---------------------------------------------------------------------------- GPU
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [1, 2, 4, 7])
+def test_device_lor_matrix_matches_host_assembly(p):
+    import torch
+    from paper_1910_03032_b200 import lor, structured as S
+    counts = (3, 2, 4) if p < 7 else (2, 2, 2)
+    m, ref, ed, perm, bptr = _perm(counts, p, 2, perturb=0.05)
+    space = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
+    A = S.DeviceLevelMatrix(space, "helmholtz", nu=1.0, c=10.0).to_scipy()
+    Ah = lor.lor_matrix(ref, "helmholtz", nu=1.0, c=10.0, constrained=ref.boundary_dof_set())
+    P = np.argsort(perm)  # new -> ref
+    Ar = Ah[P][:, P].tocsr()
+    Ar.sort_indices()
+    assert A.nnz == Ar.nnz
+    assert np.array_equal(A.indptr, Ar.indptr) and np.array_equal(A.indices, Ar.indices)
+    assert np.max(np.abs(A.data - Ar.data)) <= 1e-13 * np.max(np.abs(Ar.data))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 4])
+def test_device_block_ilu_matches_parity_smoother(p):
+    import torch
+    from paper_1910_03032_b200 import lor, solvers, structured as S
+    counts = (4, 3, 4)
+    m, ref, ed, perm, bptr = _perm(counts, p, 2, perturb=0.05)
+    space = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
+    Ad = S.DeviceLevelMatrix(space, "helmholtz", nu=1.0, c=10.0)
+    sm = S.DeviceBlockILU0(Ad, space.block_ptr)
+    P = np.argsort(perm)
+    A_ref = Ad.to_scipy()[perm][:, perm].tocsr()  # same values, reference numbering
+    host = solvers.BlockILU0Smoother(A_ref, ref, lor.first_touch_ordering(ref), 2)
+    r = np.random.default_rng(5).standard_normal(ref.ndofs_scalar)
+    rn = r[P]
+    for f in ("forward", "backward"):
+        got = getattr(sm, f)(rn)
+        want = getattr(host, f)(r)[P]
+        assert rel_err(got, want) < 1e-14, f
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 4, 7])
+def test_p_transfer_matches_nodal_interpolation(p):
+    import torch
+    from paper_1910_03032_b200 import device as dev, lor, spaces, structured as S
+    counts = (3, 2, 3) if p < 7 else (2, 2, 2)
+    m, ref, ed, perm, bptr = _perm(counts, p, 2)
+    pc = max(1, (p + 1) // 2)
+    refc = spaces.FESpace(m, pc)
+    idsc, _ = S.box_lattice_ids(counts, pc, 2)
+    permc = np.full(refc.ndofs_scalar, -1, dtype=np.int64)
+    permc[refc.element_dofs.ravel()] = S.lattice_element_dofs(idsc, pc).numpy().ravel()
+    Pm = lor.nodal_interpolation(ref, refc)
+    fine = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
+    coarse = S.BoxSpace(m, pc, block=2 if pc > 1 else 4, device=torch.device("cuda"))
+    T = S.BoxTransfer(fine, coarse)
+    rng = np.random.default_rng(1)
+    xc = rng.standard_normal(refc.ndofs_scalar)
+    xf = rng.standard_normal(ref.ndofs_scalar)
+    want_f = Pm @ xc
+    want_c = Pm.T @ xf
+    out_f = torch.empty(ref.ndofs_scalar, dtype=torch.float64, device="cuda")
+    out_c = torch.empty(refc.ndofs_scalar, dtype=torch.float64, device="cuda")
+    xc_n = np.empty_like(xc); xc_n[permc] = xc
+    xf_n = np.empty_like(xf); xf_n[perm] = xf
+    T.prolong_into(dev.to_device(xc_n), out_f)
+    T.restrict_into(dev.to_device(xf_n), out_c)
+    assert rel_err(out_f.cpu().numpy()[perm], want_f) < 1e-13
+    assert rel_err(out_c.cpu().numpy()[permc], want_c) < 1e-13
+
+
+@pytest.mark.gpu
+def test_h_transfer_adjoint_and_linear_reproduction():
+    import torch
+    from paper_1910_03032_b200 import device as dev, geometry, structured as S
+    m = geometry.cartesian_mesh((5, 4, 6))
+    fine = S.BoxSpace(m, 1, block=4, device=torch.device("cuda"))
+    coarse = S.BoxSpace(S.coarsen_box(m), 1, block=4, device=torch.device("cuda"))
+    T = S.BoxTransfer(fine, coarse)
+    # linear function of the lattice index is reproduced
+    def lattice_fun(space, scale):
+        L = space.lattice_ids.cpu().numpy()
+        gz, gy, gx = np.indices(L.shape)
+        v = np.empty(space.ndofs_scalar)
+        v[L.ravel()] = (1.0 + 2.0 * gx * scale[0] - 0.5 * gy * scale[1] + 3.0 * gz * scale[2]).ravel()
+        return v
+    fx, _ = S._coarse_vertex_index(5)
+    fy, _ = S._coarse_vertex_index(4)
+    fz, _ = S._coarse_vertex_index(6)
+    Lc = coarse.lattice_ids.cpu().numpy()
+    vc = np.empty(coarse.ndofs_scalar)
+    gz, gy, gx = np.indices(Lc.shape)
+    vc[Lc.ravel()] = (1.0 + 2.0 * fx[gx] - 0.5 * fy[gy] + 3.0 * fz[gz]).ravel()
+    out = torch.empty(fine.ndofs_scalar, dtype=torch.float64, device="cuda")
+    T.prolong_into(dev.to_device(vc), out)
+    assert rel_err(out.cpu().numpy(), lattice_fun(fine, (1, 1, 1))) < 1e-14
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal(coarse.ndofs_scalar)
+    b = rng.standard_normal(fine.ndofs_scalar)
+    Pa = torch.empty(fine.ndofs_scalar, dtype=torch.float64, device="cuda")
+    Ptb = torch.empty(coarse.ndofs_scalar, dtype=torch.float64, device="cuda")
+    T.prolong_into(dev.to_device(a), Pa)
+    T.restrict_into(dev.to_device(b), Ptb)
+    lhs = float(Pa.cpu().numpy() @ b)
+    rhs = float(a @ Ptb.cpu().numpy())
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 4])
+def test_box_operator_is_permuted_reference_operator(p):
+    import torch
+    from paper_1910_03032_b200 import geometry, mfop, structured as S
+    counts = (3, 4, 2)
+    m, ref, ed, perm, bptr = _perm(counts, p, 2, perturb=0.05)
+    space = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
+    geom = geometry.DeviceGeometry(m, space.basis.quad)
+    op = mfop.HelmholtzOperator(space, geom, c=10.0)
+    op_ref = mfop.HelmholtzOperator(ref, geometry.DeviceGeometry(m, ref.basis.quad), c=10.0)
+    x = np.random.default_rng(2).standard_normal(ref.ndofs_scalar)
+    xn = np.empty_like(x)
+    xn[perm] = x
+    assert rel_err(op.apply(xn)[perm], op_ref.apply(x)) < 1e-13
+
+
+SOLVE = {c["name"]: c for c in manifest()["solvers"]}
+BOX_CASES = ["3d_p4_helmholtz", "3d_p7_helmholtz", "3d_p2_stiffness_pert"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", BOX_CASES)
+@pytest.mark.parametrize("max_coarse", [20000, 100])
+def test_box_lor_pcg_iterations_vs_reference(name, max_coarse):
+    """Scale mode (device-built hierarchy, block ILU) against the reference's
+    golden counts: +-1 with the exact Q1 solve; with the geometric Q1
+    coarsening (max_coarse=100 forces h-levels) within +3."""
+    import torch
+    from paper_1910_03032_b200 import geometry, mfop, solvers, structured as S
+    c = SOLVE[name]
+    gold = load("solvers")
+    counts = tuple(c["counts"])
+    m, ref, ed, perm, bptr = _perm(counts, c["p"], 2, perturb=c["perturb"])
+    space = S.BoxSpace(m, c["p"], block=2, device=torch.device("cuda"))
+    geom = geometry.DeviceGeometry(m, space.basis.quad)
+    kw = {"stiffness": {"nu": 1.0}, "helmholtz": {"c": c["c"], "nu": 1.0}}[c["kind"]]
+    op = mfop.setup(c["kind"], space=space, geom=geom, **kw)
+    bdr = space.boundary_dof_set()
+    A = mfop.ConstrainedOperator(op, bdr)
+    pre = S.BoxLORPreconditioner(space, c["kind"], nu=1.0, c=c["c"], max_coarse=max_coarse)
+    if max_coarse == 100:
+        assert pre.spaces[-1].mesh is not m  # h-levels present
+    bdr_ref = ref.boundary_dof_set()
+    for seed, its_ref in zip(c["seeds"], c["iterations"]):
+        b = np.random.default_rng(seed).standard_normal(ref.ndofs)
+        b[bdr_ref] = 0.0
+        bn = np.empty_like(b)
+        bn[perm] = b
+        x, rep = solvers.cg(A, bn, precond=pre,
+                            config=solvers.SolverConfig(rel_tol=1e-8, max_iters=300))
+        assert rep.converged
+        slack = 1 if max_coarse == 20000 else 3
+        assert its_ref - 1 <= rep.iterations <= its_ref + slack, (rep.iterations, its_ref)
+        assert rel_err(x[perm], gold[f"{name}/x{seed}"]) < 1e-6
