@@ -37,6 +37,8 @@ struct TriPart {
 
 }  // namespace
 
+static int g_bilu_pipe = 1;
+
 struct fb_blockilu {
   int64_t n = 0;
   int nblocks = 0;
@@ -58,34 +60,128 @@ struct TriView {
   const int* blk_grp;
 };
 
-__device__ __forceinline__ void block_tri(const TriView& T, int b, int bs, double* y) {
-  const int g0 = T.blk_grp[b], g1 = T.blk_grp[b + 1];
-  for (int g = g0; g < g1; ++g) {
-    const int r0 = T.grp[g], r1 = T.grp[g + 1];
-    for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) {
-      const int row = T.rows[k];
-      double acc = 0.0;
-      for (int64_t e = T.ip[row]; e < T.ip[row + 1]; ++e)
-        acc = __dadd_rn(acc, __dmul_rn(T.v[e], y[T.ix[e] - bs]));
-      const double r = __dsub_rn(y[row - bs], acc);
-      y[row - bs] = T.invdiag ? __dmul_rn(r, T.invdiag[row]) : r;
-    }
-    __syncthreads();
+constexpr int kRowBuf = 13;  // strict triangle of a 27-point row: <= 13 entries
+
+struct RowLoad {
+  int c[kRowBuf];
+  double a[kRowBuf];
+  int n, row;
+  int64_t e0;
+  double inv;
+};
+
+__device__ __forceinline__ void bulk_prefetch_range(const void* p, int64_t bytes) {
+  uintptr_t b = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + uintptr_t(bytes) + 15) & ~uintptr_t(15);
+  while (b < e) {
+    const uint32_t len = uint32_t((e - b) > (1u << 20) ? (1u << 20) : (e - b));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b), "r"(len) : "memory");
+    b += len;
   }
 }
 
-__global__ void block_ilu_kernel(const int* __restrict__ block_ptr,
-                                 const int* __restrict__ new2old, TriView A, TriView B,
-                                 const double* __restrict__ r, double* __restrict__ out) {
+// Issue the loads of one row (position k of the block's level order); all
+// addresses come from shared memory, so the loads of the next level are in
+// flight while the current level computes.
+__device__ __forceinline__ void row_issue(const TriView& T, const unsigned short* srow,
+                                          const int* soff, int64_t ebase, int bs, int k,
+                                          RowLoad& R) {
+  const int lr = srow[k];
+  R.row = bs + lr;
+  R.e0 = ebase + soff[lr];
+  R.n = soff[lr + 1] - soff[lr];
+#pragma unroll
+  for (int u = 0; u < kRowBuf; ++u) {
+    const bool ok = u < R.n;
+    R.c[u] = ok ? __ldg(T.ix + R.e0 + u) : bs;
+    R.a[u] = ok ? __ldg(T.v + R.e0 + u) : 0.0;
+  }
+  R.inv = T.invdiag ? __ldg(T.invdiag + R.row) : 1.0;
+}
+
+__device__ __forceinline__ void row_finish(const TriView& T, const RowLoad& R, int bs, double* y) {
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < kRowBuf; ++u)
+    if (u < R.n) acc = __dadd_rn(acc, __dmul_rn(R.a[u], y[R.c[u] - bs]));
+  for (int u = kRowBuf; u < R.n; ++u)  // longer rows (not produced by 27-point LOR levels)
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(T.v + R.e0 + u), y[__ldg(T.ix + R.e0 + u) - bs]));
+  const double r = __dsub_rn(y[R.row - bs], acc);
+  y[R.row - bs] = T.invdiag ? __dmul_rn(r, R.inv) : r;
+}
+
+// One triangular solve of block b by ONE warp, level by level in shared
+// memory (__syncwarp between levels).  The block's level groups,
+// level-ordered local rows and entry offsets are staged in shared memory and
+// its factor entries prefetched into L2; with PIPE the loads of level g+1 are
+// issued before level g computes.  Every row's sum stays sequential in index
+// order (bitwise the host sweep).
+template <bool PIPE>
+__device__ __forceinline__ void block_tri(const TriView& T, int b, int bs, int nb, double* y,
+                                          int* sgrp, unsigned short* srow, int* soff) {
+  const int g0 = T.blk_grp[b], G = T.blk_grp[b + 1] - g0;
+  const int64_t ebase = T.ip[bs];
+  const int t = threadIdx.x;
+  for (int i = t; i <= G; i += 32) sgrp[i] = T.grp[g0 + i] - bs;
+  for (int i = t; i < nb; i += 32) srow[i] = (unsigned short)(T.rows[bs + i] - bs);
+  for (int i = t; i <= nb; i += 32) soff[i] = int(T.ip[bs + i] - ebase);
+  if (t == 0) {
+    const int64_t ne = T.ip[bs + nb] - ebase;
+    bulk_prefetch_range(T.ix + ebase, ne * int64_t(sizeof(int)));
+    bulk_prefetch_range(T.v + ebase, ne * int64_t(sizeof(double)));
+  }
+  __syncwarp();
+  if constexpr (PIPE) {
+    RowLoad cur, nxt;
+    if (G > 0 && t < sgrp[1] - sgrp[0]) row_issue(T, srow, soff, ebase, bs, sgrp[0] + t, cur);
+    for (int g = 0; g < G; ++g) {
+      const int r0 = sgrp[g], r1 = sgrp[g + 1];
+      const bool nx = g + 1 < G && t < sgrp[g + 2] - r1;
+      if (nx) row_issue(T, srow, soff, ebase, bs, r1 + t, nxt);
+      if (t < r1 - r0) row_finish(T, cur, bs, y);
+      for (int k = r0 + t + 32; k < r1; k += 32) {  // levels wider than a warp
+        RowLoad w;
+        row_issue(T, srow, soff, ebase, bs, k, w);
+        row_finish(T, w, bs, y);
+      }
+      __syncwarp();
+      if (nx) cur = nxt;
+    }
+  } else {
+    for (int g = 0; g < G; ++g) {
+      const int r0 = sgrp[g], r1 = sgrp[g + 1];
+      for (int k = r0 + t; k < r1; k += 32) {
+        RowLoad w;
+        row_issue(T, srow, soff, ebase, bs, k, w);
+        row_finish(T, w, bs, y);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <bool PIPE>
+__global__ void __launch_bounds__(32) block_ilu_kernel(const int* __restrict__ block_ptr,
+                                                       const int* __restrict__ new2old,
+                                                       TriView A, TriView B,
+                                                       const double* __restrict__ r,
+                                                       double* __restrict__ out, int max_block) {
   extern __shared__ double y[];
+  int* sgrp = reinterpret_cast<int*>(y + max_block);
+  int* soff = sgrp + max_block + 1;
+  unsigned short* srow = reinterpret_cast<unsigned short*>(soff + max_block + 1);
   const int b = blockIdx.x;
   const int bs = block_ptr[b], be = block_ptr[b + 1];
   // new2old == nullptr: the level is numbered block-major already
-  for (int i = threadIdx.x; i < be - bs; i += blockDim.x) y[i] = r[new2old ? new2old[bs + i] : bs + i];
-  __syncthreads();
-  block_tri(A, b, bs, y);
-  block_tri(B, b, bs, y);
-  for (int i = threadIdx.x; i < be - bs; i += blockDim.x) out[new2old ? new2old[bs + i] : bs + i] = y[i];
+  for (int i = threadIdx.x; i < be - bs; i += 32) y[i] = r[new2old ? new2old[bs + i] : bs + i];
+  __syncwarp();
+  block_tri<PIPE>(A, b, bs, be - bs, y, sgrp, srow, soff);
+  block_tri<PIPE>(B, b, bs, be - bs, y, sgrp, srow, soff);
+  for (int i = threadIdx.x; i < be - bs; i += 32) out[new2old ? new2old[bs + i] : bs + i] = y[i];
+}
+
+inline size_t block_ilu_smem(int max_block) {
+  return size_t(max_block) * 8 + size_t(max_block + 1) * 8 + size_t(max_block) * 2 + 16;
 }
 
 
@@ -441,7 +537,8 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
   if (rc != FB_OK) return rc;
   FB_TRY_CUDA(B->block_ptr.upload(bptr.data(), nblocks + 1));
   FB_TRY_CUDA(B->new2old.upload(n2o.data(), n));
-  FB_REQUIRE(size_t(B->max_block) * 8 <= 200 * 1024, "block too large for shared memory");
+  FB_REQUIRE(block_ilu_smem(B->max_block) <= 200 * 1024 && B->max_block <= 65535,
+             "block too large for shared memory");
   *out = B.release();
   return FB_OK;
 }
@@ -455,17 +552,23 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
   FB_REQUIRE(B != nullptr, "smoother is NULL");
   FB_REQUIRE(r != out, "in-place smoother application is not supported");
   if (B->nblocks == 0) return FB_OK;
-  const size_t smem = size_t(B->max_block) * sizeof(double);
+  const size_t smem = block_ilu_smem(B->max_block);
   static bool configured = false;
   if (!configured) {
-    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_kernel,
+    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
   const TriView a = transpose ? view(B->Ut, false) : view(B->L, true);
   const TriView b = transpose ? view(B->Lt, true) : view(B->U, false);
-  block_ilu_kernel<<<B->nblocks, 64, smem, as_stream(stream)>>>(B->block_ptr.ptr,
-                                                                 B->new2old.ptr, a, b, r, out);
+  if (g_bilu_pipe)
+    block_ilu_kernel<true><<<B->nblocks, 32, smem, as_stream(stream)>>>(
+        B->block_ptr.ptr, B->new2old.ptr, a, b, r, out, B->max_block);
+  else
+    block_ilu_kernel<false><<<B->nblocks, 32, smem, as_stream(stream)>>>(
+        B->block_ptr.ptr, B->new2old.ptr, a, b, r, out, B->max_block);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
@@ -570,7 +673,8 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
     FB_REQUIRE(block_ptr_host[b + 1] >= block_ptr_host[b], "block_ptr must be non-decreasing");
     B->max_block = std::max<int64_t>(B->max_block, block_ptr_host[b + 1] - block_ptr_host[b]);
   }
-  FB_REQUIRE(size_t(B->max_block) * 8 <= 200 * 1024, "block too large for shared memory");
+  FB_REQUIRE(block_ilu_smem(B->max_block) <= 200 * 1024 && B->max_block <= 65535,
+             "block too large for shared memory");
   cudaStream_t st = 0;
   DevBuf<int64_t> bptr64;
   FB_TRY_CUDA(bptr64.upload(block_ptr_host, nblocks + 1));
@@ -670,5 +774,10 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
   if (rc != FB_OK) return rc;
   FB_TRY_CUDA(cudaDeviceSynchronize());
   *out = B.release();  // new2old stays empty: the level is block-major already
+  return FB_OK;
+}
+
+extern "C" int fb_set_blockilu_pipeline(int on) {
+  g_bilu_pipe = on ? 1 : 0;
   return FB_OK;
 }

@@ -58,8 +58,19 @@ __global__ void csr_spmv_kernel(int64_t nrows, const int64_t* __restrict__ ip,
   if (r >= nrows) return;
   double acc = 0.0;
   const int64_t e = __ldg(ip + r + 1);
-  for (int64_t k = __ldg(ip + r); k < e; ++k)
-    acc = __dadd_rn(acc, __dmul_rn(__ldg(v + k), __ldg(x + __ldg(ix + k))));
+  // batches of 8 independent loads, summed sequentially in index order
+  for (int64_t k = __ldg(ip + r); k < e; k += 8) {
+    double a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = k + u < e;
+      a[u] = ok ? __ldg(v + k + u) : 0.0;
+      b[u] = ok ? __ldg(x + __ldg(ix + k + u)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k + u < e) acc = __dadd_rn(acc, __dmul_rn(a[u], b[u]));
+  }
   y[r] = b ? __dsub_rn(__ldg(b + r), acc) : acc;
 }
 

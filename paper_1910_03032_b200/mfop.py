@@ -143,7 +143,9 @@ def _eval_matrices(space, points):
 
 
 def _is_device_geom(geom):
-    return not hasattr(geom, "detj") or type(geom).__name__ == "DeviceGeometry"
+    # type check first: hasattr(DeviceGeometry, "detj") would materialise the
+    # host factors through the lazy property
+    return type(geom).__name__ == "DeviceGeometry" or not hasattr(geom, "detj")
 
 
 # -- operators -----------------------------------------------------------------

@@ -118,12 +118,13 @@ def test_p_transfer_matches_nodal_interpolation(p):
     m, ref, ed, perm, bptr = _perm(counts, p, 2)
     pc = max(1, (p + 1) // 2)
     refc = spaces.FESpace(m, pc)
-    idsc, _ = S.box_lattice_ids(counts, pc, 2)
+    cblock = 2 if pc > 1 else 4
+    idsc, _ = S.box_lattice_ids(counts, pc, cblock)
     permc = np.full(refc.ndofs_scalar, -1, dtype=np.int64)
     permc[refc.element_dofs.ravel()] = S.lattice_element_dofs(idsc, pc).numpy().ravel()
     Pm = lor.nodal_interpolation(ref, refc)
     fine = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
-    coarse = S.BoxSpace(m, pc, block=2 if pc > 1 else 4, device=torch.device("cuda"))
+    coarse = S.BoxSpace(m, pc, block=cblock, device=torch.device("cuda"))
     T = S.BoxTransfer(fine, coarse)
     rng = np.random.default_rng(1)
     xc = rng.standard_normal(refc.ndofs_scalar)
