@@ -91,7 +91,7 @@ _SIGS = [
     ("fb_transfer_destroy", None, [_vp]),
     ("fb_transfer_prolong", _int, [_vp, _vp, _vp, _vp]),
     ("fb_transfer_restrict", _int, [_vp, _vp, _vp, _vp]),
-    ("fb_set_blockilu_pipeline", _int, [_int]),
+    ("fb_set_blockilu_pipeline", _int, [_int, _int]),
 ]
 
 SYMBOLS = [s[0] for s in _SIGS]

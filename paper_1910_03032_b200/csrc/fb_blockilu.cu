@@ -38,6 +38,7 @@ struct TriPart {
 }  // namespace
 
 static int g_bilu_pipe = 1;
+static int g_bilu_lanes = 0;  // 0 = by block size
 
 struct fb_blockilu {
   int64_t n = 0;
@@ -110,78 +111,121 @@ __device__ __forceinline__ void row_finish(const TriView& T, const RowLoad& R, i
   y[R.row - bs] = T.invdiag ? __dmul_rn(r, R.inv) : r;
 }
 
-// One triangular solve of block b by ONE warp, level by level in shared
-// memory (__syncwarp between levels).  The block's level groups,
-// level-ordered local rows and entry offsets are staged in shared memory and
-// its factor entries prefetched into L2; with PIPE the loads of level g+1 are
-// issued before level g computes.  Every row's sum stays sequential in index
-// order (bitwise the host sweep).
-template <bool PIPE>
-__device__ __forceinline__ void block_tri(const TriView& T, int b, int bs, int nb, double* y,
-                                          int* sgrp, unsigned short* srow, int* soff) {
-  const int g0 = T.blk_grp[b], G = T.blk_grp[b + 1] - g0;
-  const int64_t ebase = T.ip[bs];
-  const int t = threadIdx.x;
-  for (int i = t; i <= G; i += 32) sgrp[i] = T.grp[g0 + i] - bs;
-  for (int i = t; i < nb; i += 32) srow[i] = (unsigned short)(T.rows[bs + i] - bs);
-  for (int i = t; i <= nb; i += 32) soff[i] = int(T.ip[bs + i] - ebase);
-  if (t == 0) {
-    const int64_t ne = T.ip[bs + nb] - ebase;
-    bulk_prefetch_range(T.ix + ebase, ne * int64_t(sizeof(int)));
-    bulk_prefetch_range(T.v + ebase, ne * int64_t(sizeof(double)));
+// Triangular solves of BPW = 32 / LPB blocks by ONE warp: lanes
+// [j LPB, (j+1) LPB) own block j and walk its level groups in shared memory
+// (__syncwarp between levels; the warp runs the longest schedule of its
+// blocks).  Level-parallel rows are few per level (1.5 at p = 2, 7 at p = 4,
+// 24 at p = 7), so several blocks share a warp's instruction stream.  The
+// block's level groups, level-ordered local rows and entry offsets are staged
+// in shared memory and its factor entries prefetched into L2; with PIPE the
+// loads of level g+1 are issued before level g computes.  Every row's sum
+// stays sequential in index order (bitwise the host sweep).
+template <int LPB, bool PIPE>
+__device__ __forceinline__ void block_tri(const TriView& T, bool live, int b, int bs, int nb,
+                                          double* y, int* sgrp, unsigned short* srow,
+                                          int* soff) {
+  const int t = threadIdx.x % LPB;
+  int G = 0;
+  int64_t ebase = 0;
+  if (live) {
+    const int g0 = T.blk_grp[b];
+    G = T.blk_grp[b + 1] - g0;
+    ebase = T.ip[bs];
+    for (int i = t; i <= G; i += LPB) sgrp[i] = T.grp[g0 + i] - bs;
+    for (int i = t; i < nb; i += LPB) srow[i] = (unsigned short)(T.rows[bs + i] - bs);
+    for (int i = t; i <= nb; i += LPB) soff[i] = int(T.ip[bs + i] - ebase);
+    if (t == 0) {
+      const int64_t ne = T.ip[bs + nb] - ebase;
+      bulk_prefetch_range(T.ix + ebase, ne * int64_t(sizeof(int)));
+      bulk_prefetch_range(T.v + ebase, ne * int64_t(sizeof(double)));
+    }
   }
+  int Gmax = G;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) Gmax = max(Gmax, __shfl_xor_sync(0xffffffffu, Gmax, o));
   __syncwarp();
   if constexpr (PIPE) {
     RowLoad cur, nxt;
     if (G > 0 && t < sgrp[1] - sgrp[0]) row_issue(T, srow, soff, ebase, bs, sgrp[0] + t, cur);
-    for (int g = 0; g < G; ++g) {
-      const int r0 = sgrp[g], r1 = sgrp[g + 1];
-      const bool nx = g + 1 < G && t < sgrp[g + 2] - r1;
-      if (nx) row_issue(T, srow, soff, ebase, bs, r1 + t, nxt);
-      if (t < r1 - r0) row_finish(T, cur, bs, y);
-      for (int k = r0 + t + 32; k < r1; k += 32) {  // levels wider than a warp
-        RowLoad w;
-        row_issue(T, srow, soff, ebase, bs, k, w);
-        row_finish(T, w, bs, y);
+    for (int g = 0; g < Gmax; ++g) {
+      if (g < G) {
+        const int r0 = sgrp[g], r1 = sgrp[g + 1];
+        const bool nx = g + 1 < G && t < sgrp[g + 2] - r1;
+        if (nx) row_issue(T, srow, soff, ebase, bs, r1 + t, nxt);
+        if (t < r1 - r0) row_finish(T, cur, bs, y);
+        for (int k = r0 + t + LPB; k < r1; k += LPB) {  // levels wider than LPB
+          RowLoad w;
+          row_issue(T, srow, soff, ebase, bs, k, w);
+          row_finish(T, w, bs, y);
+        }
+        if (nx) cur = nxt;
       }
       __syncwarp();
-      if (nx) cur = nxt;
     }
   } else {
-    for (int g = 0; g < G; ++g) {
-      const int r0 = sgrp[g], r1 = sgrp[g + 1];
-      for (int k = r0 + t; k < r1; k += 32) {
-        RowLoad w;
-        row_issue(T, srow, soff, ebase, bs, k, w);
-        row_finish(T, w, bs, y);
+    for (int g = 0; g < Gmax; ++g) {
+      if (g < G) {
+        const int r0 = sgrp[g], r1 = sgrp[g + 1];
+        for (int k = r0 + t; k < r1; k += LPB) {
+          RowLoad w;
+          row_issue(T, srow, soff, ebase, bs, k, w);
+          row_finish(T, w, bs, y);
+        }
       }
       __syncwarp();
     }
   }
 }
 
-template <bool PIPE>
+template <int LPB, bool PIPE>
 __global__ void __launch_bounds__(32) block_ilu_kernel(const int* __restrict__ block_ptr,
+                                                       int nblocks,
                                                        const int* __restrict__ new2old,
                                                        TriView A, TriView B,
                                                        const double* __restrict__ r,
                                                        double* __restrict__ out, int max_block) {
-  extern __shared__ double y[];
+  extern __shared__ double smem_d[];
+  const int j = threadIdx.x / LPB, t = threadIdx.x % LPB;
+  const size_t per = (size_t(max_block) * 18 + 16 + 15) / 16 * 2;  // doubles per block region
+  double* y = smem_d + j * per;
   int* sgrp = reinterpret_cast<int*>(y + max_block);
   int* soff = sgrp + max_block + 1;
   unsigned short* srow = reinterpret_cast<unsigned short*>(soff + max_block + 1);
-  const int b = blockIdx.x;
-  const int bs = block_ptr[b], be = block_ptr[b + 1];
+  const int b = blockIdx.x * (32 / LPB) + j;
+  const bool live = b < nblocks;
+  const int bs = live ? block_ptr[b] : 0, be = live ? block_ptr[b + 1] : 0;
   // new2old == nullptr: the level is numbered block-major already
-  for (int i = threadIdx.x; i < be - bs; i += 32) y[i] = r[new2old ? new2old[bs + i] : bs + i];
+  for (int i = t; i < be - bs; i += LPB) y[i] = r[new2old ? new2old[bs + i] : bs + i];
   __syncwarp();
-  block_tri<PIPE>(A, b, bs, be - bs, y, sgrp, srow, soff);
-  block_tri<PIPE>(B, b, bs, be - bs, y, sgrp, srow, soff);
-  for (int i = threadIdx.x; i < be - bs; i += 32) out[new2old ? new2old[bs + i] : bs + i] = y[i];
+  block_tri<LPB, PIPE>(A, live, b, bs, be - bs, y, sgrp, srow, soff);
+  block_tri<LPB, PIPE>(B, live, b, bs, be - bs, y, sgrp, srow, soff);
+  for (int i = t; i < be - bs; i += LPB) out[new2old ? new2old[bs + i] : bs + i] = y[i];
 }
 
 inline size_t block_ilu_smem(int max_block) {
-  return size_t(max_block) * 8 + size_t(max_block + 1) * 8 + size_t(max_block) * 2 + 16;
+  return (size_t(max_block) * 18 + 16 + 15) / 16 * 16;  // one block's region
+}
+
+// lanes per block: small blocks (p <= 2 levels, ~1.5 rows per dependency
+// level) share a warp 16 ways; larger blocks are smem-bound (18 B per row)
+// and run one per warp (measured, tools/box_profile.py)
+inline int block_ilu_lanes(int max_block) { return max_block <= 160 ? 2 : 32; }
+
+template <int LPB, bool PIPE>
+int launch_block_ilu(const fb_blockilu* B, TriView a, TriView b, const double* r, double* out,
+                     cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_kernel<LPB, PIPE>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = true;
+  }
+  constexpr int BPW = 32 / LPB;
+  const size_t smem = block_ilu_smem(B->max_block) * BPW;
+  block_ilu_kernel<LPB, PIPE><<<(B->nblocks + BPW - 1) / BPW, 32, smem, st>>>(
+      B->block_ptr.ptr, B->nblocks, B->new2old.ptr, a, b, r, out, B->max_block);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
 }
 
 
@@ -537,7 +581,8 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
   if (rc != FB_OK) return rc;
   FB_TRY_CUDA(B->block_ptr.upload(bptr.data(), nblocks + 1));
   FB_TRY_CUDA(B->new2old.upload(n2o.data(), n));
-  FB_REQUIRE(block_ilu_smem(B->max_block) <= 200 * 1024 && B->max_block <= 65535,
+  FB_REQUIRE(block_ilu_smem(B->max_block) * (32 / block_ilu_lanes(B->max_block)) <= 200 * 1024 &&
+                 B->max_block <= 65535,
              "block too large for shared memory");
   *out = B.release();
   return FB_OK;
@@ -552,25 +597,18 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
   FB_REQUIRE(B != nullptr, "smoother is NULL");
   FB_REQUIRE(r != out, "in-place smoother application is not supported");
   if (B->nblocks == 0) return FB_OK;
-  const size_t smem = block_ilu_smem(B->max_block);
-  static bool configured = false;
-  if (!configured) {
-    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_kernel<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured = true;
-  }
   const TriView a = transpose ? view(B->Ut, false) : view(B->L, true);
   const TriView b = transpose ? view(B->Lt, true) : view(B->U, false);
-  if (g_bilu_pipe)
-    block_ilu_kernel<true><<<B->nblocks, 32, smem, as_stream(stream)>>>(
-        B->block_ptr.ptr, B->new2old.ptr, a, b, r, out, B->max_block);
-  else
-    block_ilu_kernel<false><<<B->nblocks, 32, smem, as_stream(stream)>>>(
-        B->block_ptr.ptr, B->new2old.ptr, a, b, r, out, B->max_block);
-  FB_CHECK_LAUNCH();
-  return FB_OK;
+  cudaStream_t st = as_stream(stream);
+  const int lanes = g_bilu_lanes ? g_bilu_lanes : block_ilu_lanes(B->max_block);
+  const bool pipe = g_bilu_pipe != 0;
+  switch (lanes) {
+    case 2: return pipe ? launch_block_ilu<2, true>(B, a, b, r, out, st) : launch_block_ilu<2, false>(B, a, b, r, out, st);
+    case 4: return pipe ? launch_block_ilu<4, true>(B, a, b, r, out, st) : launch_block_ilu<4, false>(B, a, b, r, out, st);
+    case 8: return pipe ? launch_block_ilu<8, true>(B, a, b, r, out, st) : launch_block_ilu<8, false>(B, a, b, r, out, st);
+    case 16: return pipe ? launch_block_ilu<16, true>(B, a, b, r, out, st) : launch_block_ilu<16, false>(B, a, b, r, out, st);
+    default: return pipe ? launch_block_ilu<32, true>(B, a, b, r, out, st) : launch_block_ilu<32, false>(B, a, b, r, out, st);
+  }
 }
 
 // Dense coarse solve: out = Ainv x with a stored dense inverse (row-major),
@@ -673,7 +711,8 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
     FB_REQUIRE(block_ptr_host[b + 1] >= block_ptr_host[b], "block_ptr must be non-decreasing");
     B->max_block = std::max<int64_t>(B->max_block, block_ptr_host[b + 1] - block_ptr_host[b]);
   }
-  FB_REQUIRE(block_ilu_smem(B->max_block) <= 200 * 1024 && B->max_block <= 65535,
+  FB_REQUIRE(block_ilu_smem(B->max_block) * (32 / block_ilu_lanes(B->max_block)) <= 200 * 1024 &&
+                 B->max_block <= 65535,
              "block too large for shared memory");
   cudaStream_t st = 0;
   DevBuf<int64_t> bptr64;
@@ -777,7 +816,10 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
   return FB_OK;
 }
 
-extern "C" int fb_set_blockilu_pipeline(int on) {
+extern "C" int fb_set_blockilu_pipeline(int on, int lanes) {
+  FB_REQUIRE(lanes == 0 || lanes == 2 || lanes == 4 || lanes == 8 || lanes == 16 || lanes == 32,
+             "lanes per block must be 0 (auto), 2, 4, 8, 16 or 32");
   g_bilu_pipe = on ? 1 : 0;
+  g_bilu_lanes = lanes;
   return FB_OK;
 }

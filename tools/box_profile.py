@@ -12,7 +12,7 @@ from paper_1910_03032_b200 import device as dev, geometry, mfop, structured as S
 p, n = int(sys.argv[1]), int(sys.argv[2])
 if len(sys.argv) > 3:
     from paper_1910_03032_b200 import _lib
-    _lib.lib.fb_set_blockilu_pipeline(int(sys.argv[3]))
+    _lib.lib.fb_set_blockilu_pipeline(int(sys.argv[3]), int(sys.argv[4]) if len(sys.argv) > 4 else 0)
 T = {}
 t = time.perf_counter()
 mesh = S.box_mesh((n, n, n), perturb=0.05, seed=1)
