@@ -7,6 +7,8 @@
 // 100M-DoF box has ~2.7G entries), 32-bit column indices.
 struct fb_csr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
+  int warp_rows = 0;  // 1: 4 lanes per row, butterfly-order sums (device-assembled LOR levels);
+                      // 0: one thread per row, scipy's sequential order
   fb::DevBuf<int64_t> indptr;
   fb::DevBuf<int> indices;
   fb::DevBuf<double> data;

@@ -74,6 +74,32 @@ __global__ void csr_spmv_kernel(int64_t nrows, const int64_t* __restrict__ ip,
   y[r] = b ? __dsub_rn(__ldg(b + r), acc) : acc;
 }
 
+// LANES lanes per row: lanes take the row's entries in LANES-wide coalesced
+// strides and the partial sums are combined in a fixed butterfly order
+// (deterministic, not scipy's sequential order).  Used for the scale-mode
+// levels, whose rows have ~27 entries.
+template <int LANES>
+__global__ void __launch_bounds__(256) csr_spmv_group_kernel(int64_t nrows,
+                                                             const int64_t* __restrict__ ip,
+                                                             const int* __restrict__ ix,
+                                                             const double* __restrict__ v,
+                                                             const double* __restrict__ x,
+                                                             const double* __restrict__ b,
+                                                             double* __restrict__ y) {
+  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LANES;
+  const int lane = threadIdx.x % LANES;
+  const bool live = r < nrows;
+  double acc = 0.0;
+  if (live) {
+    const int64_t e0 = __ldg(ip + r), e1 = __ldg(ip + r + 1);
+    for (int64_t k = e0 + lane; k < e1; k += LANES)
+      acc = fma(__ldg(v + k), __ldg(x + __ldg(ix + k)), acc);
+  }
+#pragma unroll
+  for (int o = LANES / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (live && lane == 0) y[r] = b ? __ldg(b + r) - acc : acc;
+}
+
 // y = A^T x for CSR A without a stored transpose is not deterministic in
 // parallel; transposes are stored explicitly by the caller instead.
 
@@ -187,8 +213,12 @@ void fb_csr_destroy(fb_csr* A) { delete A; }
 int fb_csr_spmv(const fb_csr* A, const double* x, double* y, void* stream) {
   FB_REQUIRE(A != nullptr, "matrix is NULL");
   if (A->nrows == 0) return FB_OK;
-  csr_spmv_kernel<<<ceil_div(A->nrows, 128), 128, 0, as_stream(stream)>>>(
-      A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, nullptr, y);
+  if (A->warp_rows)
+    csr_spmv_group_kernel<4><<<ceil_div(A->nrows * 4, 256), 256, 0, as_stream(stream)>>>(
+        A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, nullptr, y);
+  else
+    csr_spmv_kernel<<<ceil_div(A->nrows, 128), 128, 0, as_stream(stream)>>>(
+        A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, nullptr, y);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
@@ -196,8 +226,12 @@ int fb_csr_spmv(const fb_csr* A, const double* x, double* y, void* stream) {
 int fb_csr_residual(const fb_csr* A, const double* b, const double* x, double* y, void* stream) {
   FB_REQUIRE(A != nullptr, "matrix is NULL");
   if (A->nrows == 0) return FB_OK;
-  csr_spmv_kernel<<<ceil_div(A->nrows, 128), 128, 0, as_stream(stream)>>>(
-      A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, b, y);
+  if (A->warp_rows)
+    csr_spmv_group_kernel<4><<<ceil_div(A->nrows * 4, 256), 256, 0, as_stream(stream)>>>(
+        A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, b, y);
+  else
+    csr_spmv_kernel<<<ceil_div(A->nrows, 128), 128, 0, as_stream(stream)>>>(
+        A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, b, y);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }

@@ -252,63 +252,78 @@ __device__ __forceinline__ bool owned_local(const int64_t ec[3], int l0, int l1,
   return (l0 > 0 || ec[0] == 0) && (l1 > 0 || ec[1] == 0) && (l2 > 0 || ec[2] == 0);
 }
 
-__global__ void transfer_prolong_kernel(TransferView T, const double* __restrict__ xc,
-                                        double* __restrict__ xf) {
-  __shared__ double xe[125];
-  __shared__ double w[3][9 * 5];
-  const int64_t e = blockIdx.x;
+// One warp per fine element, kTE elements per CTA.
+constexpr int kTE = 4;
+
+__global__ void __launch_bounds__(32 * kTE) transfer_prolong_kernel(TransferView T, int64_t ne,
+                                                                    const double* __restrict__ xc,
+                                                                    double* __restrict__ xf) {
+  __shared__ double xe_all[kTE][125];
+  __shared__ double w_all[kTE][3][9 * 5];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e = int64_t(blockIdx.x) * kTE + wi;
+  if (e >= ne) return;
+  double* xe = xe_all[wi];
+  double(*w)[9 * 5] = w_all[wi];
   int64_t ec[3];
   const double* Wa[3];
   transfer_elem(T, e, ec, Wa);
-  const int nc3 = T.nc * T.nc * T.nc, nf3 = T.nf * T.nf * T.nf;
-  for (int j = threadIdx.x; j < nc3; j += blockDim.x) xe[j] = xc[T.hmap[e * nc3 + j]];
-  for (int j = threadIdx.x; j < T.nf * T.nc; j += blockDim.x)
-    for (int a = 0; a < 3; ++a) w[a][j] = Wa[a][j];
-  __syncthreads();
-  for (int l = threadIdx.x; l < nf3; l += blockDim.x) {
-    const int l0 = l % T.nf, l1 = (l / T.nf) % T.nf, l2 = l / (T.nf * T.nf);
+  const int nc = T.nc, nf = T.nf;
+  const int nc3 = nc * nc * nc, nf3 = nf * nf * nf;
+  for (int j = lane; j < nc3; j += 32) xe[j] = __ldg(xc + __ldg(T.hmap + e * nc3 + j));
+  for (int j = lane; j < nf * nc; j += 32)
+    for (int a = 0; a < 3; ++a) w[a][j] = __ldg(Wa[a] + j);
+  __syncwarp();
+  for (int l = lane; l < nf3; l += 32) {
+    const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
     if (!owned_local(ec, l0, l1, l2)) continue;
     double acc = 0.0;
-    for (int c = 0; c < T.nc; ++c) {
+    for (int c = 0; c < nc; ++c) {
       double ab = 0.0;
-      for (int b = 0; b < T.nc; ++b) {
+      for (int b = 0; b < nc; ++b) {
         double aa = 0.0;
-        for (int a = 0; a < T.nc; ++a) aa += w[0][l0 * T.nc + a] * xe[(c * T.nc + b) * T.nc + a];
-        ab += w[1][l1 * T.nc + b] * aa;
+        for (int a = 0; a < nc; ++a) aa += w[0][l0 * nc + a] * xe[(c * nc + b) * nc + a];
+        ab += w[1][l1 * nc + b] * aa;
       }
-      acc += w[2][l2 * T.nc + c] * ab;
+      acc += w[2][l2 * nc + c] * ab;
     }
-    xf[T.fmap[e * nf3 + l]] = acc;
+    xf[__ldg(T.fmap + e * nf3 + l)] = acc;
   }
 }
 
-__global__ void transfer_restrict_kernel(TransferView T, const double* __restrict__ xf,
-                                         double* __restrict__ E) {
-  __shared__ double rf[729];
-  __shared__ double w[3][9 * 5];
-  const int64_t e = blockIdx.x;
+__global__ void __launch_bounds__(32 * kTE) transfer_restrict_kernel(TransferView T, int64_t ne,
+                                                                     const double* __restrict__ xf,
+                                                                     double* __restrict__ E) {
+  __shared__ double rf_all[kTE][729];
+  __shared__ double w_all[kTE][3][9 * 5];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e = int64_t(blockIdx.x) * kTE + wi;
+  if (e >= ne) return;
+  double* rf = rf_all[wi];
+  double(*w)[9 * 5] = w_all[wi];
   int64_t ec[3];
   const double* Wa[3];
   transfer_elem(T, e, ec, Wa);
-  const int nc3 = T.nc * T.nc * T.nc, nf3 = T.nf * T.nf * T.nf;
-  for (int l = threadIdx.x; l < nf3; l += blockDim.x) {
-    const int l0 = l % T.nf, l1 = (l / T.nf) % T.nf, l2 = l / (T.nf * T.nf);
-    rf[l] = owned_local(ec, l0, l1, l2) ? xf[T.fmap[e * nf3 + l]] : 0.0;
+  const int nc = T.nc, nf = T.nf;
+  const int nc3 = nc * nc * nc, nf3 = nf * nf * nf;
+  for (int l = lane; l < nf3; l += 32) {
+    const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
+    rf[l] = owned_local(ec, l0, l1, l2) ? __ldg(xf + __ldg(T.fmap + e * nf3 + l)) : 0.0;
   }
-  for (int j = threadIdx.x; j < T.nf * T.nc; j += blockDim.x)
-    for (int a = 0; a < 3; ++a) w[a][j] = Wa[a][j];
-  __syncthreads();
-  for (int j = threadIdx.x; j < nc3; j += blockDim.x) {
-    const int j0 = j % T.nc, j1 = (j / T.nc) % T.nc, j2 = j / (T.nc * T.nc);
+  for (int j = lane; j < nf * nc; j += 32)
+    for (int a = 0; a < 3; ++a) w[a][j] = __ldg(Wa[a] + j);
+  __syncwarp();
+  for (int j = lane; j < nc3; j += 32) {
+    const int j0 = j % nc, j1 = (j / nc) % nc, j2 = j / (nc * nc);
     double acc = 0.0;
-    for (int l2 = 0; l2 < T.nf; ++l2) {
+    for (int l2 = 0; l2 < nf; ++l2) {
       double s1 = 0.0;
-      for (int l1 = 0; l1 < T.nf; ++l1) {
+      for (int l1 = 0; l1 < nf; ++l1) {
         double s0 = 0.0;
-        for (int l0 = 0; l0 < T.nf; ++l0) s0 += w[0][l0 * T.nc + j0] * rf[(l2 * T.nf + l1) * T.nf + l0];
-        s1 += w[1][l1 * T.nc + j1] * s0;
+        for (int l0 = 0; l0 < nf; ++l0) s0 += w[0][l0 * nc + j0] * rf[(l2 * nf + l1) * nf + l0];
+        s1 += w[1][l1 * nc + j1] * s0;
       }
-      acc += w[2][l2 * T.nc + j2] * s1;
+      acc += w[2][l2 * nc + j2] * s1;
     }
     E[e * nc3 + j] = acc;
   }
@@ -348,6 +363,7 @@ int fb_lor_assemble_box(int p, const int64_t* counts, const double* corners_dev,
   FB_REQUIRE(n < (int64_t(1) << 31), "lattice exceeds int32 DoF ids");
   std::unique_ptr<fb_csr> A(new fb_csr());
   A->nrows = A->ncols = n;
+  A->warp_rows = 1;
   cudaStream_t st = 0;
   DevBuf<int> cnt;
   FB_TRY_CUDA(cnt.alloc(n));
@@ -435,8 +451,8 @@ static TransferView transfer_view(const fb_transfer* T) {
 int fb_transfer_prolong(const fb_transfer* T, const double* xc, double* xf, void* stream) {
   FB_REQUIRE(T != nullptr, "transfer is NULL");
   if (T->ne == 0) return FB_OK;
-  FB_REQUIRE(T->ne < (int64_t(1) << 31), "too many elements");
-  transfer_prolong_kernel<<<int(T->ne), 128, 0, as_stream(stream)>>>(transfer_view(T), xc, xf);
+  transfer_prolong_kernel<<<ceil_div(T->ne, kTE), 32 * kTE, 0, as_stream(stream)>>>(
+      transfer_view(T), T->ne, xc, xf);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
@@ -446,9 +462,8 @@ int fb_transfer_prolong(const fb_transfer* T, const double* xc, double* xf, void
 int fb_transfer_restrict(const fb_transfer* T, const double* xf, double* xc, void* stream) {
   FB_REQUIRE(T != nullptr, "transfer is NULL");
   if (T->ne == 0) return FB_OK;
-  FB_REQUIRE(T->ne < (int64_t(1) << 31), "too many elements");
-  transfer_restrict_kernel<<<int(T->ne), 128, 0, as_stream(stream)>>>(transfer_view(T), xf,
-                                                                       T->E.ptr);
+  transfer_restrict_kernel<<<ceil_div(T->ne, kTE), 32 * kTE, 0, as_stream(stream)>>>(
+      transfer_view(T), T->ne, xf, T->E.ptr);
   FB_CHECK_LAUNCH();
   return fb_restriction_scatter_add(T->hmap, T->E.ptr, xc, stream);
 }
