@@ -259,11 +259,12 @@ int fb_csr_download(const fb_csr* A, int64_t* indptr, int64_t* indices, double* 
  * solvers.py:283-290). */
 int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks, const int64_t* block_ptr_host,
                            int64_t* fail_row, fb_blockilu** out);
-/* Block-ILU sweep variant: on = 1 issues the loads of level g+1 before level
- * g computes (default), 0 = plain level loop; lanes = lanes per block (one
+/* Block-ILU sweep variant for smoothers created afterwards: mode 2 = padded
+ * rows (value/offset vectors, default), 1 = CSR rows with the next level's
+ * loads issued early, 0 = plain CSR level loop; lanes = lanes per block (one
  * warp serves 32/lanes blocks), 0 = chosen from the block size.  Same
- * results either way. */
-int fb_set_blockilu_pipeline(int on, int lanes);
+ * results in every mode. */
+int fb_set_blockilu_pipeline(int mode, int lanes);
 /* Nodal interpolation between two levels of a structured box, matrix-free
  * (lor.py:102-123).  fine: map of the fine level (ne, nf^3); hmap: for each
  * fine element the coarse DoFs of its parent coarse element (ne, nc^3);

@@ -33,11 +33,17 @@ struct TriPart {
   fb::DevBuf<int> rows;          // rows of each block, grouped by level
   fb::DevBuf<int> grp;           // level-group row offsets into `rows`
   fb::DevBuf<int> blk_grp;       // (nblocks + 1) offsets into grp
+  // padded row layout for the sweeps: row r's entries at r*width, values
+  // and shared-memory byte offsets of the column inside the block (padding:
+  // value 0 at offset 0, so sequential sums are unchanged)
+  int width = 0;
+  fb::DevBuf<double> ev;
+  fb::DevBuf<unsigned short> eo;
 };
 
 }  // namespace
 
-static int g_bilu_pipe = 1;
+static int g_bilu_pipe = 2;  // 0: CSR sweep, 1: CSR + next-level loads, 2: padded rows for large blocks, else 1
 static int g_bilu_lanes = 0;  // 0 = by block size
 
 struct fb_blockilu {
@@ -47,11 +53,16 @@ struct fb_blockilu {
   fb::DevBuf<int> block_ptr;  // (nblocks + 1) row offsets (new numbering)
   fb::DevBuf<int> new2old;    // new -> original DoF index
   TriPart L, U, Ut, Lt;       // forward: L (unit) then U; backward: U^T then L^T (unit)
+  int ell_w = 0;              // padded-row width of all parts (0: CSR sweeps)
 };
+
+static int build_ell(fb_blockilu* B);
 
 namespace fb {
 
 struct TriView {
+  const double* ev;
+  const unsigned short* eo;
   const int64_t* ip;
   const int* ix;
   const double* v;
@@ -177,6 +188,106 @@ __device__ __forceinline__ void block_tri(const TriView& T, bool live, int b, in
   }
 }
 
+// Quad-row variant for blocks with several rows per level (p >= 4 levels):
+// each row is split over 4 lanes (entries s, s+4, s+8, ... for sub-lane s),
+// the partial sums are combined with two butterfly shuffles (fixed order,
+// deterministic; not the sequential order of block_tri), and the next level's
+// entries are loaded before the current level computes.
+struct QuadLoad {
+  int c[4];
+  double a[4];
+  int n, row;
+  int64_t e0;
+  double inv;
+};
+
+__device__ __forceinline__ void quad_issue(const TriView& T, const unsigned short* srow,
+                                           const int* soff, int64_t ebase, int bs, int k, int s,
+                                           QuadLoad& R) {
+  const int lr = srow[k];
+  R.row = bs + lr;
+  R.e0 = ebase + soff[lr];
+  R.n = soff[lr + 1] - soff[lr];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = s + 4 * u;
+    const bool ok = i < R.n;
+    R.c[u] = ok ? __ldg(T.ix + R.e0 + i) : bs;
+    R.a[u] = ok ? __ldg(T.v + R.e0 + i) : 0.0;
+  }
+  R.inv = T.invdiag ? __ldg(T.invdiag + R.row) : 1.0;
+}
+
+__device__ __forceinline__ double quad_partial(const TriView& T, const QuadLoad& R, int bs, int s,
+                                               const double* y) {
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) acc = fma(R.a[u], y[R.c[u] - bs], acc);
+  for (int i = s + 16; i < R.n; i += 4)  // rows longer than 16 entries
+    acc = fma(__ldg(T.v + R.e0 + i), y[__ldg(T.ix + R.e0 + i) - bs], acc);
+  return acc;
+}
+
+template <int LPB>
+__device__ __forceinline__ void block_tri_quad(const TriView& T, bool live, int b, int bs, int nb,
+                                               double* y, int* sgrp, unsigned short* srow,
+                                               int* soff) {
+  constexpr int RPP = LPB / 4;  // rows per pass
+  const int t = threadIdx.x % LPB, q = t >> 2, s = t & 3;
+  const unsigned qmask = 0xFu << (threadIdx.x & ~3u);
+  int G = 0;
+  int64_t ebase = 0;
+  if (live) {
+    const int g0 = T.blk_grp[b];
+    G = T.blk_grp[b + 1] - g0;
+    ebase = T.ip[bs];
+    for (int i = t; i <= G; i += LPB) sgrp[i] = T.grp[g0 + i] - bs;
+    for (int i = t; i < nb; i += LPB) srow[i] = (unsigned short)(T.rows[bs + i] - bs);
+    for (int i = t; i <= nb; i += LPB) soff[i] = int(T.ip[bs + i] - ebase);
+    if (t == 0) {
+      const int64_t ne = T.ip[bs + nb] - ebase;
+      bulk_prefetch_range(T.ix + ebase, ne * int64_t(sizeof(int)));
+      bulk_prefetch_range(T.v + ebase, ne * int64_t(sizeof(double)));
+    }
+  }
+  int Gmax = G;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) Gmax = max(Gmax, __shfl_xor_sync(0xffffffffu, Gmax, o));
+  __syncwarp();
+  QuadLoad cur, nxt;
+  if (G > 0 && q < sgrp[1] - sgrp[0]) quad_issue(T, srow, soff, ebase, bs, sgrp[0] + q, s, cur);
+  for (int g = 0; g < Gmax; ++g) {
+    if (g < G) {
+      const int r0 = sgrp[g], r1 = sgrp[g + 1];
+      const bool nx = g + 1 < G && q < sgrp[g + 2] - r1;
+      if (nx) quad_issue(T, srow, soff, ebase, bs, r1 + q, s, nxt);
+      // quads are converged: every lane of a quad has the same q
+      if (q < r1 - r0) {
+        double acc = quad_partial(T, cur, bs, s, y);
+        acc += __shfl_xor_sync(qmask, acc, 1);
+        acc += __shfl_xor_sync(qmask, acc, 2);
+        if (s == 0) {
+          const double r = y[cur.row - bs] - acc;
+          y[cur.row - bs] = T.invdiag ? r * cur.inv : r;
+        }
+      }
+      for (int k = r0 + q + RPP; k < r1; k += RPP) {  // levels wider than one pass
+        QuadLoad w;
+        quad_issue(T, srow, soff, ebase, bs, k, s, w);
+        double acc = quad_partial(T, w, bs, s, y);
+        acc += __shfl_xor_sync(qmask, acc, 1);
+        acc += __shfl_xor_sync(qmask, acc, 2);
+        if (s == 0) {
+          const double r = y[w.row - bs] - acc;
+          y[w.row - bs] = T.invdiag ? r * w.inv : r;
+        }
+      }
+      if (nx) cur = nxt;
+    }
+    __syncwarp();
+  }
+}
+
 template <int LPB, bool PIPE>
 __global__ void __launch_bounds__(32) block_ilu_kernel(const int* __restrict__ block_ptr,
                                                        int nblocks,
@@ -197,9 +308,157 @@ __global__ void __launch_bounds__(32) block_ilu_kernel(const int* __restrict__ b
   // new2old == nullptr: the level is numbered block-major already
   for (int i = t; i < be - bs; i += LPB) y[i] = r[new2old ? new2old[bs + i] : bs + i];
   __syncwarp();
-  block_tri<LPB, PIPE>(A, live, b, bs, be - bs, y, sgrp, srow, soff);
-  block_tri<LPB, PIPE>(B, live, b, bs, be - bs, y, sgrp, srow, soff);
+  if constexpr (LPB >= 4 && !PIPE) {  // PIPE=false selects the quad-row sweep here
+    block_tri_quad<LPB>(A, live, b, bs, be - bs, y, sgrp, srow, soff);
+    block_tri_quad<LPB>(B, live, b, bs, be - bs, y, sgrp, srow, soff);
+  } else {
+    block_tri<LPB, PIPE>(A, live, b, bs, be - bs, y, sgrp, srow, soff);
+    block_tri<LPB, PIPE>(B, live, b, bs, be - bs, y, sgrp, srow, soff);
+  }
   for (int i = t; i < be - bs; i += LPB) out[new2old ? new2old[bs + i] : bs + i] = y[i];
+}
+
+// ---- padded-row (ELL) sweep: the production path -------------------------
+// Same schedule as block_tri (one warp serves 32/LPB blocks, level groups in
+// shared memory, next level's loads issued before the current level
+// computes) but every row is W padded entries: values as double2 and
+// shared-memory byte offsets as uint4 vector loads, no per-entry predicates
+// or address arithmetic.  Padding is value 0 at offset 0, so each row's sum
+// is still the sequential index-order sum (bitwise the CSR sweep).
+template <int W>
+struct EllRow {
+  double a[W];
+  unsigned int o[W / 2];  // two 16-bit byte offsets per word
+  int row;
+  double inv;
+};
+
+template <int W>
+__device__ __forceinline__ void ell_issue(const TriView& T, const unsigned short* srow, int bs,
+                                          int k, EllRow<W>& R) {
+  R.row = bs + srow[k];
+  const double2* va = reinterpret_cast<const double2*>(T.ev + int64_t(R.row) * W);
+  const uint4* oa = reinterpret_cast<const uint4*>(T.eo + int64_t(R.row) * W);
+#pragma unroll
+  for (int u = 0; u < W / 2; ++u) {
+    const double2 t = __ldg(va + u);
+    R.a[2 * u] = t.x;
+    R.a[2 * u + 1] = t.y;
+  }
+#pragma unroll
+  for (int u = 0; u < W / 8; ++u) {
+    const uint4 t = __ldg(oa + u);
+    R.o[4 * u] = t.x;
+    R.o[4 * u + 1] = t.y;
+    R.o[4 * u + 2] = t.z;
+    R.o[4 * u + 3] = t.w;
+  }
+  R.inv = T.invdiag ? __ldg(T.invdiag + R.row) : 1.0;
+}
+
+template <int W>
+__device__ __forceinline__ void ell_finish(const TriView& T, const EllRow<W>& R, int bs,
+                                           double* y) {
+  const char* yb = reinterpret_cast<const char*>(y);
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < W; ++u) {
+    const unsigned off = (u & 1) ? (R.o[u >> 1] >> 16) : (R.o[u >> 1] & 0xFFFFu);
+    acc = __dadd_rn(acc, __dmul_rn(R.a[u], *reinterpret_cast<const double*>(yb + off)));
+  }
+  const double r = __dsub_rn(y[R.row - bs], acc);
+  y[R.row - bs] = T.invdiag ? __dmul_rn(r, R.inv) : r;
+}
+
+template <int LPB, int W>
+__device__ __forceinline__ void block_tri_ell(const TriView& T, bool live, int b, int bs, int nb,
+                                              double* y, int* sgrp, unsigned short* srow) {
+  const int t = threadIdx.x % LPB;
+  int G = 0;
+  if (live) {
+    const int g0 = T.blk_grp[b];
+    G = T.blk_grp[b + 1] - g0;
+    for (int i = t; i <= G; i += LPB) sgrp[i] = T.grp[g0 + i] - bs;
+    for (int i = t; i < nb; i += LPB) srow[i] = (unsigned short)(T.rows[bs + i] - bs);
+    if (t == 0) {
+      bulk_prefetch_range(T.ev + int64_t(bs) * W, int64_t(nb) * W * int64_t(sizeof(double)));
+      bulk_prefetch_range(T.eo + int64_t(bs) * W, int64_t(nb) * W * int64_t(sizeof(unsigned short)));
+    }
+  }
+  int Gmax = G;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) Gmax = max(Gmax, __shfl_xor_sync(0xffffffffu, Gmax, o));
+  __syncwarp();
+  EllRow<W> cur, nxt;
+  if (G > 0 && t < sgrp[1] - sgrp[0]) ell_issue<W>(T, srow, bs, sgrp[0] + t, cur);
+  for (int g = 0; g < Gmax; ++g) {
+    if (g < G) {
+      const int r0 = sgrp[g], r1 = sgrp[g + 1];
+      const bool nx = g + 1 < G && t < sgrp[g + 2] - r1;
+      if (nx) ell_issue<W>(T, srow, bs, r1 + t, nxt);
+      if (t < r1 - r0) ell_finish<W>(T, cur, bs, y);
+      for (int k = r0 + t + LPB; k < r1; k += LPB) {  // levels wider than LPB
+        EllRow<W> w;
+        ell_issue<W>(T, srow, bs, k, w);
+        ell_finish<W>(T, w, bs, y);
+      }
+      if (nx) cur = nxt;
+    }
+    __syncwarp();
+  }
+}
+
+template <int LPB, int W>
+__global__ void __launch_bounds__(32) block_ilu_ell_kernel(const int* __restrict__ block_ptr,
+                                                           int nblocks,
+                                                           const int* __restrict__ new2old,
+                                                           TriView A, TriView B,
+                                                           const double* __restrict__ r,
+                                                           double* __restrict__ out,
+                                                           int max_block) {
+  extern __shared__ double smem_d[];
+  const int j = threadIdx.x / LPB, t = threadIdx.x % LPB;
+  const size_t per = (size_t(max_block) * 14 + 16 + 15) / 16 * 2;  // doubles per block region
+  double* y = smem_d + j * per;
+  int* sgrp = reinterpret_cast<int*>(y + max_block);
+  unsigned short* srow = reinterpret_cast<unsigned short*>(sgrp + max_block + 1);
+  const int b = blockIdx.x * (32 / LPB) + j;
+  const bool live = b < nblocks;
+  const int bs = live ? block_ptr[b] : 0, be = live ? block_ptr[b + 1] : 0;
+  for (int i = t; i < be - bs; i += LPB) y[i] = r[new2old ? new2old[bs + i] : bs + i];
+  __syncwarp();
+  block_tri_ell<LPB, W>(A, live, b, bs, be - bs, y, sgrp, srow);
+  block_tri_ell<LPB, W>(B, live, b, bs, be - bs, y, sgrp, srow);
+  for (int i = t; i < be - bs; i += LPB) out[new2old ? new2old[bs + i] : bs + i] = y[i];
+}
+
+inline size_t block_ilu_ell_smem(int max_block) {
+  return (size_t(max_block) * 14 + 16 + 15) / 16 * 16;
+}
+
+__global__ void ell_rowlen_kernel(int64_t n, const int64_t* __restrict__ ip, int* __restrict__ mx) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < n) atomicMax(mx, int(ip[r + 1] - ip[r]));
+}
+
+__global__ void ell_fill_kernel(int64_t n, int nblocks, const int* __restrict__ bptr,
+                                const int64_t* __restrict__ ip, const int* __restrict__ ix,
+                                const double* __restrict__ v, int W, double* __restrict__ ev,
+                                unsigned short* __restrict__ eo) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int lo = 0, hi = nblocks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (bptr[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  const int bs = bptr[lo];
+  const int64_t e0 = ip[r], len = ip[r + 1] - e0;
+  for (int u = 0; u < W; ++u) {
+    const bool ok = u < len;
+    ev[r * W + u] = ok ? v[e0 + u] : 0.0;
+    eo[r * W + u] = (unsigned short)(ok ? unsigned(ix[e0 + u] - bs) * 8u : 0u);
+  }
 }
 
 inline size_t block_ilu_smem(int max_block) {
@@ -525,11 +784,74 @@ void transpose_csr(int64_t n, const int64_t* ip, const int64_t* ix, const double
 }
 
 TriView view(const TriPart& P, bool unit) {
-  return TriView{P.ip.ptr, P.ix.ptr, P.v.ptr, unit ? nullptr : P.invdiag.ptr,
-                 P.rows.ptr, P.grp.ptr, P.blk_grp.ptr};
+  return TriView{P.ev.ptr, P.eo.ptr, P.ip.ptr, P.ix.ptr, P.v.ptr,
+                 unit ? nullptr : P.invdiag.ptr, P.rows.ptr, P.grp.ptr, P.blk_grp.ptr};
 }
 
 }  // namespace
+
+namespace {
+
+template <int LPB, int W>
+int launch_ell(const fb_blockilu* B, TriView a, TriView b, const double* r, double* out,
+               cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_ell_kernel<LPB, W>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = true;
+  }
+  constexpr int BPW = 32 / LPB;
+  const size_t smem = block_ilu_ell_smem(B->max_block) * BPW;
+  block_ilu_ell_kernel<LPB, W><<<(B->nblocks + BPW - 1) / BPW, 32, smem, st>>>(
+      B->block_ptr.ptr, B->nblocks, B->new2old.ptr, a, b, r, out, B->max_block);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+template <int W>
+int launch_ell_w(const fb_blockilu* B, int lanes, TriView a, TriView b, const double* r,
+                 double* out, cudaStream_t st) {
+  return lanes == 2 ? launch_ell<2, W>(B, a, b, r, out, st) : launch_ell<32, W>(B, a, b, r, out, st);
+}
+
+}  // namespace
+
+// Convert the four triangular parts to the padded-row layout (all parts
+// padded to one width, a multiple of 8) and drop their CSR arrays.
+static int build_ell(fb_blockilu* B) {
+  // measured (tools/box_profile.py): padded rows pay off for the large p = 7
+  // blocks (~3000 rows, 24 rows per level); CSR rows are faster below
+  if (B->max_block <= 1000) return FB_OK;
+  if (B->max_block > 8191) return FB_OK;  // byte offsets must fit 16 bits
+  TriPart* parts[4] = {&B->L, &B->U, &B->Ut, &B->Lt};
+  DevBuf<int> mx;
+  FB_TRY_CUDA(mx.alloc(1));
+  FB_TRY_CUDA(cudaMemset(mx.ptr, 0, sizeof(int)));
+  const int64_t n = B->n;
+  for (TriPart* P : parts) {
+    ell_rowlen_kernel<<<ceil_div(n, 256), 256>>>(n, P->ip.ptr, mx.ptr);
+    FB_CHECK_LAUNCH();
+  }
+  int maxlen = 0;
+  FB_TRY_CUDA(cudaMemcpy(&maxlen, mx.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+  const int W = maxlen <= 8 ? 8 : (maxlen <= 16 ? 16 : (maxlen <= 24 ? 24 : (maxlen <= 32 ? 32 : 0)));
+  if (W == 0) return FB_OK;
+  for (TriPart* P : parts) {
+    FB_TRY_CUDA(P->ev.alloc(n * W));
+    FB_TRY_CUDA(P->eo.alloc(n * W));
+    ell_fill_kernel<<<ceil_div(n, 256), 256>>>(n, B->nblocks, B->block_ptr.ptr, P->ip.ptr,
+                                               P->ix.ptr, P->v.ptr, W, P->ev.ptr, P->eo.ptr);
+    FB_CHECK_LAUNCH();
+    FB_TRY_CUDA(cudaDeviceSynchronize());
+    P->width = W;
+    P->ix.reset();
+    P->v.reset();
+    P->ip.reset();
+  }
+  B->ell_w = W;
+  return FB_OK;
+}
 
 extern "C" {
 
@@ -584,6 +906,10 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
   FB_REQUIRE(block_ilu_smem(B->max_block) * (32 / block_ilu_lanes(B->max_block)) <= 200 * 1024 &&
                  B->max_block <= 65535,
              "block too large for shared memory");
+  if (g_bilu_pipe == 2) {
+    const int rc_ell = build_ell(B.get());
+    if (rc_ell != FB_OK) return rc_ell;
+  }
   *out = B.release();
   return FB_OK;
 }
@@ -601,7 +927,16 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
   const TriView b = transpose ? view(B->Lt, true) : view(B->U, false);
   cudaStream_t st = as_stream(stream);
   const int lanes = g_bilu_lanes ? g_bilu_lanes : block_ilu_lanes(B->max_block);
-  const bool pipe = g_bilu_pipe != 0;
+  if (B->ell_w) {
+    const int l2 = lanes == 2 ? 2 : 32;
+    switch (B->ell_w) {
+      case 8: return launch_ell_w<8>(B, l2, a, b, r, out, st);
+      case 16: return launch_ell_w<16>(B, l2, a, b, r, out, st);
+      case 24: return launch_ell_w<24>(B, l2, a, b, r, out, st);
+      default: return launch_ell_w<32>(B, l2, a, b, r, out, st);
+    }
+  }
+  const bool pipe = g_bilu_pipe >= 1;
   switch (lanes) {
     case 2: return pipe ? launch_block_ilu<2, true>(B, a, b, r, out, st) : launch_block_ilu<2, false>(B, a, b, r, out, st);
     case 4: return pipe ? launch_block_ilu<4, true>(B, a, b, r, out, st) : launch_block_ilu<4, false>(B, a, b, r, out, st);
@@ -812,14 +1147,19 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
   rc = device_levels(n, nblocks, bptr64.ptr, B->Lt, false, st);
   if (rc != FB_OK) return rc;
   FB_TRY_CUDA(cudaDeviceSynchronize());
+  if (g_bilu_pipe == 2) {
+    const int rc_ell = build_ell(B.get());
+    if (rc_ell != FB_OK) return rc_ell;
+  }
   *out = B.release();  // new2old stays empty: the level is block-major already
   return FB_OK;
 }
 
-extern "C" int fb_set_blockilu_pipeline(int on, int lanes) {
+extern "C" int fb_set_blockilu_pipeline(int mode, int lanes) {
   FB_REQUIRE(lanes == 0 || lanes == 2 || lanes == 4 || lanes == 8 || lanes == 16 || lanes == 32,
              "lanes per block must be 0 (auto), 2, 4, 8, 16 or 32");
-  g_bilu_pipe = on ? 1 : 0;
+  FB_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0, 1 or 2");
+  g_bilu_pipe = mode;
   g_bilu_lanes = lanes;
   return FB_OK;
 }
