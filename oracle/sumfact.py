@@ -165,6 +165,31 @@ def divergence_apply(v_dofs, nsv, p_dofs, nsp, Bv, Dv, Bp, Dp, d, grad, u):
     return scatter_add(p_dofs, evp.values_t(f), nsp)
 
 
+def convection_apply(element_dofs, ns, B, D, d, jinv, wdet, u):
+    """N(u)_i = int ((u . grad) u) . phi_i  (mfop.py:322-358): values and
+    physical gradients of every component at the qpts, then values_t."""
+    ev = Eval(B, D, d)
+    vals, gphys = [], {}
+    for c in range(d):
+        loc = gather(element_dofs, u[c * ns:(c + 1) * ns])
+        vals.append(ev.values(loc))
+        gs = ev.grads(loc)
+        for k in range(d):
+            gphys[c, k] = sum(jinv[..., m, k] * gs[m] for m in range(d))
+    out = np.empty(d * ns)
+    for c in range(d):
+        conv = sum(vals[k] * gphys[c, k] for k in range(d))
+        out[c * ns:(c + 1) * ns] = scatter_add(element_dofs, ev.values_t(conv * wdet), ns)
+    return out
+
+
+def make_convection(vspace, geom):
+    B, D = eval_matrices(vspace, geom.rule.points)
+    wdet = mass_factor(geom.detj, geom.w)
+    return lambda u: convection_apply(vspace.element_dofs, vspace.ndofs_scalar, B, D, vspace.dim,
+                                      geom.jinv, wdet, u)
+
+
 def constrained_apply(apply, constrained, x):
     xi = x.copy()
     xi[constrained] = 0.0

@@ -18,7 +18,8 @@ FB_ERR_CUDA = 2
 FB_ERR_OOM = 3
 FB_ERR_UNSUPPORTED = 4
 
-KIND = {"mass": 0, "stiffness": 1, "helmholtz": 2, "gradient": 3, "divergence": 4}
+KIND = {"mass": 0, "stiffness": 1, "helmholtz": 2, "gradient": 3, "divergence": 4,
+        "convection": 5}
 
 _vp = C.c_void_p
 _i64 = C.c_int64

@@ -43,13 +43,19 @@ __global__ void scatter_rows_kernel(int64_t nrows, const int* __restrict__ row_d
 }
 
 // Slot-ordered variant (fused path): each thread sums RPT consecutive rows
-// whose slots are contiguous, so the offsets come in one vector load and all
-// slot loads of the thread are independent (memory-level parallelism).
-constexpr int kRPT = 4;
-__global__ void scatter_slots_kernel(int64_t nrows, const int* __restrict__ row_dof,
-                                     const int* __restrict__ off, const double* __restrict__ S,
-                                     int64_t S_comp_stride, double* __restrict__ y,
-                                     int64_t y_comp_stride) {
+// whose slots are contiguous.  A conforming hex mesh shares a DoF among at
+// most 8 elements, so every row's slots are issued as 8 predicated loads up
+// front (all loads of the thread in flight together) and then summed in
+// slot order -- the same sequential sum, bitwise np.bincount.
+constexpr int kRPT = 2;
+constexpr int kMaxMult = 8;
+__global__ void __launch_bounds__(256) scatter_slots_kernel(int64_t nrows,
+                                                            const int* __restrict__ row_dof,
+                                                            const int* __restrict__ off,
+                                                            const double* __restrict__ S,
+                                                            int64_t S_comp_stride,
+                                                            double* __restrict__ y,
+                                                            int64_t y_comp_stride) {
   const int64_t r0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kRPT;
   if (r0 >= nrows) return;
   const int comp = blockIdx.y;
@@ -61,16 +67,22 @@ __global__ void scatter_slots_kernel(int64_t nrows, const int* __restrict__ row_
   for (int i = 0; i <= kRPT; ++i) o[i] = i <= nr ? __ldg(off + r0 + i) : 0;
 #pragma unroll
   for (int i = 0; i < kRPT; ++i) d[i] = i < nr ? __ldg(row_dof + r0 + i) : 0;
-  double acc[kRPT];
-#pragma unroll
-  for (int i = 0; i < kRPT; ++i) {
-    acc[i] = 0.0;
-    if (i < nr)
-      for (int k = o[i]; k < o[i + 1]; ++k) acc[i] += __ldg(Sc + k);
-  }
+  double v[kRPT][kMaxMult];
 #pragma unroll
   for (int i = 0; i < kRPT; ++i)
-    if (i < nr) yc[d[i]] = acc[i];
+#pragma unroll
+    for (int u = 0; u < kMaxMult; ++u)
+      v[i][u] = (i < nr && o[i] + u < o[i + 1]) ? __ldg(Sc + o[i] + u) : 0.0;
+#pragma unroll
+  for (int i = 0; i < kRPT; ++i) {
+    if (i >= nr) continue;
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < kMaxMult; ++u)
+      if (o[i] + u < o[i + 1]) acc += v[i][u];
+    for (int k = o[i] + kMaxMult; k < o[i + 1]; ++k) acc += __ldg(Sc + k);  // non-conforming
+    yc[d[i]] = acc;
+  }
 }
 
 __global__ void gather_kernel(int64_t total, const int* __restrict__ map,
@@ -337,7 +349,7 @@ static int finish_operator(fb_operator* op, const double* points, const double* 
     // E-vector scratch: largest of input/output E-vectors over components
     const int64_t nvl = rv->nloc, npl = rp ? rp->nloc : 0;
     int64_t need = 0;
-    if (kind <= FB_HELMHOLTZ) need = int64_t(vdim) * ne * nvl;
+    if (kind <= FB_HELMHOLTZ || kind == FB_CONVECTION) need = int64_t(vdim) * ne * nvl;
     else if (kind == FB_GRADIENT) need = int64_t(dim) * ne * nvl + ne * npl;
     else need = ne * npl;
     FB_TRY_CUDA(op->S.alloc(need));
@@ -483,7 +495,7 @@ int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction*
   FB_REQUIRE(out != nullptr, "out is NULL");
   *out = nullptr;
   FB_REQUIRE(rv != nullptr, "space restriction is NULL");
-  FB_REQUIRE(kind >= FB_MASS && kind <= FB_DIVERGENCE, "unknown operator kind");
+  FB_REQUIRE(kind >= FB_MASS && kind <= FB_CONVECTION, "unknown operator kind");
   FB_REQUIRE(nq1 >= 1 && nq1 <= 32, "unsupported rule size");
   FB_REQUIRE(B != nullptr && D != nullptr && points != nullptr, "B/D/points are NULL");
   std::unique_ptr<fb_operator> op(new fb_operator());
@@ -514,6 +526,13 @@ int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction*
     }
     if (kind != FB_MASS)
       relayout(stiff, ne, nqd, ksym, fac.data(), op->fstride, koff, lanes, op->nfac);
+  } else if (kind == FB_CONVECTION) {
+    FB_REQUIRE(vdim == dim, "convection expects a vector space with vdim == dim");
+    FB_REQUIRE(grad != nullptr, "gradient factor required");
+    op->nfac = dim * dim;
+    op->fstride = (int64_t(op->nfac) * nqd + 1) / 2 * 2;
+    fac.assign(size_t(ne) * op->fstride, 0.0);
+    relayout(grad, ne, nqd, dim * dim, fac.data(), op->fstride, 0);
   } else {
     FB_REQUIRE(rp != nullptr, "pressure restriction is NULL");
     FB_REQUIRE(rp->ne == ne && rp->dim == dim, "velocity/pressure spaces disagree");
@@ -541,7 +560,7 @@ int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restric
   FB_REQUIRE(out != nullptr, "out is NULL");
   *out = nullptr;
   FB_REQUIRE(rv != nullptr, "space restriction is NULL");
-  FB_REQUIRE(kind >= FB_MASS && kind <= FB_DIVERGENCE, "unknown operator kind");
+  FB_REQUIRE(kind >= FB_MASS && kind <= FB_CONVECTION, "unknown operator kind");
   FB_REQUIRE(nq1 >= 1 && nq1 <= 32, "unsupported rule size");
   FB_REQUIRE(points && weights && B && D, "points/weights/B/D are NULL");
   FB_REQUIRE(rv->ne == 0 || corners != nullptr, "corners are NULL");
@@ -558,6 +577,9 @@ int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restric
   const int ksym = dim == 2 ? 3 : 6;
   if (kind <= FB_HELMHOLTZ) {
     op->nfac = (kind == FB_MASS) ? 1 : (kind == FB_STIFFNESS ? ksym : ksym + 1);
+  } else if (kind == FB_CONVECTION) {
+    FB_REQUIRE(vdim == dim, "convection expects a vector space with vdim == dim");
+    op->nfac = dim * dim;
   } else {
     FB_REQUIRE(rp != nullptr && rp->ne == ne && rp->dim == dim, "pressure restriction mismatch");
     FB_REQUIRE(Bp != nullptr && Dp != nullptr, "Bp/Dp required");
@@ -630,7 +652,7 @@ static int general_apply(const fb_operator* op, int gkind, const double* x, doub
   const fb_restriction* rin = rv;
   const fb_restriction* rout = rv;
   int ncomp_out = 1;
-  if (gkind <= kgHelm) {
+  if (gkind <= kgHelm || gkind == kgConv) {
     gy = op->vdim;
     ncomp_out = op->vdim;
     P.in_comp_stride = rv->ndofs;
@@ -699,6 +721,7 @@ int fb_operator_apply(const fb_operator* op, const double* x, double* y, void* s
     case FB_STIFFNESS: gk = kgStiff; break;
     case FB_HELMHOLTZ: gk = kgHelm; break;
     case FB_GRADIENT: gk = kgGrad; break;
+    case FB_CONVECTION: gk = kgConv; break;
     default: gk = kgDiv; break;
   }
   return general_apply(op, gk, x, y, st);

@@ -13,7 +13,7 @@
 
 namespace fb {
 
-enum GenKind { kgMass = 0, kgStiff = 1, kgHelm = 2, kgGrad = 3, kgDiv = 4, kgGradT = 5 };
+enum GenKind { kgMass = 0, kgStiff = 1, kgHelm = 2, kgGrad = 3, kgDiv = 4, kgGradT = 5, kgConv = 6 };
 
 struct SFGParams {
   const int* __restrict__ map_in;   // (ne, nin^dim)
@@ -231,6 +231,36 @@ __global__ void sf_general_kernel(const __grid_constant__ SFGParams P) {
       for (int l = tid; l < nvd; l += nt) ye[l] = out[l];
       __syncthreads();
     }
+    return;
+  }
+
+  if (kind == kgConv) {
+    // convection load, output component comp (mfop.py:341-358):
+    //   conv_c = sum_k U_k sum_m (wdet Jinv[m,k]) dU_c/dxi_m,  y_c = B^T conv_c
+    // factors are the gradient set fe[(k*dim + m)] = wdet Jinv[m,k]
+    for (int k = 0; k < dim; ++k) {  // values of every component -> f[k]
+      const double* xk = P.x + k * P.in_comp_stride;
+      for (int l = tid; l < nvd; l += nt) xin[l] = xk[P.map_in[e * nvd + l]];
+      __syncthreads();
+      gen_values(dim, xin, nv, Bv, nq, f[k], false, t0, t1);
+    }
+    const double* xc = P.x + comp * P.in_comp_stride;
+    for (int l = tid; l < nvd; l += nt) xin[l] = xc[P.map_in[e * nvd + l]];
+    __syncthreads();
+    gen_grads(dim, xin, nv, Bv, Dv, nq, g, t0, t1);
+    for (int qp = tid; qp < nqd; qp += nt) {
+      double s = 0.0;
+      for (int k = 0; k < dim; ++k) {
+        double gk = 0.0;
+        for (int m = 0; m < dim; ++m) gk += fe[(k * dim + m) * nqd + qp] * g[m][qp];
+        s += f[k][qp] * gk;
+      }
+      vals[qp] = s;
+    }
+    __syncthreads();
+    gen_values(dim, vals, nq, BvT, nv, xin, false, t0, t1);
+    double* ye = P.ye + (int64_t(comp) * P.ne + e) * nvd;
+    for (int l = tid; l < nvd; l += nt) ye[l] = xin[l];
     return;
   }
 

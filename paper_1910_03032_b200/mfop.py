@@ -358,6 +358,36 @@ class DivergenceOperator(_MixedOperator):
         self.in_size, self.out_size = vspace.ndofs, pspace.ndofs_scalar
 
 
+class ConvectionOperator(_DeviceOperator):
+    """Nonlinear convection load N(u)_i = int ((u . grad) u) . phi_i
+    (mfop.py:322-358), used by the projection stepper's extrapolated
+    convection term (timeint.py:356).  One kernel computes the values of all
+    components and the physical gradient of the output component at the
+    quadrature points (factors wdet Jinv, the gradient set) and the
+    transposed interpolation; the E->L sum is the deterministic one."""
+
+    kind = "convection"
+
+    def __init__(self, vspace, geom):
+        _check_rule_match(vspace, geom)
+        if vspace.vdim != vspace.dim:
+            raise ValueError("convection expects a vector space with vdim == dim")
+        t0 = time.perf_counter()
+        self.vspace = vspace
+        self.geom = geom
+        pts = np.asarray(geom.rule.points, dtype=np.float64)
+        self.rule_points = pts
+        self.B, self.D = _eval_matrices(vspace, pts)
+        self.factors = QPointFactors(grad=None if _is_device_geom(geom) else _grad_factor(geom))
+        self.restriction = restriction(vspace)
+        self._create(self.kind, self.restriction, None, vspace.dim, pts, self.B, self.D, None,
+                     None, None, None, self.factors.grad, geom)
+        n = vspace.ndofs
+        self.shape = (n, n)
+        self.in_size = self.out_size = n
+        self.setup_seconds = time.perf_counter() - t0
+
+
 class ConstrainedOperator(Operator):
     """Identity on constrained rows, the inner operator elsewhere
     (mfop.py:416-433): xi = x; xi[C] = 0; y = A xi; y[C] = x[C]."""
@@ -409,7 +439,9 @@ def setup(kind, space=None, geom=None, vspace=None, pspace=None, nu=1.0, c=0.0):
         return GradientOperator(vspace, pspace, geom)
     if kind == "divergence":
         return DivergenceOperator(vspace, pspace, geom)
-    if kind in ("convection", "curlcurl"):
+    if kind == "convection":
+        return ConvectionOperator(vspace or space, geom)
+    if kind == "curlcurl":
         raise NotImplementedError(f"operator kind {kind!r} is outside the B200 hot path")
     raise ValueError(f"unknown operator kind {kind!r}")
 

@@ -240,7 +240,34 @@ def make_stokes():
     return {"stokes": manifest}
 
 
-GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers, "stokes": make_stokes}
+# (name, d, counts, periodic, perturb, p, seed): ConvectionOperator (mfop.py:322-358)
+CONV_CASES = [
+    ("conv_2d_p3", 2, (4, 3), None, 0.08, 3, 1),
+    ("conv_2d_p6", 2, (2, 2), None, 0.05, 6, 2),
+    ("conv_3d_p2", 3, (3, 2, 2), None, 0.08, 2, 3),
+    ("conv_3d_p4", 3, (2, 2, 2), None, 0.05, 4, 4),
+    ("conv_3d_p5_periodic", 3, (3, 3, 3), (True,) * 3, 0.05, 5, 5),
+    ("conv_3d_p7", 3, (2, 1, 1), None, 0.05, 7, 6),
+]
+
+
+def make_extras():
+    """Next-row operators of SURVEY 8(f) item 4 (cfg5 projection step)."""
+    mesh, fespace, mfop, _, _, _ = ref_modules()
+    out, manifest = {}, []
+    for (name, d, counts, periodic, perturb, p, seed) in CONV_CASES:
+        _, vs, geom = build(mesh, fespace, d, counts, periodic, perturb, p, vdim=d)
+        op = mfop.ConvectionOperator(vs, geom)
+        u = np.random.default_rng(seed).standard_normal(vs.ndofs)
+        out[name + "/y"] = op.apply(u)
+        manifest.append(dict(name=name, d=d, counts=counts, periodic=periodic, perturb=perturb,
+                             p=p, seed=seed, ndofs=int(vs.ndofs)))
+    np.savez_compressed(os.path.join(HERE, "extras.npz"), **out)
+    return {"convection": manifest}
+
+
+GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers, "stokes": make_stokes,
+          "extras": make_extras}
 
 
 def main(argv):

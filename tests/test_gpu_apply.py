@@ -139,3 +139,21 @@ def test_full_size_properties(p):
     ones = torch.ones(sp.ndofs, dtype=torch.float64, device="cuda")
     assert abs((ones @ M.apply(ones)).item() - 1.0) < 1e-12
     assert L.apply(ones).abs().max().item() < 1e-10
+
+
+CONV = {c["name"]: c for c in MAN.get("convection", [])}
+
+
+@pytest.mark.parametrize("device_geom", [False, True])
+@pytest.mark.parametrize("name", sorted(CONV))
+def test_convection_matches_reference(name, device_geom):
+    """ConvectionOperator on the device vs the reference's (extras.npz)."""
+    from paper_1910_03032_b200 import geometry, mfop
+    c = CONV[name]
+    gold = load("extras")
+    m, vs, geom = build(c["d"], c["counts"], c["periodic"], c["perturb"], c["p"], vdim=c["d"])
+    if device_geom:
+        geom = geometry.DeviceGeometry(m, vs.basis.quad)
+    op = mfop.setup("convection", vspace=vs, geom=geom)
+    u = np.random.default_rng(c["seed"]).standard_normal(vs.ndofs)
+    assert rel_err(op.apply(u), gold[name + "/y"]) < 1e-12
