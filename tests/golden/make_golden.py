@@ -262,8 +262,38 @@ def make_extras():
         out[name + "/y"] = op.apply(u)
         manifest.append(dict(name=name, d=d, counts=counts, periodic=periodic, perturb=perturb,
                              p=p, seed=seed, ndofs=int(vs.ndofs)))
+    # cfg5-shaped projection stepping (timeint.py:218-388): periodic 3D
+    # Taylor-Green, BDF3/EXT3, equal order (SURVEY 8(c) recorded counts)
+    sys.path.insert(0, REF)
+    from flowbench import timeint
+    tgv = dict(name="tgv3d_p3", counts=(4, 4, 4), p=3, k=3, dt=0.02, nu=1.0 / 1600.0, steps=4)
+    m = mesh.cartesian_mesh(tgv["counts"], lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                            periodic=(True,) * 3)
+    vs = fespace.FESpace(m, tgv["p"], vdim=3)
+    ps = fespace.FESpace(m, tgv["p"])
+    geom = mesh.compute_geometric_factors(m, vs.basis.quad)
+    st = timeint.ProjectionStepper(vs, ps, geom, k=tgv["k"], dt=tgv["dt"], nu=tgv["nu"])
+    u0 = vs.project(tgv_velocity)
+    st.initialize(u0)
+    its = []
+    for _ in range(tgv["steps"]):
+        r = st.step()
+        its.append([r.mass_iters, r.pressure_iters, r.helmholtz_iters])
+    out["tgv3d_p3/u0"] = u0
+    out["tgv3d_p3/u"] = st.u
+    out["tgv3d_p3/p"] = st.p
+    out["tgv3d_p3/its"] = np.array(its)
+    out["tgv3d_p3/energy"] = np.array([st.kinetic_energy()])
     np.savez_compressed(os.path.join(HERE, "extras.npz"), **out)
-    return {"convection": manifest}
+    return {"convection": manifest, "projection": [dict(tgv, counts=list(tgv["counts"]),
+                                                        iterations=its)]}
+
+
+def tgv_velocity(x):
+    """3D Taylor-Green initial velocity on [-pi, pi]^3 (vdim = 3 columns)."""
+    X, Y, Z = x[:, 0], x[:, 1], x[:, 2]
+    return np.stack([np.sin(X) * np.cos(Y) * np.cos(Z), -np.cos(X) * np.sin(Y) * np.cos(Z),
+                     np.zeros_like(X)], axis=1)
 
 
 GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers, "stokes": make_stokes,
