@@ -1036,7 +1036,7 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
   *fail_row = -1;
   FB_REQUIRE(A != nullptr && block_ptr_host != nullptr, "bad block ILU input");
   const int64_t n = A->nrows;
-  FB_REQUIRE(A->ncols == n, "block ILU needs a square matrix");
+  FB_REQUIRE(A->ncols >= n, "block ILU needs ncols >= nrows (columns beyond the rows are ghosts)");
   FB_REQUIRE(nblocks >= 1 && block_ptr_host[0] == 0 && block_ptr_host[nblocks] == n,
              "block_ptr must cover all rows");
   std::unique_ptr<fb_blockilu> B(new fb_blockilu());

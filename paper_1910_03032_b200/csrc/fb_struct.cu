@@ -38,6 +38,7 @@ struct fb_transfer {
   const fb_restriction* hmap = nullptr;  // coarse DoFs of each fine element's parent (ne, nc^3)
   int nf = 0, nc = 0;
   int64_t ne = 0, counts[3] = {0, 0, 0};
+  int64_t origin[3] = {0, 0, 0};  // global coordinates of local element (0,0,0)
   fb::DevBuf<double> W;   // (nw, nf, nc) weight tables
   fb::DevBuf<int> widx;   // per axis, per element coordinate: table index
   fb::DevBuf<double> E;   // (ne, nc^3) restriction contributions
@@ -70,14 +71,17 @@ struct BoxParams {
   int64_t Nx, Ny, Nz;   // lattice sizes (n_a p + 1)
   const double* corners;  // (ne, 8, 3)
   const int* lid;         // lattice -> DoF id, x fastest
-  int kind, constrain;
+  int kind, constrain;   // constrain: bitmask of constrained box faces (x-, x+, y-, y+, z-, z+)
+  int64_t nrows;         // rows with id >= nrows are not assembled (other ranks own them)
   double nu, c;
   double nodes[17];
 };
 
 __device__ __forceinline__ bool on_box_boundary(const BoxParams& P, int64_t gx, int64_t gy,
                                                 int64_t gz) {
-  return gx == 0 || gy == 0 || gz == 0 || gx == P.Nx - 1 || gy == P.Ny - 1 || gz == P.Nz - 1;
+  const int m = P.constrain;
+  return ((m & 1) && gx == 0) || ((m & 2) && gx == P.Nx - 1) || ((m & 4) && gy == 0) ||
+         ((m & 8) && gy == P.Ny - 1) || ((m & 16) && gz == 0) || ((m & 32) && gz == P.Nz - 1);
 }
 
 // physical position of lattice point (gx,gy,gz) through element (ex,ey,ez)
@@ -153,7 +157,8 @@ __global__ void lor_box_count_kernel(BoxParams P, int* __restrict__ cnt) {
   const int64_t total = P.Nx * P.Ny * P.Nz;
   if (t >= total) return;
   const int64_t gx = t % P.Nx, gy = (t / P.Nx) % P.Ny, gz = t / (P.Nx * P.Ny);
-  cnt[P.lid[t]] = axis_span(gx, P.Nx) * axis_span(gy, P.Ny) * axis_span(gz, P.Nz);
+  const int row = P.lid[t];
+  if (row >= 0 && row < P.nrows) cnt[row] = axis_span(gx, P.Nx) * axis_span(gy, P.Ny) * axis_span(gz, P.Nz);
 }
 
 __global__ void __launch_bounds__(128) lor_box_fill_kernel(BoxParams P,
@@ -163,10 +168,11 @@ __global__ void __launch_bounds__(128) lor_box_fill_kernel(BoxParams P,
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t total = P.Nx * P.Ny * P.Nz;
   if (t >= total) return;
+  if (P.lid[t] < 0 || P.lid[t] >= P.nrows) return;  // a row of another rank
   const int64_t g[3] = {t % P.Nx, (t / P.Nx) % P.Ny, t / (P.Nx * P.Ny)};
   const int64_t N[3] = {P.Nx, P.Ny, P.Nz};
   const int64_t ne_[3] = {P.nx, P.ny, P.nz};
-  const bool brow = P.constrain && on_box_boundary(P, g[0], g[1], g[2]);
+  const bool brow = on_box_boundary(P, g[0], g[1], g[2]);
   double acc[27];
   for (int k = 0; k < 27; ++k) acc[k] = 0.0;
   if (!brow) {
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(128) lor_box_fill_kernel(BoxParams P,
         const int col = P.lid[(hz * N[1] + hy) * N[0] + hx];
         double val = acc[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)];
         if (brow) val = (dx == 0 && dy == 0 && dz == 0) ? 1.0 : 0.0;
-        else if (P.constrain && on_box_boundary(P, hx, hy, hz)) val = 0.0;
+        else if (on_box_boundary(P, hx, hy, hz)) val = 0.0;
         int j = m - 1;
         while (j >= 0 && cols[j] > col) {
           cols[j + 1] = cols[j];
@@ -233,6 +239,7 @@ struct TransferView {
   const double* W;   // (nw, nf, nc)
   const int* widx;   // [nx | ny | nz]
   int64_t nx, ny, nz;
+  int64_t ox, oy, oz;
   int nf, nc;
 };
 
@@ -244,6 +251,10 @@ __device__ __forceinline__ void transfer_elem(const TransferView& T, int64_t e, 
   ec[2] = e / (T.nx * T.ny);
   const int64_t off[3] = {0, T.nx, T.nx + T.ny};
   for (int a = 0; a < 3; ++a) Wa[a] = T.W + int64_t(T.widx[off[a] + ec[a]]) * T.nf * T.nc;
+  // ownership is decided in global element coordinates (slab-local levels)
+  ec[0] += T.ox;
+  ec[1] += T.oy;
+  ec[2] += T.oz;
 }
 
 // first-touch ownership on a structured box: local lattice index 0 along an
@@ -335,9 +346,10 @@ using namespace fb;
 
 extern "C" {
 
-int fb_lor_assemble_box(int p, const int64_t* counts, const double* corners_dev,
-                        const double* nodes, const int* lattice_ids_dev, int kind, double nu,
-                        double c, int constrain_boundary, fb_csr** out) {
+int fb_lor_assemble_box_rows(int p, const int64_t* counts, const double* corners_dev,
+                             const double* nodes, const int* lattice_ids_dev, int kind,
+                             double nu, double c, int constrain_faces, int64_t nrows,
+                             int64_t ncols, fb_csr** out) {
   FB_REQUIRE(out != nullptr, "out is NULL");
   *out = nullptr;
   FB_REQUIRE(p >= 1 && p <= 16, "degree must be in [1, 16]");
@@ -355,19 +367,22 @@ int fb_lor_assemble_box(int p, const int64_t* counts, const double* corners_dev,
   P.corners = corners_dev;
   P.lid = lattice_ids_dev;
   P.kind = kind;
-  P.constrain = constrain_boundary ? 1 : 0;
+  P.constrain = constrain_faces & 63;
   P.nu = nu;
   P.c = c;
   for (int i = 0; i <= p; ++i) P.nodes[i] = nodes[i];
-  const int64_t n = P.Nx * P.Ny * P.Nz;
-  FB_REQUIRE(n < (int64_t(1) << 31), "lattice exceeds int32 DoF ids");
+  const int64_t npts = P.Nx * P.Ny * P.Nz;
+  FB_REQUIRE(npts < (int64_t(1) << 31), "lattice exceeds int32 DoF ids");
+  const int64_t n = nrows < 0 ? npts : nrows;
+  P.nrows = n;
   std::unique_ptr<fb_csr> A(new fb_csr());
-  A->nrows = A->ncols = n;
+  A->nrows = n;
+  A->ncols = ncols < 0 ? npts : ncols;
   A->warp_rows = 1;
   cudaStream_t st = 0;
   DevBuf<int> cnt;
   FB_TRY_CUDA(cnt.alloc(n));
-  lor_box_count_kernel<<<ceil_div(n, 256), 256, 0, st>>>(P, cnt.ptr);
+  lor_box_count_kernel<<<ceil_div(npts, 256), 256, 0, st>>>(P, cnt.ptr);
   FB_CHECK_LAUNCH();
   FB_TRY_CUDA(A->indptr.alloc(n + 1));
   int rc = exclusive_offsets(cnt.ptr, n, A->indptr.ptr, st);
@@ -376,12 +391,19 @@ int fb_lor_assemble_box(int p, const int64_t* counts, const double* corners_dev,
   FB_TRY_CUDA(cudaMemcpy(&A->nnz, A->indptr.ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
   FB_TRY_CUDA(A->indices.alloc(A->nnz));
   FB_TRY_CUDA(A->data.alloc(A->nnz));
-  lor_box_fill_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P, A->indptr.ptr, A->indices.ptr,
-                                                        A->data.ptr);
+  lor_box_fill_kernel<<<ceil_div(npts, 128), 128, 0, st>>>(P, A->indptr.ptr, A->indices.ptr,
+                                                           A->data.ptr);
   FB_CHECK_LAUNCH();
   FB_TRY_CUDA(cudaDeviceSynchronize());
   *out = A.release();
   return FB_OK;
+}
+
+int fb_lor_assemble_box(int p, const int64_t* counts, const double* corners_dev,
+                        const double* nodes, const int* lattice_ids_dev, int kind, double nu,
+                        double c, int constrain_boundary, fb_csr** out) {
+  return fb_lor_assemble_box_rows(p, counts, corners_dev, nodes, lattice_ids_dev, kind, nu, c,
+                                  constrain_boundary ? 63 : 0, -1, -1, out);
 }
 
 int fb_csr_info(const fb_csr* A, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
@@ -442,9 +464,32 @@ int fb_transfer_create(const fb_restriction* fine, const fb_restriction* hmap,
 
 void fb_transfer_destroy(fb_transfer* T) { delete T; }
 
+int fb_transfer_set_origin(fb_transfer* T, int64_t x0, int64_t y0, int64_t z0) {
+  FB_REQUIRE(T != nullptr && x0 >= 0 && y0 >= 0 && z0 >= 0, "bad transfer origin");
+  T->origin[0] = x0;
+  T->origin[1] = y0;
+  T->origin[2] = z0;
+  return FB_OK;
+}
+
+__global__ void index_add_kernel(int64_t n, const int* __restrict__ idx,
+                                 const double* __restrict__ v, double* __restrict__ y) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[idx[i]] += v[i];
+}
+
+// y[idx[i]] += v[i] (indices distinct; halo partial sums on slab cut planes)
+int fb_index_add(int64_t n, const int* idx, const double* v, double* y, void* stream) {
+  if (n <= 0) return FB_OK;
+  index_add_kernel<<<ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, idx, v, y);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
 static TransferView transfer_view(const fb_transfer* T) {
   return TransferView{restriction_map(T->fine), restriction_map(T->hmap), T->W.ptr, T->widx.ptr,
-                      T->counts[0], T->counts[1], T->counts[2], T->nf, T->nc};
+                      T->counts[0], T->counts[1], T->counts[2], T->origin[0], T->origin[1],
+                      T->origin[2], T->nf, T->nc};
 }
 
 // xf (fine L-vector) = P xc: every fine DoF written once, by its owner element

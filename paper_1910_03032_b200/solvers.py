@@ -180,8 +180,12 @@ def collocated_mass_diagonal(space, constrained=None):
 
 # -- Krylov --------------------------------------------------------------------------
 
-def cg(A, b, precond=None, config=None, x0=None, project=None):
-    """Preconditioned CG with the reference recurrence (solvers.py:108-169)."""
+def cg(A, b, precond=None, config=None, x0=None, project=None, inner=None):
+    """Preconditioned CG with the reference recurrence (solvers.py:108-169).
+    inner(x, y, out): the inner product into a 1-element device tensor
+    (default: the deterministic libfbb200 dot; the sharded solver passes an
+    owned-slice dot + all-reduce)."""
+    dot_into = inner if inner is not None else vec.dot_into
     apply_A = _device_apply(A)
     M = _device_apply(precond) if precond is not None else None
     proj = _device_project(project) if project is not None else None
@@ -209,7 +213,7 @@ def cg(A, b, precond=None, config=None, x0=None, project=None):
         vec.copy(r, z)
     if proj is not None:
         proj(z, z)
-    vec.dot_into(r, z, s[0:1])
+    dot_into(r, z, s[0:1])
     rz = float(s[0].item())
     norm0 = math.sqrt(abs(rz))
     history = [1.0]
@@ -228,7 +232,7 @@ def cg(A, b, precond=None, config=None, x0=None, project=None):
     converged = False
     for it in range(1, cfg.max_iters + 1):
         apply_A(p, Ap)
-        vec.dot_into(p, Ap, s[1:2])
+        dot_into(p, Ap, s[1:2])
         vec.safe_div(s[0:1], s[1:2], s[2:3])  # alpha = rz / pAp (0 if pAp <= 0)
         vec.axpy_dev(s[2:3], p, x, +1)
         if it % 50 == 0:
@@ -245,7 +249,7 @@ def cg(A, b, precond=None, config=None, x0=None, project=None):
             vec.copy(r, z)
         if proj is not None:
             proj(z, z)
-        vec.dot_into(r, z, s[3:4])
+        dot_into(r, z, s[3:4])
         pAp, _, rz_new = s[1:4].tolist()
         if pAp <= 0.0:
             break

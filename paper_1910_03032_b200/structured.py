@@ -68,9 +68,10 @@ def _axis_tables(n_el, p, block):
     return {"N": N, "nb": nb, "TW": TW, "B": blk[o], "C": cnt[o], "SP": SP[o], "R": l - s}
 
 
-def box_lattice_ids(counts, p, block, device=None):
+def box_lattice_ids(counts, p, block, device=None, gz_range=None):
     """(Nz, Ny, Nx) int64 tensor: DoF id of every lattice point, plus the
-    (nblocks+1) block row offsets (numpy)."""
+    (nblocks+1) block row offsets (numpy).  gz_range = (g0, g1) restricts the
+    result to the lattice planes g0 <= gz < g1 (ids stay global)."""
     device = device if device is not None else torch.device("cpu")
     tx, ty, tz = (_axis_tables(counts[a], p, block) for a in range(3))
     bsize = (tz["TW"][:, None, None] * ty["TW"][None, :, None] * tx["TW"][None, None, :])
@@ -81,6 +82,10 @@ def box_lattice_ids(counts, p, block, device=None):
     def T(a, shape):
         return torch.from_numpy(np.ascontiguousarray(a)).to(device).view(shape)
 
+    if gz_range is not None:
+        g0, g1 = gz_range
+        tz = {k: (v[g0:g1] if isinstance(v, np.ndarray) and v.shape[0] == tz["N"] else v)
+              for k, v in tz.items()}
     zs, ys, xs = (-1, 1, 1), (1, -1, 1), (1, 1, -1)
     Bz, By, Bx = T(tz["B"], zs), T(ty["B"], ys), T(tx["B"], xs)
     TWy, TWx = T(ty["TW"][ty["B"]], ys), T(tx["TW"][tx["B"]], xs)

@@ -1,0 +1,78 @@
+"""Sharded scale mode (paper_1910_03032_b200/dist_box.py).
+
+The multi-rank path runs as R threads of one process on one GPU through the
+in-process communicator (host-side barriers only; no kernel waits on another
+rank), so the NCCL code path's algorithm -- slab layout, halo exchanges,
+owned-slice dots, agglomerated Q1 solve -- is checked against the single-GPU
+scale-mode solve on the same global problem."""
+
+import numpy as np
+import pytest
+
+from tests.cases import rel_err
+
+
+def test_slab_layers_align_to_units():
+    from paper_1910_03032_b200 import dist_box as D
+    assert D.slab_layers(12, 3, 4) == [(0, 4), (4, 8), (8, 12)]
+    assert D.slab_layers(16, 3, 4) == [(0, 4), (4, 8), (8, 16)]
+    with pytest.raises(ValueError):
+        D.slab_layers(10, 2, 4)
+    with pytest.raises(ValueError):
+        D.slab_layers(8, 3, 4)
+
+
+def test_thread_comm_exchange_and_reductions():
+    import torch
+    from paper_1910_03032_b200 import dist_box as D
+
+    def fn(comm):
+        r, w = comm.rank, comm.world
+        sd = torch.full((3,), float(10 * r + 1)) if r > 0 else None
+        su = torch.full((3,), float(10 * r + 2)) if r < w - 1 else None
+        rd = torch.empty(3) if r > 0 else None
+        ru = torch.empty(3) if r < w - 1 else None
+        comm.exchange(sd, su, rd, ru)
+        s = comm.allreduce_sum(torch.tensor([float(r + 1)]))
+        g = comm.allgather(torch.arange(r + 1, dtype=torch.float64), list(range(1, w + 1)))
+        return (None if rd is None else rd[0].item(), None if ru is None else ru[0].item(),
+                s.item(), g.tolist())
+
+    import unittest.mock as um
+    with um.patch.object(torch.cuda, "synchronize", lambda: None):
+        out = D.run_threads(3, fn)
+    assert out[0][:2] == (None, 11.0) and out[1][:2] == (2.0, 21.0) and out[2][:2] == (12.0, None)
+    assert all(o[2] == 6.0 for o in out)
+    assert out[0][3] == [0.0, 0.0, 1.0, 0.0, 1.0, 2.0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,counts,p", [(2, (3, 4, 8), 4), (3, (4, 3, 12), 2), (2, (2, 3, 8), 7)])
+def test_sharded_lor_pcg_matches_single_gpu(world, counts, p):
+    import torch
+    from paper_1910_03032_b200 import dist_box as D, solvers, structured as S
+    cfg = solvers.SolverConfig(rel_tol=1e-8, max_iters=300)
+    mesh = S.box_mesh(counts, perturb=0.05, seed=1)
+    ref = S.helmholtz_box_problem(counts, p, c=10.0, max_coarse=100)
+    x_ref, rep_ref = solvers.cg(ref["A"], ref["b"], precond=ref["M"], config=cfg)
+    x_ref = x_ref.cpu().numpy()
+    y_ref = ref["A"].apply(ref["b"]).cpu().numpy()
+
+    def fn(comm):
+        pr = D.helmholtz_slab_problem(comm, counts, p, c=10.0, max_coarse=100, mesh=mesh)
+        lv = pr["level"]
+        y = torch.empty_like(pr["b"])
+        pr["A"].apply_into(pr["b"], y)
+        x, rep = D.dist_cg(pr["A"], pr["b"], pr["M"], comm, lv.n_own, cfg)
+        return lv.off, lv.n_own, y[:lv.n_own].cpu().numpy(), x[:lv.n_own].cpu().numpy(), rep
+
+    out = D.run_threads(world, fn)
+    assert [o[0] for o in out] == list(np.cumsum([0] + [o[1] for o in out[:-1]]))
+    y = np.concatenate([o[2] for o in out])
+    x = np.concatenate([o[3] for o in out])
+    assert rel_err(y, y_ref) < 1e-13
+    for o in out:
+        assert o[4].iterations == out[0][4].iterations
+    assert abs(out[0][4].iterations - rep_ref.iterations) <= 1, (out[0][4].iterations,
+                                                                 rep_ref.iterations)
+    assert rel_err(x, x_ref) < 1e-7
