@@ -46,6 +46,53 @@ def test_thread_comm_exchange_and_reductions():
     assert out[0][3] == [0.0, 0.0, 1.0, 0.0, 1.0, 2.0]
 
 
+def _torchcomm_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1910_03032_b200 import dist_box as D
+        comm = D.TorchComm()
+        r, w = comm.rank, comm.world
+        sd = torch.full((3,), float(10 * r + 1)) if r > 0 else None
+        su = torch.full((3,), float(10 * r + 2)) if r < w - 1 else None
+        rd = torch.empty(3) if r > 0 else None
+        ru = torch.empty(3) if r < w - 1 else None
+        comm.exchange(sd, su, rd, ru)
+        s = comm.allreduce_sum(torch.tensor([float(r + 1)], dtype=torch.float64))
+        g = comm.allgather(torch.arange(r + 1, dtype=torch.float64), list(range(1, w + 1)))
+        q.put((r, None if rd is None else rd[0].item(), None if ru is None else ru[0].item(),
+               s.item(), g.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torch_comm_over_gloo_matches_thread_comm():
+    """The torch.distributed communicator (NCCL on the GPU box) has the
+    same exchange / all-reduce / all-gather semantics (gloo, 3 processes)."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_torchcomm_worker, args=(r, 3, port, q)) for r in range(3)]
+    for pr in procs:
+        pr.start()
+    out = sorted(q.get(timeout=240) for _ in range(3))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert out[0][1:3] == (None, 11.0) and out[1][1:3] == (2.0, 21.0) and out[2][1:3] == (12.0, None)
+    assert all(o[3] == 6.0 for o in out)
+    assert all(o[4] == [0.0, 0.0, 1.0, 0.0, 1.0, 2.0] for o in out)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,counts,p", [(2, (3, 4, 8), 4), (3, (4, 3, 12), 2), (2, (2, 3, 8), 7)])
 def test_sharded_lor_pcg_matches_single_gpu(world, counts, p):
