@@ -42,47 +42,40 @@ __global__ void scatter_rows_kernel(int64_t nrows, const int* __restrict__ row_d
   y[comp * y_comp_stride + dof] = acc;
 }
 
-// Slot-ordered variant (fused path): each thread sums RPT consecutive rows
-// whose slots are contiguous.  A conforming hex mesh shares a DoF among at
-// most 8 elements, so every row's slots are issued as 8 predicated loads up
-// front (all loads of the thread in flight together) and then summed in
-// slot order -- the same sequential sum, bitwise np.bincount.
-constexpr int kRPT = 2;
-constexpr int kMaxMult = 8;
-__global__ void __launch_bounds__(256) scatter_slots_kernel(int64_t nrows,
+// Slot sum of the fused path: shared rows are grouped by multiplicity m and
+// a class stores its contributions slot-major (contribution j of all its rows,
+// then j+1, ...), so one thread per row reads its m slots as m coalesced
+// loads and sums them in flat-E order -- the sequential sum, bitwise
+// np.bincount -- and the destinations are ascending DoF ids.
+struct SlotClasses {
+  int n;
+  int m[16];
+  int64_t row[17], slot[16];
+};
+
+__global__ void __launch_bounds__(256) scatter_slots_kernel(SlotClasses K,
                                                             const int* __restrict__ row_dof,
-                                                            const int* __restrict__ off,
                                                             const double* __restrict__ S,
                                                             int64_t S_comp_stride,
                                                             double* __restrict__ y,
                                                             int64_t y_comp_stride) {
-  const int64_t r0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kRPT;
-  if (r0 >= nrows) return;
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= K.row[K.n]) return;
+  int c = 0;
+  while (r >= K.row[c + 1]) ++c;
   const int comp = blockIdx.y;
-  const double* __restrict__ Sc = S + comp * S_comp_stride;
-  double* __restrict__ yc = y + comp * y_comp_stride;
-  int o[kRPT + 1], d[kRPT];
-  const int nr = (nrows - r0) < kRPT ? int(nrows - r0) : kRPT;
+  const int64_t k = r - K.row[c], nc = K.row[c + 1] - K.row[c];
+  const double* __restrict__ Sc = S + comp * S_comp_stride + K.slot[c] + k;
+  const int m = K.m[c];
+  double v[8];
 #pragma unroll
-  for (int i = 0; i <= kRPT; ++i) o[i] = i <= nr ? __ldg(off + r0 + i) : 0;
+  for (int j = 0; j < 8; ++j) v[j] = j < m ? __ldg(Sc + j * nc) : 0.0;
+  double acc = 0.0;
 #pragma unroll
-  for (int i = 0; i < kRPT; ++i) d[i] = i < nr ? __ldg(row_dof + r0 + i) : 0;
-  double v[kRPT][kMaxMult];
-#pragma unroll
-  for (int i = 0; i < kRPT; ++i)
-#pragma unroll
-    for (int u = 0; u < kMaxMult; ++u)
-      v[i][u] = (i < nr && o[i] + u < o[i + 1]) ? __ldg(Sc + o[i] + u) : 0.0;
-#pragma unroll
-  for (int i = 0; i < kRPT; ++i) {
-    if (i >= nr) continue;
-    double acc = 0.0;
-#pragma unroll
-    for (int u = 0; u < kMaxMult; ++u)
-      if (o[i] + u < o[i + 1]) acc += v[i][u];
-    for (int k = o[i] + kMaxMult; k < o[i + 1]; ++k) acc += __ldg(Sc + k);  // non-conforming
-    yc[d[i]] = acc;
-  }
+  for (int j = 0; j < 8; ++j)
+    if (j < m) acc += v[j];
+  for (int j = 8; j < m; ++j) acc += __ldg(Sc + j * nc);
+  y[comp * y_comp_stride + __ldg(row_dof + r)] = acc;
 }
 
 __global__ void gather_kernel(int64_t total, const int* __restrict__ map,
@@ -104,6 +97,12 @@ struct fb_restriction {
   int nb = 0;  // element-boundary positions per element
   int64_t nsrows = 0;
   DevBuf<int> s_row, s_off, s_ent;
+  // class-major slot layout: shared rows grouped by multiplicity m; class c
+  // holds rows [cls_row[c], cls_row[c+1]) and their slots at
+  // cls_slot[c] + j * (rows in class) + k  (j = contribution rank in flat-E order)
+  int ncls = 0;
+  int cls_m[16] = {0};
+  int64_t cls_row[17] = {0}, cls_slot[16] = {0};
   int nlocp = 0;           // per-element stride of map_pad (multiple of 4)
   DevBuf<int> map_pad;     // (ne, nlocp) for 16-byte bulk copies
   int nbp = 0;             // per-element stride of s_pos (multiple of 4)
@@ -240,9 +239,16 @@ int scatter_rows(const fb_restriction* r, bool split, const double* S, int64_t S
   const int64_t nrows = split ? r->nsrows : r->ndofs;
   if (nrows == 0) return FB_OK;
   if (split) {
-    dim3 grid(ceil_div(ceil_div(nrows, kRPT), 256), ncomp);
-    scatter_slots_kernel<<<grid, 256, 0, st>>>(nrows, r->s_row.ptr, r->s_off.ptr, S,
-                                               S_comp_stride, y, y_comp_stride);
+    SlotClasses K;
+    K.n = r->ncls;
+    for (int c = 0; c < r->ncls; ++c) {
+      K.m[c] = r->cls_m[c];
+      K.slot[c] = r->cls_slot[c];
+    }
+    for (int c = 0; c <= r->ncls; ++c) K.row[c] = r->cls_row[c];
+    dim3 grid(ceil_div(nrows, 256), ncomp);
+    scatter_slots_kernel<<<grid, 256, 0, st>>>(K, r->s_row.ptr, S, S_comp_stride, y,
+                                               y_comp_stride);
   } else {
     dim3 grid(ceil_div(nrows, 256), ncomp);
     scatter_rows_kernel<<<grid, 256, 0, st>>>(nrows, nullptr, r->full_off.ptr, r->full_ent.ptr,
@@ -438,33 +444,61 @@ int fb_restriction_create(int dim, int p, int64_t ne, int64_t ndofs,
   FB_TRY_CUDA(r->full_off.upload(off.data(), ndofs + 1));
   FB_TRY_CUDA(r->full_ent.upload(ent.data(), total));
   if (ok) {
-    std::vector<int> rowid(ndofs, -1);
-    std::vector<int> rows;
-    rows.reserve(ndofs);
+    // shared rows (element-boundary DoFs) grouped by multiplicity, ascending
+    // DoF order inside a class
+    int mult_max = 0;
     for (int64_t i = 0; i < ndofs; ++i)
-      if (!direct[i]) {
-        rowid[i] = int(rows.size());
-        rows.push_back(int(i));
+      if (!direct[i]) mult_max = std::max(mult_max, count[i]);
+    std::vector<int> cls_of_m(mult_max + 1, -1);
+    int ncls = 0;
+    for (int64_t i = 0; i < ndofs; ++i)
+      if (!direct[i] && cls_of_m[count[i]] < 0) cls_of_m[count[i]] = 1;
+    for (int m = 1; m <= mult_max; ++m)
+      if (cls_of_m[m] > 0) cls_of_m[m] = ncls++;
+    ok = ncls <= 16;
+    if (ok) {
+      r->ncls = ncls;
+      std::vector<int64_t> ccount(ncls, 0);
+      for (int m = 1; m <= mult_max; ++m)
+        if (cls_of_m[m] >= 0) r->cls_m[cls_of_m[m]] = m;
+      for (int64_t i = 0; i < ndofs; ++i)
+        if (!direct[i]) ccount[cls_of_m[count[i]]]++;
+      r->cls_row[0] = 0;
+      int64_t slot = 0;
+      for (int c = 0; c < ncls; ++c) {
+        r->cls_row[c + 1] = r->cls_row[c] + ccount[c];
+        r->cls_slot[c] = slot;
+        slot += ccount[c] * r->cls_m[c];
       }
-    const int64_t nr = int64_t(rows.size());
-    std::vector<int> soff(nr + 1, 0);
-    for (int64_t i = 0; i < nr; ++i) soff[i + 1] = soff[i] + count[rows[i]];
-    // slot of every (element, boundary position) contribution in row order;
-    // within a row, slots ascend with the flat E index (np.bincount order)
-    r->nbp = (nb + 3) / 4 * 4;
-    std::vector<int> spos(size_t(ne) * r->nbp, 0);
-    std::vector<int> pos(soff.begin(), soff.end() - 1);
-    for (int64_t e = 0; e < ne; ++e)
-      for (int l = 0; l < nloc; ++l) {
-        if (interior[l]) continue;
-        const int d = map[e * nloc + l];
-        spos[e * r->nbp + rank[l]] = pos[rowid[d]]++;
-      }
-    r->nsrows = nr;
-    FB_TRY_CUDA(r->s_row.upload(rows.data(), nr));
-    FB_TRY_CUDA(r->s_off.upload(soff.data(), nr + 1));
-    FB_TRY_CUDA(r->s_pos.upload(spos.data(), int64_t(spos.size())));
-    r->s_ent.reset();
+      std::vector<int> rows(r->cls_row[ncls]);
+      std::vector<int64_t> rowpos(ndofs, -1);  // class-ordered row index
+      std::vector<int64_t> fill(r->cls_row, r->cls_row + ncls);
+      for (int64_t i = 0; i < ndofs; ++i)
+        if (!direct[i]) {
+          const int c = cls_of_m[count[i]];
+          rowpos[i] = fill[c];
+          rows[fill[c]++] = int(i);
+        }
+      // slot of every (element, boundary position) contribution; j-th
+      // contribution of a row in ascending flat-E order (np.bincount order)
+      r->nbp = (nb + 3) / 4 * 4;
+      std::vector<int> spos(size_t(ne) * r->nbp, 0);
+      std::vector<int> seen(ndofs, 0);
+      for (int64_t e = 0; e < ne; ++e)
+        for (int l = 0; l < nloc; ++l) {
+          if (interior[l]) continue;
+          const int d = map[e * nloc + l];
+          const int c = cls_of_m[count[d]];
+          const int64_t k = rowpos[d] - r->cls_row[c];
+          const int64_t nc = r->cls_row[c + 1] - r->cls_row[c];
+          spos[e * r->nbp + rank[l]] = int(r->cls_slot[c] + int64_t(seen[d]++) * nc + k);
+        }
+      r->nsrows = int64_t(rows.size());
+      FB_TRY_CUDA(r->s_row.upload(rows.data(), r->nsrows));
+      FB_TRY_CUDA(r->s_pos.upload(spos.data(), int64_t(spos.size())));
+      r->s_ent.reset();
+    }
+    r->split_ok = ok ? 1 : 0;
   }
   *out = r.release();
   return FB_OK;
