@@ -21,7 +21,7 @@ struct GeomParams {
   int64_t ne;
   int dim, nq, kind, nfac;
   int64_t fstride;
-  int lanes;  // 0: element-blocked; 32: [ne/32][K][nq][32] interleaved
+  int lanes;  // 0: element-blocked; 32: [ne/32][nq][K][32] interleaved, point-major
   double c, nu;
   double pts[32];
   double w1[32];
@@ -83,9 +83,9 @@ __global__ void factor_kernel(const __grid_constant__ GeomParams P) {
   double w = 1.0;
   for (int a = d - 1; a >= 0; --a) w = __dmul_rn(w, P.w1[qi[a]]);
   const double wdet = __dmul_rn(detj, w);
-  const int64_t kstride = P.lanes ? int64_t(nqd) * P.lanes : nqd;
-  double* out = P.lanes ? P.fac + (e / P.lanes) * P.nfac * kstride + int64_t(q) * P.lanes +
-                              (e % P.lanes)
+  const int64_t kstride = P.lanes ? P.lanes : nqd;
+  double* out = P.lanes ? P.fac + (e / P.lanes) * P.nfac * int64_t(nqd) * P.lanes +
+                              int64_t(q) * P.nfac * P.lanes + (e % P.lanes)
                         : P.fac + e * P.fstride + q;
   int k = 0;
   if (P.kind == FB_MASS || P.kind == FB_HELMHOLTZ) {

@@ -259,7 +259,7 @@ int scatter_rows(const fb_restriction* r, bool split, const double* S, int64_t S
 }
 
 // AoS (ne, nq, k) -> element-blocked (ne, [k, nq] padded to fstride), or for
-// lanes = 32 the interleaved layout [ne/32][ktot][nq][32].
+// lanes = 32 the interleaved, point-major layout [ne/32][nq][ktot][32].
 void relayout(const double* src, int64_t ne, int nqd, int k, double* dst, int64_t fstride,
               int koff, int lanes = 0, int ktot = 0) {
   for (int64_t e = 0; e < ne; ++e)
@@ -267,8 +267,8 @@ void relayout(const double* src, int64_t ne, int nqd, int k, double* dst, int64_
       for (int q = 0; q < nqd; ++q) {
         const double v = src[(e * nqd + q) * k + c];
         if (lanes)
-          dst[((e / lanes) * ktot + koff + c) * int64_t(nqd) * lanes + int64_t(q) * lanes +
-              (e % lanes)] = v;
+          dst[((e / lanes) * int64_t(nqd) + q) * int64_t(ktot) * lanes +
+              int64_t(koff + c) * lanes + (e % lanes)] = v;
         else
           dst[e * fstride + int64_t(koff + c) * nqd + q] = v;
       }

@@ -6,10 +6,13 @@
 // and drowns in index arithmetic here, so this kernel keeps the whole element
 // on chip: U at the 27 points and the transposed accumulator V live in
 // thread-private shared-memory columns ([q][thread], conflict free), the
-// gradients and factors of one 3-point row live in registers.  Factors use an element-interleaved
-// layout (groups of 32 elements, [group][K][27][32]) so every factor load of a
-// warp is one fully used 256-byte segment; map and slot rows are read as
-// 16-byte vectors.  All 8 outputs of an element lie on the element boundary,
+// gradients and factors of one 3-point row live in registers.  Factors use an
+// element-interleaved, point-major layout (groups of 32 elements,
+// [group][27][K][32]) so every factor load of a warp is one fully used
+// 256-byte segment and one 3-point row of a warp is one contiguous
+// 3*K*256-byte run, streamed into L2 two rows ahead of its use (a whole-block
+// prefetch would keep ~110 MB in flight and get evicted before use); map and
+// slot rows are read as 16-byte vectors.  All 8 outputs of an element lie on the element boundary,
 // so they go to their transposed-map slots (scatter_rows sums them in
 // np.bincount order).  Same arithmetic as the general path: U = B(x)B(x)B x,
 // G_m = Dq_m U, pointwise factors, V = f_u + sum Dq_m^T f_m, y = B^T(x)B^T(x)B^T V
@@ -49,10 +52,12 @@ __global__ void __launch_bounds__(kQ1Threads, 4) sf3_q1_kernel(const __grid_cons
   const int64_t e = int64_t(blockIdx.x) * T + tid;
   if (e >= P.ne) return;  // no block-level barriers below
   const int lane = int(e & 31);
-  const double* __restrict__ f = P.fac + (e >> 5) * (int64_t(NK) * 27 * 32) + lane;
-  // one lane per warp streams the warp's interleaved factor block into L2
-  // (bulk prefetch) while the warp gathers x and runs the forward passes
-  if (lane == 0) bulk_prefetch_l2(f, int64_t(NK) * 27 * 32 * 8);
+  const double* __restrict__ fblk = P.fac + (e >> 5) * (int64_t(NK) * 27 * 32);
+  const double* __restrict__ f = fblk + lane;
+  constexpr int64_t kRowBytes = int64_t(3) * NK * 32 * 8;  // one 3-point row of the warp
+  // lane 0 streams rows 0 and 1 of the warp's factor block into L2 now, and
+  // row cb+2 while row cb is computed
+  if (lane == 0) bulk_prefetch_l2(fblk, 2 * kRowBytes);
   double* U = su + tid;
   double* V = sv + tid;
   int m[8], sl[8];
@@ -101,18 +106,20 @@ __global__ void __launch_bounds__(kQ1Threads, 4) sf3_q1_kernel(const __grid_cons
 #pragma unroll 1
     for (int cb = 0; cb < 9; ++cb) {
       const int c = cb / 3, b = cb - 3 * c;
+      if (lane == 0 && comp == 0 && cb + 2 < 9)
+        bulk_prefetch_l2(fblk + (cb + 2) * 3 * NK * 32, kRowBytes);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const int q = cb * 3 + a;
-        const double* fq = f + q * 32;
+        const double* fq = f + q * NK * 32;
         if (KIND == kMass) {
           V[q * T] = __ldg(fq) * U[q * T];
           continue;
         }
         constexpr int o = (KIND == kHelm) ? 1 : 0;
-        const double w00 = __ldg(fq + (o + 0) * 27 * 32), w01 = __ldg(fq + (o + 1) * 27 * 32);
-        const double w02 = __ldg(fq + (o + 2) * 27 * 32), w11 = __ldg(fq + (o + 3) * 27 * 32);
-        const double w12 = __ldg(fq + (o + 4) * 27 * 32), w22 = __ldg(fq + (o + 5) * 27 * 32);
+        const double w00 = __ldg(fq + (o + 0) * 32), w01 = __ldg(fq + (o + 1) * 32);
+        const double w02 = __ldg(fq + (o + 2) * 32), w11 = __ldg(fq + (o + 3) * 32);
+        const double w12 = __ldg(fq + (o + 4) * 32), w22 = __ldg(fq + (o + 5) * 32);
         const double wm = (KIND == kHelm) ? __ldg(fq) : 0.0;
         double g0 = 0.0, g1 = 0.0, g2 = 0.0;
 #pragma unroll
