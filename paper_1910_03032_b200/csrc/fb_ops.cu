@@ -158,7 +158,7 @@ void diff_matrix(const double* x, int n, double* D) {
   }
 }
 
-template <int N, int Q, int KIND, int NE, int NT, int MINB, bool ZL>
+template <int N, int Q, int KIND, int NE, int NT, int MINB, int ZL>
 int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   constexpr size_t smem = SF3Shape<N, Q, KIND, NE, ZL>::SMEM;
   // persistent grid: as many CTAs as can be resident at once
@@ -183,7 +183,7 @@ int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_
   return FB_OK;
 }
 
-template <int N, int Q, int NE, int NT, int MINB, bool ZL = false>
+template <int N, int Q, int NE, int NT, int MINB, int ZL = 0>
 int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   switch (op->kind) {
     case FB_MASS: return launch_fast_t<N, Q, kMass, NE, NT, MINB, ZL>(op, x, y, st);
@@ -196,7 +196,10 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // per CTA: double-buffered map/slot stage, gather buffer, 4 work buffers per
 // element (34-52 KB); the grid is persistent (all CTAs resident).
 // Runtime-selectable launch shapes (tuning): g_fast_cfg[p] picks a variant.
-static int g_fast_cfg[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+// Defaults measured with tools/tune_fast.py: p = 5, 6 stage their factor
+// blocks in shared memory through the TMA engine (variant 5 / 4: +14 % / +2 %);
+// at p = 7, 8 the extra 41-56 KB per CTA costs more occupancy than it saves.
+static int g_fast_cfg[9] = {0, 0, 0, 0, 0, 5, 4, 0, 0};
 
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   const int v = g_fast_cfg[op->rv->p < 9 ? op->rv->p : 0];
@@ -213,22 +216,37 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
     case 4:
       if (v == 1) return launch_fast_kind<5, 6, 4, 160, 5>(op, x, y, st);
       if (v == 2) return launch_fast_kind<5, 6, 1, 64, 12>(op, x, y, st);
+      if (v == 3) return launch_fast_kind<5, 6, 2, 96, 6, 2>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<5, 6, 1, 64, 12, 2>(op, x, y, st);
+      if (v == 5) return launch_fast_kind<5, 6, 1, 96, 8, 2>(op, x, y, st);
       return launch_fast_kind<5, 6, 2, 96, 8>(op, x, y, st);
     case 5:
       if (v == 1) return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
       if (v == 2) return launch_fast_kind<6, 7, 2, 128, 6>(op, x, y, st);
+      if (v == 3) return launch_fast_kind<6, 7, 1, 64, 8, 2>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<6, 7, 1, 96, 6, 2>(op, x, y, st);
+      if (v == 5) return launch_fast_kind<6, 7, 2, 128, 3, 2>(op, x, y, st);
       return launch_fast_kind<6, 7, 1, 64, 10>(op, x, y, st);
     case 6:
       if (v == 1) return launch_fast_kind<7, 8, 2, 128, 6>(op, x, y, st);
       if (v == 2) return launch_fast_kind<7, 8, 2, 192, 4>(op, x, y, st);
+      if (v == 3) return launch_fast_kind<7, 8, 1, 96, 5, 2>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<7, 8, 1, 128, 4, 2>(op, x, y, st);
+      if (v == 5) return launch_fast_kind<7, 8, 1, 64, 6, 2>(op, x, y, st);
       return launch_fast_kind<7, 8, 1, 96, 8>(op, x, y, st);
     case 7:
       if (v == 1) return launch_fast_kind<8, 9, 2, 192, 3>(op, x, y, st);
       if (v == 2) return launch_fast_kind<8, 9, 1, 96, 6>(op, x, y, st);
+      if (v == 3) return launch_fast_kind<8, 9, 1, 128, 3, 2>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<8, 9, 1, 192, 2, 2>(op, x, y, st);
+      if (v == 5) return launch_fast_kind<8, 9, 1, 96, 3, 2>(op, x, y, st);
       return launch_fast_kind<8, 9, 1, 128, 4>(op, x, y, st);
     case 8:
       if (v == 1) return launch_fast_kind<9, 10, 1, 96, 5>(op, x, y, st);
       if (v == 2) return launch_fast_kind<9, 10, 2, 224, 2>(op, x, y, st);
+      if (v == 3) return launch_fast_kind<9, 10, 1, 128, 2, 2>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<9, 10, 1, 192, 2, 2>(op, x, y, st);
+      if (v == 5) return launch_fast_kind<9, 10, 1, 256, 1, 2>(op, x, y, st);
       return launch_fast_kind<9, 10, 1, 128, 4>(op, x, y, st);
     default: set_error("fast path not built for this degree"); return FB_ERR_UNSUPPORTED;
   }
@@ -651,7 +669,7 @@ int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count) 
 int64_t fb_operator_factor_count(const fb_operator* op) { return op ? op->fac.n : 0; }
 
 int fb_set_fast_config(int p, int variant) {
-  FB_REQUIRE(p >= 1 && p <= 8 && variant >= 0 && variant <= 2, "bad fast-path config");
+  FB_REQUIRE(p >= 1 && p <= 8 && variant >= 0 && variant <= 5, "bad fast-path config");
   g_fast_cfg[p] = variant;
   return FB_OK;
 }

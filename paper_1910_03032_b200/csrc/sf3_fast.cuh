@@ -97,7 +97,12 @@ struct SF3Pitch {
 };
 
 // Compile-time geometry of one instantiation.
-template <int N, int Q, int KIND, int NE, bool ZL = false>
+// ZL: 0 = four work buffers, factors read from L2 in P5 (bulk L2 prefetch one
+// batch ahead); 1 = z-line schedule (three buffers, G_z in registers);
+// 2 = as 0, but the batch's factor block is copied into shared memory by the
+// TMA engine (cp.async.bulk, issued right after the previous batch's P5), so
+// P5 reads factors from shared memory instead of waiting on L2.
+template <int N, int Q, int KIND, int NE, int ZL = 0>
 struct SF3Shape {
   static constexpr int QP = SF3Pitch<Q>::QP;  // x-row pitch
   static constexpr int YP = SF3Pitch<Q>::YP;  // z-plane pitch
@@ -111,7 +116,8 @@ struct SF3Shape {
   static constexpr int NB = (N <= 2) ? NLOC : NLOC - (N - 2) * (N - 2) * (N - 2);
   static constexpr int NBP = round_up(NB, 4);
   // work buffers per element: the z-line schedule (ZL) keeps G_z in registers
-  static constexpr int NBUF = (KIND == kMass) ? 2 : (ZL ? 3 : 4);
+  static constexpr int NBUF = (KIND == kMass) ? 2 : (ZL == 1 ? 3 : 4);
+  static constexpr bool FSTAGE = (ZL == 2) && (KIND != kMass);
   static constexpr int XBUF = N * N * (N | 1);          // gathered x_e (odd pitch)
   // shared-memory plan (bytes):
   //   [3 mbarriers | 3 x (map | slots) | gather buffer | work buffers]
@@ -121,7 +127,8 @@ struct SF3Shape {
   static constexpr int OFF_X = OFF_STAGE + NSTAGE * STAGE;
   static constexpr int OFF_WORK = round_up(OFF_X + NE * XBUF * 8, 16);
   static constexpr int ES = NBUF * BUF + SF3Pitch<Q>::PAD;  // element stride (doubles)
-  static constexpr int SMEM = OFF_WORK + NE * ES * 8;
+  static constexpr int OFF_FAC = round_up(OFF_WORK + NE * ES * 8, 16);
+  static constexpr int SMEM = OFF_FAC + (FSTAGE ? NE * FACP * 8 : 0);
 };
 
 // rank of lattice position (k,j,i) among the element-boundary positions of
@@ -193,7 +200,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-template <int N, int Q, int KIND, int NE, int NT, int MINB, bool ZL>
+template <int N, int Q, int KIND, int NE, int NT, int MINB, int ZL>
 __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constant__ SF3Params P) {
   using Sh = SF3Shape<N, Q, KIND, NE, ZL>;
   constexpr int QP = Sh::QP, BUF = Sh::BUF, NLOC = Sh::NLOC, NLOCP = Sh::NLOCP;
@@ -205,6 +212,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* sx = reinterpret_cast<double*>(smem_raw + Sh::OFF_X);
   double* smem = reinterpret_cast<double*>(smem_raw + Sh::OFF_WORK);
+  double* fsm = reinterpret_cast<double*>(smem_raw + Sh::OFF_FAC);  // staged factors (ZL == 2)
   auto stage_map = [&](int s) {
     return reinterpret_cast<const int*>(smem_raw + Sh::OFF_STAGE + s * Sh::STAGE);
   };
@@ -237,7 +245,14 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
   };
   auto prefetch_factors = [&](int batch) {
     const int64_t e0 = int64_t(batch) * NE;
-    bulk_prefetch_l2(P.fac + e0 * FACP, int64_t(nel_of(batch)) * FACP * 8);
+    if constexpr (Sh::FSTAGE) {  // TMA copy of the whole factor block into shared memory
+      const uint32_t bar = smem_u32(&bars[Sh::NSTAGE]);
+      const uint32_t bytes = uint32_t(nel_of(batch)) * FACP * 8u;
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(smem_u32(fsm), P.fac + e0 * FACP, bytes, bar);
+    } else {
+      bulk_prefetch_l2(P.fac + e0 * FACP, int64_t(nel_of(batch)) * FACP * 8);
+    }
   };
   // all threads: cp.async gathers of component `comp` of `batch` into sx
   auto issue_gather = [&](int batch, int comp, int s) {
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
   };
 
   if (tid == 0) {
-    for (int h = 0; h < Sh::NSTAGE; ++h) mbar_init(smem_u32(&bars[h]), 1);
+    for (int h = 0; h < Sh::NSTAGE + (Sh::FSTAGE ? 1 : 0); ++h) mbar_init(smem_u32(&bars[h]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -285,7 +300,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
     // slot (it+2)%3 was last read by batch it-1, finished at its final barrier
     if (tid == 0) {
       if (next + G < nbatch) issue_stage(next + G, (it + 2) % Sh::NSTAGE);
-      if (next < nbatch) prefetch_factors(next);
+      if (!Sh::FSTAGE && next < nbatch) prefetch_factors(next);
     }
 
 #pragma unroll 1
@@ -343,7 +358,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       }
       __syncthreads();
 
-      if constexpr (!ZL) {
+      if constexpr (ZL != 1) {
       // ---- P3: z-lines (b,a): b0 -> U (b0 in place), Gz = Dq_z U (b3) -------
 #pragma unroll 1
       for (int L = tid; L < NE * Q2; L += NT) {
@@ -423,19 +438,24 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         //   (points (c, b, a), c = 0..Q-1: constant strides, coalesced L2 reads)
         //   b0: U -> f_u,  b1: G0 -> f0,  b2: G1 -> f1,  b3: G2 -> f2
         constexpr int o = (KIND == kHelm) ? 1 : 0;
+        if constexpr (Sh::FSTAGE) {
+          if (comp == 0) mbar_wait(smem_u32(&bars[Sh::NSTAGE]), uint32_t(it & 1));
+        }
+        auto ldf = [&](const double* p_) { return Sh::FSTAGE ? *p_ : __ldg(p_); };
 #pragma unroll 1
         for (int L = tid; L < nel * Q2; L += NT) {
           const int el = L / Q2, ba = L - el * Q2;
           double* col = smem + el * ES + IX(0, ba / Q, ba % Q);
-          const double* __restrict__ f = P.fac + (e0 + el) * FACP + ba;
+          const double* __restrict__ f =
+              Sh::FSTAGE ? fsm + el * FACP + ba : P.fac + (e0 + el) * FACP + ba;
 #pragma unroll 2
           for (int c = 0; c < Q; ++c) {
             const double* fc = f + c * Q2;
             double* pt = col + c * YP;
-            const double w00 = __ldg(fc + (o + 0) * Q3), w01 = __ldg(fc + (o + 1) * Q3);
-            const double w02 = __ldg(fc + (o + 2) * Q3), w11 = __ldg(fc + (o + 3) * Q3);
-            const double w12 = __ldg(fc + (o + 4) * Q3), w22 = __ldg(fc + (o + 5) * Q3);
-            const double wm = (KIND == kHelm) ? __ldg(fc) : 0.0;
+            const double w00 = ldf(fc + (o + 0) * Q3), w01 = ldf(fc + (o + 1) * Q3);
+            const double w02 = ldf(fc + (o + 2) * Q3), w11 = ldf(fc + (o + 3) * Q3);
+            const double w12 = ldf(fc + (o + 4) * Q3), w22 = ldf(fc + (o + 5) * Q3);
+            const double wm = (KIND == kHelm) ? ldf(fc) : 0.0;
             const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = pt[3 * BUF];
             pt[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
             pt[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
@@ -444,6 +464,9 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           }
         }
         __syncthreads();
+        if constexpr (Sh::FSTAGE) {  // factor buffer free: stage the next batch's block
+          if (tid == 0 && comp == vdim - 1 && next < nbatch) prefetch_factors(next);
+        }
 
         // ---- P6: transposed derivative lines, in place: x b1, y b2, z b3 ---
 #pragma unroll 1

@@ -1,0 +1,20 @@
+"""Check that every fused-kernel launch variant gives bitwise-identical output."""
+import sys
+sys.path.insert(0, ".")
+import torch
+import bench
+from paper_1910_03032_b200 import _lib
+for p in range(2, 9):
+    pr = bench.build_problem(p, target=2e6)
+    x = torch.randn(pr["N"], dtype=torch.float64, device="cuda")
+    ref = None
+    for v in range(6):
+        if _lib.lib.fb_set_fast_config(p, v) != 0:
+            continue
+        y = torch.empty_like(x)
+        pr["op"].apply_into(x, y)
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = y.clone()
+        print(p, v, "max|diff|", float((y - ref).abs().max()), flush=True)
+    _lib.lib.fb_set_fast_config(p, 0)
