@@ -51,6 +51,18 @@ def algorithmic_flops(ne, p):
     return ne * (2.0 * (4 * n ** 3 * q + 6 * n ** 2 * q ** 2 + 8 * n * q ** 3) + 17.0 * q ** 3)
 
 
+def _traffic():
+    """Measured DRAM bytes (read + write) of one sweep step -- every fused
+    kernel and E->L sum launch -- from the committed ncu launch list
+    (profiles/r1_traffic.json); None if the profile is absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+    try:
+        with open(path) as f:
+            return int(json.load(f)["sweep_dram_bytes"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -521,7 +533,8 @@ def run_ours(args, rank, world):
         "per_p": per_p,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": None, "peak_source": peak_kind,
+                     "traffic": _traffic(), "algorithmic_bytes_per_step": int(tot_bytes),
+                     "peak_source": peak_kind,
                      "note": "full apply (fused element kernel + E->L sum of shared DoFs), "
                              "algorithmic bytes 16N + 4 ne (p+1)^3 + 56 ne (p+2)^3 over the "
                              "p=1..8 sweep"},
