@@ -268,6 +268,131 @@ def cg(A, b, precond=None, config=None, x0=None, project=None, inner=None):
     return done(converged, it, relres)
 
 
+def minres(A, b, precond=None, config=None, x0=None, shift=0.0):
+    """Preconditioned MINRES for symmetric (indefinite) A with an SPD
+    preconditioner -- the Krylov method the north star names for the
+    block-diagonal-preconditioned Stokes problem.  The
+    reference has no MINRES; this restates the Paige-Saunders recurrence and
+    stopping tests of scipy.sparse.linalg.minres (the oracle of
+    tests/test_gpu_minres.py) with device vectors and libfbb200 kernels: per
+    iteration one A apply, one preconditioner apply, three inner products
+    (the only host round trips) and six axpy-type updates.
+    Returns (x, SolveReport); converged means scipy's istop in {1, 2}."""
+    apply_A = _device_apply(A)
+    M = _device_apply(precond) if precond is not None else None
+    cfg = config or SolverConfig()
+    rtol, maxiter = cfg.rel_tol, cfg.max_iters
+    eps = float(np.finfo(np.float64).eps)
+    t0 = time.perf_counter()
+    bd, host = dev.DeviceIn.get(b)
+    n = bd.shape[0]
+    sc = dev.empty(1)
+
+    def dot(u, v):
+        vec.dot_into(u, v, sc)
+        return float(sc.item())
+
+    x = dev.zeros(n) if x0 is None else dev.to_device(x0).clone()
+    R1 = dev.empty(n)
+    if x0 is None:
+        vec.copy(bd, R1)
+    else:
+        apply_A(x, R1)
+        vec.axpby(1.0, bd, -1.0, R1)
+    Y = dev.empty(n)
+    if M is not None:
+        M(R1, Y)
+    else:
+        vec.copy(R1, Y)
+    beta1 = dot(R1, Y)
+
+    def done(conv, its, rel, hist):
+        return (dev.to_host(x) if host else x), SolveReport(conv, its, rel,
+                                                           time.perf_counter() - t0, cfg.label,
+                                                           hist)
+
+    if beta1 < 0:
+        raise ValueError("indefinite preconditioner")
+    if beta1 == 0 or dot(bd, bd) == 0:
+        return done(True, 0, 0.0, [0.0])
+    beta1 = math.sqrt(beta1)
+    R2 = R1.clone()
+    T, V = dev.empty(n), dev.empty(n)
+    W, W1, W2 = dev.zeros(n), dev.zeros(n), dev.zeros(n)
+    oldb, beta, dbar, epsln, phibar = 0.0, beta1, 0.0, 0.0, beta1
+    rhs1, rhs2, tnorm2, gmax, gmin = beta1, 0.0, 0.0, 0.0, float(np.finfo(np.float64).max)
+    cs, sn = -1.0, 0.0
+    istop, itn, rnorm = 0, 0, beta1
+    history = [1.0]
+    while itn < maxiter:
+        itn += 1
+        vec.scale(1.0 / beta, Y, V)            # v = y / beta
+        apply_A(V, T)                           # y = A v - shift v
+        if shift:
+            vec.axpby(-shift, V, 1.0, T)
+        if itn >= 2:
+            vec.axpby(-beta / oldb, R1, 1.0, T)
+        alfa = dot(V, T)
+        vec.axpby(-alfa / beta, R2, 1.0, T)
+        R1, R2, T = R2, T, R1                   # r1 <- r2, r2 <- y
+        if M is not None:                       # y = M r2
+            M(R2, Y)
+        else:
+            vec.copy(R2, Y)
+        oldb = beta
+        beta = dot(R2, Y)
+        if beta < 0:
+            raise ValueError("non-symmetric matrix")
+        beta = math.sqrt(beta)
+        tnorm2 += alfa ** 2 + oldb ** 2 + beta ** 2
+        if itn == 1 and beta / beta1 <= 10 * eps:
+            istop = -1
+        oldeps = epsln
+        delta = cs * dbar + sn * alfa
+        gbar = sn * dbar - cs * alfa
+        epsln = sn * beta
+        dbar = -cs * beta
+        root = math.hypot(gbar, dbar)
+        gamma = max(math.hypot(gbar, beta), eps)
+        cs, sn = gbar / gamma, beta / gamma
+        phi = cs * phibar
+        phibar = sn * phibar
+        denom = 1.0 / gamma
+        W1, W2, W = W2, W, W1                   # w1 <- w2, w2 <- w
+        vec.scale(denom, V, W)                  # w = (v - oldeps w1 - delta w2) / gamma
+        vec.axpby(-oldeps * denom, W1, 1.0, W)
+        vec.axpby(-delta * denom, W2, 1.0, W)
+        vec.axpby(phi, W, 1.0, x)
+        gmax, gmin = max(gmax, gamma), min(gmin, gamma)
+        z = rhs1 / gamma
+        rhs1, rhs2 = rhs2 - delta * z, -epsln * z
+        Anorm = math.sqrt(tnorm2)
+        ynorm = math.sqrt(dot(x, x))
+        epsx = Anorm * ynorm * eps
+        rnorm = phibar
+        test1 = math.inf if (ynorm == 0 or Anorm == 0) else rnorm / (Anorm * ynorm)
+        test2 = math.inf if Anorm == 0 else root / Anorm
+        history.append(rnorm / beta1)
+        if istop == 0:
+            if 1 + test2 <= 1:
+                istop = 2
+            if 1 + test1 <= 1:
+                istop = 1
+            if itn >= maxiter:
+                istop = 6
+            if gmax / gmin >= 0.1 / eps:
+                istop = 4
+            if epsx >= beta1:
+                istop = 3
+            if test2 <= rtol:
+                istop = 2
+            if test1 <= rtol:
+                istop = 1
+        if istop != 0:
+            break
+    return done(istop in (1, 2), itn, rnorm / beta1, history)
+
+
 def fgmres(A, b, precond=None, config=None, x0=None, project=None):
     """Right-preconditioned flexible GMRES(m) with MGS (solvers.py:172-254)."""
     apply_A = _device_apply(A)

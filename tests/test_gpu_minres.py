@@ -1,0 +1,51 @@
+"""GPU: device MINRES (solvers.minres) against scipy.sparse.linalg.minres --
+its oracle -- on symmetric indefinite problems with SPD
+preconditioners, on the same device operators."""
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+from tests.cases import build, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(c, p=3, counts=(4, 3, 3)):
+    from paper_1910_03032_b200 import mfop, solvers
+    m, sp_, geom = build(3, counts, None, 0.05, p)
+    op = mfop.HelmholtzOperator(sp_, geom, c=c)
+    bdr = sp_.boundary_dof_set()
+    A = mfop.ConstrainedOperator(op, bdr)
+    diag = solvers.collocated_mass_diagonal(sp_, bdr)
+    b = np.random.default_rng(3).standard_normal(sp_.ndofs)
+    b[bdr] = 0.0
+    return sp_, A, diag, b
+
+
+@pytest.mark.parametrize("c", [-60.0, -250.0, 10.0])
+@pytest.mark.parametrize("precond", ["diag", "none"])
+def test_minres_matches_scipy(c, precond):
+    from paper_1910_03032_b200 import solvers
+    sp_, A, diag, b = _problem(c)
+    n = sp_.ndofs
+    Aop = spla.LinearOperator((n, n), matvec=lambda v: A.apply(np.ascontiguousarray(v)))
+    M = solvers.DiagonalPreconditioner(diag) if precond == "diag" else None
+    Mop = spla.LinearOperator((n, n), matvec=lambda v: v / diag) if precond == "diag" else None
+    its = [0]
+
+    def cb(_):
+        its[0] += 1
+
+    x_ref, info = spla.minres(Aop, b, M=Mop, rtol=1e-8, maxiter=500, callback=cb)
+    assert info == 0
+    x, rep = solvers.minres(A, b, precond=M,
+                            config=solvers.SolverConfig(rel_tol=1e-8, max_iters=500))
+    assert rep.converged
+    assert abs(rep.iterations - its[0]) <= 1, (rep.iterations, its[0])
+    # MINRES stops on ||r|| / (||A|| ||x||) <= rtol: solutions agree to the
+    # level of that test, and the true residuals are of the same size
+    assert rel_err(x, x_ref) < 1e-5
+    res = np.linalg.norm(b - A.apply(x))
+    res_ref = np.linalg.norm(b - A.apply(x_ref))
+    assert res <= 2.0 * res_ref + 1e-12 * np.linalg.norm(b), (res, res_ref)

@@ -55,3 +55,21 @@ def test_block_operator_rejects_bad_shape():
         S.K.apply(np.zeros(S.K.shape[0] + 1))
     with pytest.raises(ValueError):
         stokes.StokesSystem(vs, spaces.FESpace(m, 2), geom)
+
+
+@pytest.mark.parametrize("name", ["cav2d_p2", "cav2d_p4", "cav3d_p2"])
+def test_minres_lid_cavity_matches_reference_solution(name, gold):
+    """Block-diagonal-preconditioned MINRES on the symmetric saddle form
+    (north star's Stokes solver; no reference counterpart) reaches the
+    reference's FGMRES solution of the same cavity."""
+    from paper_1910_03032_b200 import geometry, solvers, spaces, stokes
+    c = CASES[name]
+    m = geometry.cartesian_mesh(tuple(c["counts"]))
+    vs = spaces.FESpace(m, c["p"], vdim=c["d"])
+    ps = spaces.FESpace(m, c["p"] - 1)
+    geom = geometry.compute_geometric_factors(m, vs.basis.quad)
+    S = stokes.StokesSystem(vs, ps, geom, nu=1.0)
+    u, p, rep = S.solve_minres(g=lid, config=solvers.SolverConfig(rel_tol=1e-12, max_iters=2000))
+    assert rep.converged, rep
+    assert rel_err(u, gold[name + "/u"]) < 1e-6
+    assert rel_err(p, gold[name + "/p"]) < 1e-5
