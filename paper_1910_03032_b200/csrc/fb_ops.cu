@@ -196,10 +196,11 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // per CTA: double-buffered map/slot stage, gather buffer, 4 work buffers per
 // element (34-52 KB); the grid is persistent (all CTAs resident).
 // Runtime-selectable launch shapes (tuning): g_fast_cfg[p] picks a variant.
-// Defaults measured with tools/tune_fast.py: p = 5, 6 stage their factor
-// blocks in shared memory through the TMA engine (variant 5 / 4: +14 % / +2 %);
-// at p = 7, 8 the extra 41-56 KB per CTA costs more occupancy than it saves.
-static int g_fast_cfg[9] = {0, 0, 0, 0, 0, 5, 4, 0, 0};
+// Defaults measured with tools/tune_fast.py: p = 2, 3, 5, 6 stage their
+// factor blocks in shared memory through the TMA engine (p = 3: +5 %, p = 5:
+// +14 %, p = 2, 6: +1-2 %); at p = 7, 8 the extra 41-56 KB per CTA costs more
+// occupancy than it saves.
+static int g_fast_cfg[9] = {0, 0, 3, 5, 0, 5, 4, 0, 0};
 
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   const int v = g_fast_cfg[op->rv->p < 9 ? op->rv->p : 0];
@@ -208,10 +209,15 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
     case 2:
       if (v == 1) return launch_fast_kind<3, 4, 16, 256, 3, true>(op, x, y, st);
       if (v == 2) return launch_fast_kind<3, 4, 8, 128, 6, false>(op, x, y, st);
+      if (v == 3) return launch_fast_kind<3, 4, 4, 64, 8, 3>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<3, 4, 4, 64, 10, 3>(op, x, y, st);
       return launch_fast_kind<3, 4, 4, 64, 10, true>(op, x, y, st);
     case 3:
       if (v == 1) return launch_fast_kind<4, 5, 8, 256, 3, true>(op, x, y, st);
       if (v == 2) return launch_fast_kind<4, 5, 4, 128, 6, false>(op, x, y, st);
+      if (v == 3) return launch_fast_kind<4, 5, 2, 64, 8, 3>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<4, 5, 2, 64, 10, 3>(op, x, y, st);
+      if (v == 5) return launch_fast_kind<4, 5, 4, 128, 4, 3>(op, x, y, st);
       return launch_fast_kind<4, 5, 2, 64, 10, true>(op, x, y, st);
     case 4:
       if (v == 1) return launch_fast_kind<5, 6, 4, 160, 5>(op, x, y, st);

@@ -101,7 +101,8 @@ struct SF3Pitch {
 // batch ahead); 1 = z-line schedule (three buffers, G_z in registers);
 // 2 = as 0, but the batch's factor block is copied into shared memory by the
 // TMA engine (cp.async.bulk, issued right after the previous batch's P5), so
-// P5 reads factors from shared memory instead of waiting on L2.
+// P5 reads factors from shared memory instead of waiting on L2; 3 = the
+// z-line schedule with that factor staging.
 template <int N, int Q, int KIND, int NE, int ZL = 0>
 struct SF3Shape {
   static constexpr int QP = SF3Pitch<Q>::QP;  // x-row pitch
@@ -116,8 +117,8 @@ struct SF3Shape {
   static constexpr int NB = (N <= 2) ? NLOC : NLOC - (N - 2) * (N - 2) * (N - 2);
   static constexpr int NBP = round_up(NB, 4);
   // work buffers per element: the z-line schedule (ZL) keeps G_z in registers
-  static constexpr int NBUF = (KIND == kMass) ? 2 : (ZL == 1 ? 3 : 4);
-  static constexpr bool FSTAGE = (ZL == 2) && (KIND != kMass);
+  static constexpr int NBUF = (KIND == kMass) ? 2 : ((ZL == 1 || ZL == 3) ? 3 : 4);
+  static constexpr bool FSTAGE = (ZL == 2 || ZL == 3) && (KIND != kMass);
   static constexpr int XBUF = N * N * (N | 1);          // gathered x_e (odd pitch)
   // shared-memory plan (bytes):
   //   [3 mbarriers | 3 x (map | slots) | gather buffer | work buffers]
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       }
       __syncthreads();
 
-      if constexpr (ZL != 1) {
+      if constexpr (ZL != 1 && ZL != 3) {
       // ---- P3: z-lines (b,a): b0 -> U (b0 in place), Gz = Dq_z U (b3) -------
 #pragma unroll 1
       for (int L = tid; L < NE * Q2; L += NT) {
@@ -600,12 +601,17 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         //   G_z = Dq_z U in registers; per point f = W g (g0, g1 from b1, b2);
         //   f0 -> b1, f1 -> b2; V = f_u + Dq_z^T f_z -> b0 (replaces U)
         constexpr int o = (KIND == kHelm) ? 1 : 0;
+        if constexpr (Sh::FSTAGE) {
+          if (comp == 0) mbar_wait(smem_u32(&bars[Sh::NSTAGE]), uint32_t(it & 1));
+        }
+        auto ldf = [&](const double* p_) { return Sh::FSTAGE ? *p_ : __ldg(p_); };
 #pragma unroll 1
         for (int L = tid; L < nel * Q2; L += NT) {
           const int el = L / Q2, ba = L - el * Q2;
           const int b = ba / Q, a = ba - b * Q;
           double* col = smem + el * ES + IX(0, b, a);
-          const double* __restrict__ f = P.fac + (e0 + el) * FACP + ba;
+          const double* __restrict__ f =
+              Sh::FSTAGE ? fsm + el * FACP + ba : P.fac + (e0 + el) * FACP + ba;
           double u[Q], g[Q];
 #pragma unroll
           for (int c = 0; c < Q; ++c) u[c] = col[c * YP];
@@ -619,15 +625,15 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
             const double* fc = f + c * Q2;
-            const double w00 = __ldg(fc + (o + 0) * Q3), w01 = __ldg(fc + (o + 1) * Q3);
-            const double w02 = __ldg(fc + (o + 2) * Q3), w11 = __ldg(fc + (o + 3) * Q3);
-            const double w12 = __ldg(fc + (o + 4) * Q3), w22 = __ldg(fc + (o + 5) * Q3);
+            const double w00 = ldf(fc + (o + 0) * Q3), w01 = ldf(fc + (o + 1) * Q3);
+            const double w02 = ldf(fc + (o + 2) * Q3), w11 = ldf(fc + (o + 3) * Q3);
+            const double w12 = ldf(fc + (o + 4) * Q3), w22 = ldf(fc + (o + 5) * Q3);
             double* pt = col + c * YP;
             const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = g[c];
             pt[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
             pt[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
             g[c] = w02 * g0 + w12 * g1 + w22 * g2;
-            u[c] = (KIND == kHelm) ? __ldg(fc) * u[c] : 0.0;
+            u[c] = (KIND == kHelm) ? ldf(fc) * u[c] : 0.0;
           }
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
@@ -638,6 +644,9 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           }
         }
         __syncthreads();
+        if constexpr (Sh::FSTAGE) {  // factor buffer free: stage the next batch's block
+          if (tid == 0 && comp == vdim - 1 && next < nbatch) prefetch_factors(next);
+        }
 
         // ---- P6: transposed derivative lines, in place: x b1, y b2 ---------
 #pragma unroll 1
