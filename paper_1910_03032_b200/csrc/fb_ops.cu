@@ -197,10 +197,11 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // element (34-52 KB); the grid is persistent (all CTAs resident).
 // Runtime-selectable launch shapes (tuning): g_fast_cfg[p] picks a variant.
 // Defaults measured with tools/tune_fast.py: p = 2, 3, 5, 6 stage their
-// factor blocks in shared memory through the TMA engine (p = 3: +5 %, p = 5:
+// factor blocks in shared memory through the TMA engine (p = 3: +5 %, p = 4
+// with the z-line schedule: +9 %, p = 5:
 // +14 %, p = 2, 6: +1-2 %); at p = 7, 8 the extra 41-56 KB per CTA costs more
 // occupancy than it saves.
-static int g_fast_cfg[9] = {0, 0, 3, 5, 0, 5, 4, 0, 0};
+static int g_fast_cfg[9] = {0, 0, 3, 5, 6, 5, 4, 0, 0};
 
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   const int v = g_fast_cfg[op->rv->p < 9 ? op->rv->p : 0];
@@ -225,6 +226,8 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
       if (v == 3) return launch_fast_kind<5, 6, 2, 96, 6, 2>(op, x, y, st);
       if (v == 4) return launch_fast_kind<5, 6, 1, 64, 12, 2>(op, x, y, st);
       if (v == 5) return launch_fast_kind<5, 6, 1, 96, 8, 2>(op, x, y, st);
+      if (v == 6) return launch_fast_kind<5, 6, 2, 96, 6, 3>(op, x, y, st);
+      if (v == 7) return launch_fast_kind<5, 6, 2, 64, 8, 3>(op, x, y, st);
       return launch_fast_kind<5, 6, 2, 96, 8>(op, x, y, st);
     case 5:
       if (v == 1) return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
@@ -246,6 +249,8 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
       if (v == 3) return launch_fast_kind<8, 9, 1, 128, 3, 2>(op, x, y, st);
       if (v == 4) return launch_fast_kind<8, 9, 1, 192, 2, 2>(op, x, y, st);
       if (v == 5) return launch_fast_kind<8, 9, 1, 96, 3, 2>(op, x, y, st);
+      if (v == 6) return launch_fast_kind<8, 9, 1, 128, 2, 3>(op, x, y, st);
+      if (v == 7) return launch_fast_kind<8, 9, 1, 192, 2, 3>(op, x, y, st);
       return launch_fast_kind<8, 9, 1, 128, 4>(op, x, y, st);
     case 8:
       if (v == 1) return launch_fast_kind<9, 10, 1, 96, 5>(op, x, y, st);
@@ -253,6 +258,8 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
       if (v == 3) return launch_fast_kind<9, 10, 1, 128, 2, 2>(op, x, y, st);
       if (v == 4) return launch_fast_kind<9, 10, 1, 192, 2, 2>(op, x, y, st);
       if (v == 5) return launch_fast_kind<9, 10, 1, 256, 1, 2>(op, x, y, st);
+      if (v == 6) return launch_fast_kind<9, 10, 1, 128, 2, 3>(op, x, y, st);
+      if (v == 7) return launch_fast_kind<9, 10, 1, 192, 1, 3>(op, x, y, st);
       return launch_fast_kind<9, 10, 1, 128, 4>(op, x, y, st);
     default: set_error("fast path not built for this degree"); return FB_ERR_UNSUPPORTED;
   }
@@ -675,7 +682,7 @@ int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count) 
 int64_t fb_operator_factor_count(const fb_operator* op) { return op ? op->fac.n : 0; }
 
 int fb_set_fast_config(int p, int variant) {
-  FB_REQUIRE(p >= 1 && p <= 8 && variant >= 0 && variant <= 5, "bad fast-path config");
+  FB_REQUIRE(p >= 1 && p <= 8 && variant >= 0 && variant <= 7, "bad fast-path config");
   g_fast_cfg[p] = variant;
   return FB_OK;
 }

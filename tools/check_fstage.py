@@ -8,7 +8,7 @@ for p in range(2, 9):
     pr = bench.build_problem(p, target=2e6)
     x = torch.randn(pr["N"], dtype=torch.float64, device="cuda")
     ref = None
-    for v in range(6):
+    for v in range(8):
         if _lib.lib.fb_set_fast_config(p, v) != 0:
             continue
         y = torch.empty_like(x)

@@ -26,7 +26,7 @@ def main():
         y = torch.empty_like(x)
         by = bench.algorithmic_bytes(pr["N"], pr["ne"], p)
         res = []
-        for v in range(6):
+        for v in range(8):
             if _lib.lib.fb_set_fast_config(p, v) != 0:
                 continue
             for _ in range(3):
