@@ -914,7 +914,10 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
   return FB_OK;
 }
 
-void fb_blockilu_destroy(fb_blockilu* B) { delete B; }
+void fb_blockilu_destroy(fb_blockilu* B) {
+  if (B) debug_canary_unregister(B->block_ptr.ptr);
+  delete B;
+}
 
 // out = (LU)^-1 r (transpose=0) or (LU)^-T r (transpose=1), both in the
 // original numbering.
@@ -1151,6 +1154,7 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
     const int rc_ell = build_ell(B.get());
     if (rc_ell != FB_OK) return rc_ell;
   }
+  debug_canary_register(B->block_ptr.ptr, int(nblocks + 1));  // FB_DEBUG_SYNC=1 only
   *out = B.release();  // new2old stays empty: the level is block-major already
   return FB_OK;
 }

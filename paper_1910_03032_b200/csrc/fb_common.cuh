@@ -27,12 +27,23 @@ inline void count_launch() { ++launch_counter(); }
     }                                                                                  \
   } while (0)
 
+bool debug_sync();  // FB_DEBUG_SYNC=1: synchronise and check after every launch
+void debug_canary_register(const int* dev_ptr, int n);
+void debug_canary_unregister(const int* dev_ptr);
+bool debug_canary_check(const char* where);
+
 #define FB_CHECK_LAUNCH()                                                              \
   do {                                                                                 \
     ::fb::count_launch();                                                              \
     cudaError_t _e = cudaGetLastError();                                               \
+    if (_e == cudaSuccess && ::fb::debug_sync()) {                                     \
+      _e = cudaDeviceSynchronize();                                                    \
+      if (_e == cudaSuccess)                                                           \
+        ::fb::debug_canary_check((std::string(__FILE__) + ":" + std::to_string(__LINE__)).c_str()); \
+    }                                                                                  \
     if (_e != cudaSuccess) {                                                           \
-      ::fb::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e));        \
+      ::fb::set_error(std::string("kernel launch (") + __FILE__ + ":" +               \
+                      std::to_string(__LINE__) + "): " + cudaGetErrorString(_e));      \
       return FB_ERR_CUDA;                                                              \
     }                                                                                  \
   } while (0)

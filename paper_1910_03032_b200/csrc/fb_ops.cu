@@ -3,6 +3,8 @@
 //   fb_operator_*     <- mfop Mass/Stiffness/Helmholtz/Gradient/Divergence
 //                        (mfop.py:169-319)
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -20,6 +22,41 @@ int build_factors_device(int dim, int64_t ne, const double* corners_dev, int nq,
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+bool debug_sync() {
+  static const bool on = [] {
+    const char* v = std::getenv("FB_DEBUG_SYNC");
+    return v != nullptr && v[0] == '1';
+  }();
+  return on;
+}
+
+static std::vector<std::pair<const int*, std::vector<int>>> g_canaries;
+void debug_canary_register(const int* p, int n) {
+  if (!debug_sync()) return;
+  std::vector<int> h(n);
+  cudaMemcpy(h.data(), p, n * sizeof(int), cudaMemcpyDeviceToHost);
+  g_canaries.push_back({p, h});
+}
+void debug_canary_unregister(const int* p) {
+  for (size_t i = 0; i < g_canaries.size(); ++i)
+    if (g_canaries[i].first == p) {
+      g_canaries.erase(g_canaries.begin() + i);
+      return;
+    }
+}
+bool debug_canary_check(const char* where) {
+  for (auto& c : g_canaries) {
+    std::vector<int> h(c.second.size());
+    cudaMemcpy(h.data(), c.first, h.size() * sizeof(int), cudaMemcpyDeviceToHost);
+    if (h != c.second) {
+      fprintf(stderr, "CANARY %p corrupted after launch at %s\n", (const void*)c.first, where);
+      c.second = h;  // report once
+      return false;
+    }
+  }
+  return true;
+}
+
 int64_t& launch_counter() {
   static int64_t n = 0;
   return n;
@@ -482,15 +519,17 @@ int fb_restriction_create(int dim, int p, int64_t ne, int64_t ndofs,
       if (!direct[i]) mult_max = std::max(mult_max, count[i]);
     std::vector<int> cls_of_m(mult_max + 1, -1);
     int ncls = 0;
+    // multiplicity 0: DoFs no element touches (ghost planes of a slab-local
+    // space); their class has no slots and the sum writes 0.0 (np.bincount)
     for (int64_t i = 0; i < ndofs; ++i)
       if (!direct[i] && cls_of_m[count[i]] < 0) cls_of_m[count[i]] = 1;
-    for (int m = 1; m <= mult_max; ++m)
+    for (int m = 0; m <= mult_max; ++m)
       if (cls_of_m[m] > 0) cls_of_m[m] = ncls++;
     ok = ncls <= 16;
     if (ok) {
       r->ncls = ncls;
       std::vector<int64_t> ccount(ncls, 0);
-      for (int m = 1; m <= mult_max; ++m)
+      for (int m = 0; m <= mult_max; ++m)
         if (cls_of_m[m] >= 0) r->cls_m[cls_of_m[m]] = m;
       for (int64_t i = 0; i < ndofs; ++i)
         if (!direct[i]) ccount[cls_of_m[count[i]]]++;

@@ -94,11 +94,17 @@ class TorchComm:
 
 
 class ThreadHub:
-    """Shared state of R in-process ranks (one thread each, one GPU)."""
+    """Shared state of R in-process ranks (one thread each, one GPU).  A
+    baton lock lets exactly one rank thread run host code (and enqueue device
+    work) at a time; it is released only while a rank waits at a barrier, so
+    ranks run one after another between communication points -- the
+    multi-process semantics without concurrent host threads in torch / the C
+    library."""
 
     def __init__(self, world):
         self.world = world
         self.barrier = threading.Barrier(world)
+        self.baton = threading.Lock()
         self.slots = {}
 
 
@@ -113,8 +119,16 @@ class ThreadComm:
         self.world = hub.world
 
     def _sync(self):
-        torch.cuda.synchronize()
-        self.hub.barrier.wait()
+        try:
+            torch.cuda.synchronize()
+        except BaseException:
+            self.hub.barrier.abort()
+            raise
+        self.hub.baton.release()
+        try:
+            self.hub.barrier.wait()
+        finally:
+            self.hub.baton.acquire()
 
     def exchange(self, send_down, send_up, recv_down, recv_up):
         h, r = self.hub, self.rank
@@ -150,15 +164,27 @@ class ThreadComm:
 def run_threads(world, fn):
     """Run fn(comm) for ranks 0..world-1 as threads on the current device;
     returns the per-rank results (re-raises the first exception)."""
+    if torch.cuda.is_available():
+        # lazy CUDA / cuSOLVER initialisation must not race between the rank threads
+        torch.cuda.init()
+        torch.linalg.inv(torch.eye(2, dtype=torch.float64, device=dev.device()))
     hub = ThreadHub(world)
     res, err = [None] * world, [None]
 
     def body(r):
+        hub.baton.acquire()
         try:
             res[r] = fn(ThreadComm(hub, r))
         except BaseException as e:  # noqa: BLE001 -- surfaced below
             err[0] = err[0] or e
             hub.barrier.abort()
+        finally:
+            try:
+                if torch.cuda.is_available():
+                    torch.cuda.synchronize()
+            except BaseException as e:  # noqa: BLE001 -- a device fault: surfaced below
+                err[0] = err[0] or e
+            hub.baton.release()
 
     th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
     for t in th:

@@ -7,6 +7,7 @@ computes on the host.
 """
 
 import ctypes as C
+import threading
 
 import numpy as np
 import torch
@@ -36,7 +37,9 @@ _WS = {}
 
 
 def workspace(n):
-    key = torch.cuda.current_device()
+    # per device AND per host thread: the in-process multi-rank tests drive
+    # several ranks from threads, which must not share reduction scratch
+    key = (torch.cuda.current_device(), threading.get_ident())
     ws = _WS.get(key)
     if ws is None:
         ws = _WS[key] = Workspace(n)

@@ -157,3 +157,24 @@ def test_convection_matches_reference(name, device_geom):
     op = mfop.setup("convection", vspace=vs, geom=geom)
     u = np.random.default_rng(c["seed"]).standard_normal(vs.ndofs)
     assert rel_err(op.apply(u), gold[name + "/y"]) < 1e-12
+
+
+def test_restriction_with_untouched_dofs_is_bincount():
+    """DoFs no element touches (the ghost planes of a slab-local space) sum
+    to zero in the class-major E->L layout -- bitwise np.bincount."""
+    from paper_1910_03032_b200 import geometry, mfop, spaces
+
+    class Padded:
+        def __init__(self, sp, extra):
+            self.dim, self.p = sp.dim, sp.p
+            self.element_dofs = sp.element_dofs
+            self.ndofs_scalar = sp.ndofs_scalar + extra
+
+    m = geometry.cartesian_mesh((3, 2, 2))
+    for p in (1, 3):
+        sp = Padded(spaces.FESpace(m, p), 37)
+        r = mfop.Restriction(sp)
+        xe = np.random.default_rng(p).standard_normal(sp.element_dofs.shape)
+        want = np.bincount(sp.element_dofs.ravel(), weights=xe.ravel(), minlength=sp.ndofs_scalar)
+        got = r.scatter_add(xe)
+        assert np.array_equal(got, want)
