@@ -503,7 +503,10 @@ def run_ours(args, rank, world):
         probs.clear()
         gc.collect()
         torch.cuda.empty_cache()
-        sharded = lor_pcg_sharded(rank, world)
+        try:
+            sharded = lor_pcg_sharded(rank, world)
+        except Exception as exc:  # keep the headline line if the auxiliary solve fails
+            sharded = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank != 0:
         return
     peak, peak_kind = load_peaks()
