@@ -44,6 +44,7 @@ extern "C" {
 #define FB_GRADIENT 3
 #define FB_DIVERGENCE 4
 #define FB_CONVECTION 5  /* nonlinear (u . grad) u load, mfop.py:322-358 */
+#define FB_CURLCURL 6    /* weak rotational viscous term, mfop.py:361-413 */
 
 typedef struct fb_restriction fb_restriction;
 typedef struct fb_operator fb_operator;

@@ -183,6 +183,45 @@ def convection_apply(element_dofs, ns, B, D, d, jinv, wdet, u):
     return out
 
 
+def curlcurl_apply(element_dofs, ns, B, D, d, jinv, wdet, nu, u):
+    """int nu (curl u) . (curl v) (mfop.py:381-413)."""
+    ev = Eval(B, D, d)
+    wd = nu * wdet
+    gphys = {}
+    for c in range(d):
+        gs = ev.grads(gather(element_dofs, u[c * ns:(c + 1) * ns]))
+        for k in range(d):
+            gphys[c, k] = sum(jinv[..., m, k] * gs[m] for m in range(d))
+    out = np.empty(d * ns)
+    if d == 2:
+        om = wd * (gphys[1, 0] - gphys[0, 1])
+        for c, (k, sign) in enumerate([(1, -1.0), (0, 1.0)]):
+            fs = [sign * jinv[..., m, k] * om for m in range(d)]
+            out[c * ns:(c + 1) * ns] = scatter_add(element_dofs, ev.grads_t(fs), ns)
+        return out
+    om = [wd * (gphys[2, 1] - gphys[1, 2]), wd * (gphys[0, 2] - gphys[2, 0]),
+          wd * (gphys[1, 0] - gphys[0, 1])]
+    eps = np.zeros((3, 3, 3))
+    for a, b, c in [(0, 1, 2), (1, 2, 0), (2, 0, 1)]:
+        eps[a, b, c] = 1.0
+        eps[a, c, b] = -1.0
+    for c in range(d):
+        t = [None] * d
+        for b in range(d):
+            terms = [eps[a, b, c] * om[a] for a in range(d) if eps[a, b, c] != 0.0]
+            t[b] = sum(terms) if terms else None
+        fs = [sum(jinv[..., m, b] * t[b] for b in range(d) if t[b] is not None) for m in range(d)]
+        out[c * ns:(c + 1) * ns] = scatter_add(element_dofs, ev.grads_t(fs), ns)
+    return out
+
+
+def make_curlcurl(vspace, geom, nu=1.0):
+    B, D = eval_matrices(vspace, geom.rule.points)
+    wdet = mass_factor(geom.detj, geom.w)
+    return lambda u: curlcurl_apply(vspace.element_dofs, vspace.ndofs_scalar, B, D, vspace.dim,
+                                    geom.jinv, wdet, nu, u)
+
+
 def make_convection(vspace, geom):
     B, D = eval_matrices(vspace, geom.rule.points)
     wdet = mass_factor(geom.detj, geom.w)

@@ -19,7 +19,7 @@ FB_ERR_OOM = 3
 FB_ERR_UNSUPPORTED = 4
 
 KIND = {"mass": 0, "stiffness": 1, "helmholtz": 2, "gradient": 3, "divergence": 4,
-        "convection": 5}
+        "convection": 5, "curlcurl": 6}
 
 _vp = C.c_void_p
 _i64 = C.c_int64

@@ -100,6 +100,11 @@ __global__ void factor_kernel(const __grid_constant__ GeomParams P) {
         out[int64_t(k++) * kstride] = __dmul_rn(nw, sacc);
       }
   }
+  if (P.kind == FB_CURLCURL) {
+    out[0] = __dmul_rn(P.nu, wdet);
+    for (int mm = 0; mm < d; ++mm)
+      for (int kk = 0; kk < d; ++kk) out[int64_t(1 + mm * d + kk) * kstride] = jinv[mm][kk];
+  }
   if (P.kind == FB_GRADIENT || P.kind == FB_DIVERGENCE || P.kind == FB_CONVECTION) {
     for (int cc = 0; cc < d; ++cc)
       for (int mm = 0; mm < d; ++mm) out[int64_t(cc * d + mm) * kstride] = __dmul_rn(wdet, jinv[mm][cc]);

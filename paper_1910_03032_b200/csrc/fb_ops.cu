@@ -423,7 +423,8 @@ static int finish_operator(fb_operator* op, const double* points, const double* 
     // E-vector scratch: largest of input/output E-vectors over components
     const int64_t nvl = rv->nloc, npl = rp ? rp->nloc : 0;
     int64_t need = 0;
-    if (kind <= FB_HELMHOLTZ || kind == FB_CONVECTION) need = int64_t(vdim) * ne * nvl;
+    if (kind <= FB_HELMHOLTZ || kind == FB_CONVECTION || kind == FB_CURLCURL)
+      need = int64_t(vdim) * ne * nvl;
     else if (kind == FB_GRADIENT) need = int64_t(dim) * ne * nvl + ne * npl;
     else need = ne * npl;
     FB_TRY_CUDA(op->S.alloc(need));
@@ -599,7 +600,7 @@ int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction*
   FB_REQUIRE(out != nullptr, "out is NULL");
   *out = nullptr;
   FB_REQUIRE(rv != nullptr, "space restriction is NULL");
-  FB_REQUIRE(kind >= FB_MASS && kind <= FB_CONVECTION, "unknown operator kind");
+  FB_REQUIRE(kind >= FB_MASS && kind <= FB_CURLCURL, "unknown operator kind");
   FB_REQUIRE(nq1 >= 1 && nq1 <= 32, "unsupported rule size");
   FB_REQUIRE(B != nullptr && D != nullptr && points != nullptr, "B/D/points are NULL");
   std::unique_ptr<fb_operator> op(new fb_operator());
@@ -630,6 +631,13 @@ int fb_operator_create(int kind, const fb_restriction* rv, const fb_restriction*
     }
     if (kind != FB_MASS)
       relayout(stiff, ne, nqd, ksym, fac.data(), op->fstride, koff, lanes, op->nfac);
+  } else if (kind == FB_CURLCURL) {
+    FB_REQUIRE(vdim == dim, "curl-curl expects a vector space with vdim == dim");
+    FB_REQUIRE(grad != nullptr, "curl factor (nu wdet, Jinv) required");
+    op->nfac = 1 + dim * dim;
+    op->fstride = (int64_t(op->nfac) * nqd + 1) / 2 * 2;
+    fac.assign(size_t(ne) * op->fstride, 0.0);
+    relayout(grad, ne, nqd, 1 + dim * dim, fac.data(), op->fstride, 0);
   } else if (kind == FB_CONVECTION) {
     FB_REQUIRE(vdim == dim, "convection expects a vector space with vdim == dim");
     FB_REQUIRE(grad != nullptr, "gradient factor required");
@@ -664,7 +672,7 @@ int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restric
   FB_REQUIRE(out != nullptr, "out is NULL");
   *out = nullptr;
   FB_REQUIRE(rv != nullptr, "space restriction is NULL");
-  FB_REQUIRE(kind >= FB_MASS && kind <= FB_CONVECTION, "unknown operator kind");
+  FB_REQUIRE(kind >= FB_MASS && kind <= FB_CURLCURL, "unknown operator kind");
   FB_REQUIRE(nq1 >= 1 && nq1 <= 32, "unsupported rule size");
   FB_REQUIRE(points && weights && B && D, "points/weights/B/D are NULL");
   FB_REQUIRE(rv->ne == 0 || corners != nullptr, "corners are NULL");
@@ -684,6 +692,9 @@ int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restric
   } else if (kind == FB_CONVECTION) {
     FB_REQUIRE(vdim == dim, "convection expects a vector space with vdim == dim");
     op->nfac = dim * dim;
+  } else if (kind == FB_CURLCURL) {
+    FB_REQUIRE(vdim == dim, "curl-curl expects a vector space with vdim == dim");
+    op->nfac = 1 + dim * dim;
   } else {
     FB_REQUIRE(rp != nullptr && rp->ne == ne && rp->dim == dim, "pressure restriction mismatch");
     FB_REQUIRE(Bp != nullptr && Dp != nullptr, "Bp/Dp required");
@@ -756,7 +767,7 @@ static int general_apply(const fb_operator* op, int gkind, const double* x, doub
   const fb_restriction* rin = rv;
   const fb_restriction* rout = rv;
   int ncomp_out = 1;
-  if (gkind <= kgHelm || gkind == kgConv) {
+  if (gkind <= kgHelm || gkind == kgConv || gkind == kgCurl) {
     gy = op->vdim;
     ncomp_out = op->vdim;
     P.in_comp_stride = rv->ndofs;
@@ -826,6 +837,7 @@ int fb_operator_apply(const fb_operator* op, const double* x, double* y, void* s
     case FB_HELMHOLTZ: gk = kgHelm; break;
     case FB_GRADIENT: gk = kgGrad; break;
     case FB_CONVECTION: gk = kgConv; break;
+    case FB_CURLCURL: gk = kgCurl; break;
     default: gk = kgDiv; break;
   }
   return general_apply(op, gk, x, y, st);

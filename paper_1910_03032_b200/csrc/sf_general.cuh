@@ -13,7 +13,7 @@
 
 namespace fb {
 
-enum GenKind { kgMass = 0, kgStiff = 1, kgHelm = 2, kgGrad = 3, kgDiv = 4, kgGradT = 5, kgConv = 6 };
+enum GenKind { kgMass = 0, kgStiff = 1, kgHelm = 2, kgGrad = 3, kgDiv = 4, kgGradT = 5, kgConv = 6, kgCurl = 7 };
 
 struct SFGParams {
   const int* __restrict__ map_in;   // (ne, nin^dim)
@@ -259,6 +259,69 @@ __global__ void sf_general_kernel(const __grid_constant__ SFGParams P) {
     }
     __syncthreads();
     gen_values(dim, vals, nq, BvT, nv, xin, false, t0, t1);
+    double* ye = P.ye + (int64_t(comp) * P.ne + e) * nvd;
+    for (int l = tid; l < nvd; l += nt) ye[l] = xin[l];
+    return;
+  }
+
+  if (kind == kgCurl) {
+    // curl-curl, output component comp (mfop.py:381-413); factors
+    // fe[0] = nu wdet, fe[1 + m d + k] = Jinv[m][k].  om = nu wdet curl u is
+    // accumulated component by component in f[], then fs_m = sum_b Jinv[m][b]
+    // t_b with t = eps(., ., comp) om, and y_comp = grads_t(fs).
+    const int nom = dim == 3 ? 3 : 1;
+    for (int a = 0; a < nom; ++a)
+      for (int qp = tid; qp < nqd; qp += nt) f[a][qp] = 0.0;
+    for (int cc = 0; cc < dim; ++cc) {
+      const double* xk = P.x + cc * P.in_comp_stride;
+      for (int l = tid; l < nvd; l += nt) xin[l] = xk[P.map_in[e * nvd + l]];
+      __syncthreads();
+      gen_grads(dim, xin, nv, Bv, Dv, nq, g, t0, t1);
+      for (int qp = tid; qp < nqd; qp += nt) {
+        const double wd = fe[qp];
+        double gp[3];
+        for (int k = 0; k < dim; ++k) {
+          double s = 0.0;
+          for (int m = 0; m < dim; ++m) s += fe[(1 + m * dim + k) * nqd + qp] * g[m][qp];
+          gp[k] = s;  // d u_cc / d x_k
+        }
+        if (dim == 2) {
+          f[0][qp] += (cc == 1 ? wd * gp[0] : -wd * gp[1]);
+        } else if (cc == 0) {
+          f[1][qp] += wd * gp[2];
+          f[2][qp] -= wd * gp[1];
+        } else if (cc == 1) {
+          f[0][qp] -= wd * gp[2];
+          f[2][qp] += wd * gp[0];
+        } else {
+          f[0][qp] += wd * gp[1];
+          f[1][qp] -= wd * gp[0];
+        }
+      }
+      __syncthreads();
+    }
+    for (int qp = tid; qp < nqd; qp += nt) {
+      double t[3] = {0.0, 0.0, 0.0};
+      if (dim == 2) {
+        if (comp == 0) t[1] = -f[0][qp]; else t[0] = f[0][qp];
+      } else if (comp == 0) {
+        t[2] = f[1][qp];
+        t[1] = -f[2][qp];
+      } else if (comp == 1) {
+        t[0] = f[2][qp];
+        t[2] = -f[0][qp];
+      } else {
+        t[1] = f[0][qp];
+        t[0] = -f[1][qp];
+      }
+      for (int m = 0; m < dim; ++m) {
+        double s = 0.0;
+        for (int b = 0; b < dim; ++b) s += fe[(1 + m * dim + b) * nqd + qp] * t[b];
+        g[m][qp] = s;
+      }
+    }
+    __syncthreads();
+    gen_grads_t(dim, g, nq, BvT, DvT, nv, xin, false, t0, t1);
     double* ye = P.ye + (int64_t(comp) * P.ne + e) * nvd;
     for (int l = tid; l < nvd; l += nt) ye[l] = xin[l];
     return;

@@ -388,6 +388,46 @@ class ConvectionOperator(_DeviceOperator):
         self.setup_seconds = time.perf_counter() - t0
 
 
+def _curl_factor(geom, nu):
+    """(ne, nq, 1 + d^2): nu * wdet, then Jinv[m][k] (m-major)."""
+    wdet = _mass_factor(geom)
+    d = geom.jinv.shape[-1]
+    out = np.empty(wdet.shape + (1 + d * d,))
+    out[..., 0] = nu * wdet
+    out[..., 1:] = geom.jinv.reshape(wdet.shape + (d * d,))
+    return out
+
+
+class CurlCurlOperator(_DeviceOperator):
+    """Weak rotational viscous term int nu (curl u) . (curl v) (mfop.py:361-413).
+    One kernel computes the physical gradients of every velocity component,
+    the weighted vorticity and the transposed gradient of the output
+    component; deterministic E->L sum."""
+
+    kind = "curlcurl"
+
+    def __init__(self, vspace, geom, nu=1.0):
+        _check_rule_match(vspace, geom)
+        if vspace.vdim != vspace.dim:
+            raise ValueError("curl-curl expects a vector space with vdim == dim")
+        t0 = time.perf_counter()
+        self.vspace = vspace
+        self.geom = geom
+        self.nu = float(nu)
+        pts = np.asarray(geom.rule.points, dtype=np.float64)
+        self.rule_points = pts
+        self.B, self.D = _eval_matrices(vspace, pts)
+        self.factors = QPointFactors()
+        curl = None if _is_device_geom(geom) else _curl_factor(geom, self.nu)
+        self.restriction = restriction(vspace)
+        self._create(self.kind, self.restriction, None, vspace.dim, pts, self.B, self.D, None,
+                     None, None, None, curl, geom, nu=self.nu)
+        n = vspace.ndofs
+        self.shape = (n, n)
+        self.in_size = self.out_size = n
+        self.setup_seconds = time.perf_counter() - t0
+
+
 class ConstrainedOperator(Operator):
     """Identity on constrained rows, the inner operator elsewhere
     (mfop.py:416-433): xi = x; xi[C] = 0; y = A xi; y[C] = x[C]."""
@@ -442,7 +482,7 @@ def setup(kind, space=None, geom=None, vspace=None, pspace=None, nu=1.0, c=0.0):
     if kind == "convection":
         return ConvectionOperator(vspace or space, geom)
     if kind == "curlcurl":
-        raise NotImplementedError(f"operator kind {kind!r} is outside the B200 hot path")
+        return CurlCurlOperator(vspace or space, geom, nu=nu)
     raise ValueError(f"unknown operator kind {kind!r}")
 
 

@@ -251,6 +251,13 @@ CONV_CASES = [
 ]
 
 
+CURL_CASES = [
+    ("curl_2d_p3", 2, (4, 3), None, 0.08, 3, 7),
+    ("curl_3d_p2", 3, (3, 2, 2), None, 0.08, 2, 8),
+    ("curl_3d_p4_periodic", 3, (3, 3, 3), (True,) * 3, 0.05, 4, 9),
+]
+
+
 def make_extras():
     """Next-row operators of SURVEY 8(f) item 4 (cfg5 projection step)."""
     mesh, fespace, mfop, _, _, _ = ref_modules()
@@ -284,8 +291,16 @@ def make_extras():
     out["tgv3d_p3/p"] = st.p
     out["tgv3d_p3/its"] = np.array(its)
     out["tgv3d_p3/energy"] = np.array([st.kinetic_energy()])
+    curl = []
+    for (name, d, counts, periodic, perturb, p, seed) in CURL_CASES:
+        _, vs, geom = build(mesh, fespace, d, counts, periodic, perturb, p, vdim=d)
+        op = mfop.CurlCurlOperator(vs, geom, nu=0.7)
+        u = np.random.default_rng(seed).standard_normal(vs.ndofs)
+        out[name + "/y"] = op.apply(u)
+        curl.append(dict(name=name, d=d, counts=counts, periodic=periodic, perturb=perturb,
+                         p=p, seed=seed, nu=0.7))
     np.savez_compressed(os.path.join(HERE, "extras.npz"), **out)
-    return {"convection": manifest, "projection": [dict(tgv, counts=list(tgv["counts"]),
+    return {"convection": manifest, "curlcurl": curl, "projection": [dict(tgv, counts=list(tgv["counts"]),
                                                         iterations=its)]}
 
 

@@ -178,3 +178,21 @@ def test_restriction_with_untouched_dofs_is_bincount():
         want = np.bincount(sp.element_dofs.ravel(), weights=xe.ravel(), minlength=sp.ndofs_scalar)
         got = r.scatter_add(xe)
         assert np.array_equal(got, want)
+
+
+CURL = {c["name"]: c for c in MAN.get("curlcurl", [])}
+
+
+@pytest.mark.parametrize("device_geom", [False, True])
+@pytest.mark.parametrize("name", sorted(CURL))
+def test_curlcurl_matches_reference(name, device_geom):
+    """CurlCurlOperator on the device vs the reference's (extras.npz)."""
+    from paper_1910_03032_b200 import geometry, mfop
+    c = CURL[name]
+    gold = load("extras")
+    m, vs, geom = build(c["d"], c["counts"], c["periodic"], c["perturb"], c["p"], vdim=c["d"])
+    if device_geom:
+        geom = geometry.DeviceGeometry(m, vs.basis.quad)
+    op = mfop.setup("curlcurl", vspace=vs, geom=geom, nu=c["nu"])
+    u = np.random.default_rng(c["seed"]).standard_normal(vs.ndofs)
+    assert rel_err(op.apply(u), gold[name + "/y"]) < 1e-12
