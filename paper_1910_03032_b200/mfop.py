@@ -522,3 +522,19 @@ def load_vector(space, geom, f):
         out[c * ns:(c + 1) * ns] = np.bincount(space.element_dofs.ravel(), weights=loc.ravel(),
                                                 minlength=ns)
     return out
+
+
+def boundary_normal_flux(space, g, attributes=None, n_quad=None):
+    """Boundary load b_i = int_faces psi_i (g . n) (mfop.py:623-684): a device
+    SpMV of a face matrix built once per space (boundary.py)."""
+    from . import boundary
+    return boundary.boundary_normal_flux(space, g, attributes=attributes, n_quad=n_quad)
+
+
+def boundary_rotational_rhs(vspace, pspace, u, nu=1.0, attributes=None, n_quad=None):
+    """Pressure load r_j = -nu int_faces (n x curl u) . grad psi_j
+    (mfop.py:687-807): a device SpMV of a face matrix built once per space
+    pair (boundary.py).  Device u gives a device result, host u a host one."""
+    from . import boundary
+    return boundary.boundary_rotational_rhs(vspace, pspace, u, nu=nu, attributes=attributes,
+                                            n_quad=n_quad)

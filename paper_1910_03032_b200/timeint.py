@@ -9,10 +9,12 @@ LOR V-cycle, and a mass solve for the nodal convection term.  Every operator
 solver runs through libfbb200; the state and the history vectors live on the
 device and the BDF combinations are libfbb200 axpby kernels.
 
-Scope: domains without boundary (the periodic Taylor-Green vortex of cfg5).
-Bounded domains also need the reference's boundary surface functionals
-(``boundary_rotational_rhs`` / ``boundary_normal_flux``, mfop.py:600-807),
-which are not on the B200 path yet.
+Periodic domains (the Taylor-Green vortex of cfg5) and bounded ones: with
+boundary faces the step adds the reference's surface functionals
+(``boundary_rotational_rhs`` / ``boundary_normal_flux``, mfop.py:623-807; both
+device SpMVs of face matrices built once, ``boundary.py``), Dirichlet
+velocity lifting and a constrained Helmholtz solve with a Dirichlet LOR
+V-cycle (timeint.py:266-269, 310-316, 338-381).
 """
 
 from dataclasses import dataclass
@@ -20,6 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import boundary
 from . import device as dev
 from . import mfop, vec
 from .solvers import (BlockDiagonalPreconditioner, DiagonalPreconditioner, LORPreconditioner,
@@ -89,9 +92,6 @@ class ProjectionStepper:
             raise ValueError("projection order must be 1, 2, or 3")
         mesh = vspace.mesh
         self.has_boundary = mesh.boundary_faces.shape[0] > 0
-        if self.has_boundary:
-            raise NotImplementedError("bounded domains need boundary_rotational_rhs / "
-                                      "boundary_normal_flux, not on the B200 path yet")
         self.dt = float(dt)
         self.nu = float(nu)
         self.vspace, self.pspace, self.geom = vspace, pspace, geom
@@ -110,13 +110,15 @@ class ProjectionStepper:
                                               smoother=smoother)
         self.mean = MeanProjector()
         self.pressure_weights = collocated_mass_diagonal(pspace)
-        self.bdofs = np.zeros(0, dtype=np.int64)
+        self.bdofs = (vspace.expand_dofs(vspace.boundary_dof_set())
+                      if self.has_boundary else np.zeros(0, dtype=np.int64))
+        self._bdofs_dev = torch.from_numpy(self.bdofs).to(dev.device()) if self.has_boundary else None
         self._helm = {}
         self._scalar_v = FESpace(mesh, vspace.p)
         self.t = None
         self.u = None
         self.p = None
-        self.u_hist, self.n_hist = [], []
+        self.u_hist, self.n_hist, self.r_hist = [], [], []
         self._volume = float(np.sum(geom.detj @ geom.w))
 
     # -- state ----------------------------------------------------------------
@@ -127,6 +129,23 @@ class ProjectionStepper:
         self.p = dev.zeros(self.pspace.ndofs)
         self.u_hist = [self.u.clone()]
         self.n_hist = [self._nodal_convection(self.u)[0]]
+        self.r_hist = [self._rotational_bc(self.u)]
+        return self
+
+    def initialize_history(self, states, t_last):
+        """Full-order start from k states ordered oldest to newest
+        (timeint.py:280-294)."""
+        if len(states) != self.k:
+            raise ValueError(f"need {self.k} states, got {len(states)}")
+        self.t = float(t_last)
+        self.u_hist, self.n_hist, self.r_hist = [], [], []
+        for u in states:
+            u = dev.to_device(np.asarray(u, dtype=np.float64)).clone()
+            self.u_hist.insert(0, u)
+            self.n_hist.insert(0, self._nodal_convection(u)[0])
+            self.r_hist.insert(0, self._rotational_bc(u))
+        self.u = self.u_hist[0].clone()
+        self.p = dev.zeros(self.pspace.ndofs)
         return self
 
     # -- pieces ----------------------------------------------------------------
@@ -144,6 +163,12 @@ class ProjectionStepper:
         vec.scale(-1.0, y, y)
         return self._mass_solve(y)
 
+    def _rotational_bc(self, u):
+        """-nu (n x curl u, grad q) on the boundary (timeint.py:310-316)."""
+        if not self.has_boundary:
+            return None
+        return boundary.boundary_rotational_rhs(self.vspace, self.pspace, u, nu=self.nu)
+
     def _helmholtz(self, b0):
         key = round(b0, 12)
         if key not in self._helm:
@@ -151,7 +176,8 @@ class ProjectionStepper:
             op = mfop.HelmholtzOperator(self.vspace, self.geom, c=c, nu=self.nu)
             A = mfop.ConstrainedOperator(op, self.bdofs)
             cyc = LORPreconditioner(self._scalar_v, "helmholtz", nu=self.nu, c=c,
-                                    dirichlet_attrs=None, smoother=self.smoother)
+                                    dirichlet_attrs=("all" if self.has_boundary else None),
+                                    smoother=self.smoother)
             pre = BlockDiagonalPreconditioner(cyc, self.vspace.vdim, self.vspace.ndofs_scalar)
             self._helm[key] = (op, A, pre)
         return self._helm[key]
@@ -180,7 +206,16 @@ class ProjectionStepper:
             terms.insert(0, (1.0, f_star))
         F = _combo(terms, nv)
 
-        rhs_p = deflate_mean(self.G.apply_transpose(F))
+        g_new = (None if self.dirichlet is None or not self.has_boundary
+                 else (lambda x: self.dirichlet(x, t_new)))
+        rhs_p = self.G.apply_transpose(F)
+        if self.has_boundary:
+            for j in range(1, k_eff + 1):
+                vec.axpby(float(s.a[j - 1]), self.r_hist[j - 1], 1.0, rhs_p)
+            if g_new is not None:
+                fl = boundary.flux_matrix(self.pspace)(g_new)  # device SpMV
+                vec.axpby(-(b0 / dt), fl, 1.0, rhs_p)
+        rhs_p = deflate_mean(rhs_p)
         p, prep = cg(self.Lp, rhs_p, precond=self.pressure_pre, x0=self.p, project=self.mean,
                      config=self.config)
         if not prep.converged:
@@ -190,16 +225,27 @@ class ProjectionStepper:
         op, A, pre = self._helmholtz(b0)
         b_u = self.M.apply(F)
         vec.axpby(-1.0, self.G.apply(p), 1.0, b_u)
+        u_lift = None
+        if g_new is not None:
+            lift = np.zeros(nv)
+            lift[self.bdofs] = self.vspace.project(g_new)[self.bdofs]
+            u_lift = dev.to_device(lift)
+            vec.axpby(-1.0, op.apply(u_lift), 1.0, b_u)
+        if self.has_boundary:
+            b_u.index_fill_(0, self._bdofs_dev, 0.0)
         u, hrep = cg(A, b_u, precond=pre, config=self.config)
         if not hrep.converged:
             raise RuntimeError(f"velocity solve failed: {hrep}")
         rep.helmholtz_iters = hrep.iterations
+        if u_lift is not None:
+            vec.axpby(1.0, u_lift, 1.0, u)
 
         n_new, it_n = self._nodal_convection(u)
         rep.mass_iters = it_n
         self.u_hist.insert(0, u)
         self.n_hist.insert(0, n_new)
-        del self.u_hist[self.k:], self.n_hist[self.k:]
+        self.r_hist.insert(0, self._rotational_bc(u))
+        del self.u_hist[self.k:], self.n_hist[self.k:], self.r_hist[self.k:]
         self.u, self.p, self.t = u, deflate_mean(p, self.pressure_weights), t_new
         return rep
 

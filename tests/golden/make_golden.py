@@ -311,8 +311,78 @@ def tgv_velocity(x):
                      np.zeros_like(X)], axis=1)
 
 
+# (name, d, counts, perturb, p_v, p_p, attributes, n_quad, seed): the boundary
+# surface functionals of the bounded-domain projection step (mfop.py:623-807)
+BOUNDARY_CASES = [
+    ("bnd_2d_p3", 2, (3, 2), 0.08, 3, 3, None, None, 1),
+    ("bnd_2d_p4_th", 2, (2, 3), 0.05, 4, 3, (1, 3), None, 2),
+    ("bnd_3d_p2", 3, (2, 2, 2), 0.08, 2, 2, None, None, 3),
+    ("bnd_3d_p3_nq", 3, (2, 1, 2), 0.05, 3, 3, (2, 5), 6, 4),
+]
+
+
+def flux_field(x):
+    """A smooth vector field with nonzero normal flux on every face."""
+    d = x.shape[1]
+    cols = [np.sin(1.3 * x[:, 0] + 0.2) + x[:, 1] ** 2, np.cos(0.7 * x[:, 1]) - x[:, 0] * x[:, 1]]
+    if d == 3:
+        cols.append(x[:, 2] * (1.0 + x[:, 0]) + np.sin(x[:, 1]))
+        cols[0] = cols[0] + 0.5 * x[:, 2]
+    return np.stack(cols, axis=1)
+
+
+def tgv2d_exact(nu):
+    def g(x, t):
+        f = np.exp(-2.0 * nu * t)
+        X, Y = x[:, 0], x[:, 1]
+        return np.stack([np.sin(X) * np.cos(Y) * f, -np.cos(X) * np.sin(Y) * f], axis=1)
+    return g
+
+
+def make_boundary():
+    mesh, fespace, mfop, solvers, _, _ = ref_modules()
+    from flowbench import timeint
+    out, cases = {}, []
+    for (name, d, counts, perturb, pv, pp, attrs, nq, seed) in BOUNDARY_CASES:
+        m = mesh.perturb_mesh(mesh.cartesian_mesh(counts), perturb, seed=11)
+        vs = fespace.FESpace(m, pv, vdim=d)
+        ps = fespace.FESpace(m, pp)
+        u = np.random.default_rng(seed).standard_normal(vs.ndofs)
+        out[name + "/rot"] = mfop.boundary_rotational_rhs(vs, ps, u, nu=0.37, attributes=attrs,
+                                                          n_quad=nq)
+        out[name + "/flux"] = mfop.boundary_normal_flux(ps, flux_field, attributes=attrs,
+                                                        n_quad=nq)
+        cases.append(dict(name=name, d=d, counts=counts, perturb=perturb, p_v=pv, p_p=pp,
+                          attributes=attrs, n_quad=nq, seed=seed, nu=0.37))
+    # bounded-domain projection stepping (timeint.py:218-388): 2D Taylor-Green
+    # on [-1, 1]^2 with the exact decaying solution as Dirichlet data (nonzero
+    # normal flux and rotational boundary terms), BDF2/EXT2
+    proj = dict(name="tgv2d_box_p4", counts=(4, 4), p=4, k=2, dt=0.05, nu=0.05, steps=4,
+                perturb=0.05)
+    m = mesh.perturb_mesh(mesh.cartesian_mesh(proj["counts"], lows=(-1.0, -1.0),
+                                              highs=(1.0, 1.0)), proj["perturb"], seed=11)
+    vs = fespace.FESpace(m, proj["p"], vdim=2)
+    ps = fespace.FESpace(m, proj["p"])
+    geom = mesh.compute_geometric_factors(m, vs.basis.quad)
+    g = tgv2d_exact(proj["nu"])
+    st = timeint.ProjectionStepper(vs, ps, geom, k=proj["k"], dt=proj["dt"], nu=proj["nu"],
+                                   dirichlet=g)
+    u0 = vs.project(lambda x: g(x, 0.0))
+    st.initialize(u0)
+    its = []
+    for _ in range(proj["steps"]):
+        r = st.step()
+        its.append([r.mass_iters, r.pressure_iters, r.helmholtz_iters])
+    out["tgv2d_box_p4/u0"] = u0
+    out["tgv2d_box_p4/u"] = st.u
+    out["tgv2d_box_p4/p"] = st.p
+    np.savez_compressed(os.path.join(HERE, "boundary.npz"), **out)
+    return {"boundary": cases, "projection_bounded": [dict(proj, counts=list(proj["counts"]),
+                                                          iterations=its)]}
+
+
 GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers, "stokes": make_stokes,
-          "extras": make_extras}
+          "extras": make_extras, "boundary": make_boundary}
 
 
 def main(argv):
