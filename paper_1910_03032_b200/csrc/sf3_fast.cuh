@@ -443,13 +443,16 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           if (comp == 0) mbar_wait(smem_u32(&bars[Sh::NSTAGE]), uint32_t(it & 1));
         }
         auto ldf = [&](const double* p_) { return Sh::FSTAGE ? *p_ : __ldg(p_); };
+        // factors from L2 (no staging): more points per unrolled step keep
+        // more loads in flight against the L2 latency
+        constexpr int P5U = Sh::FSTAGE ? 2 : ((Q == 9) ? 5 : 2);  // p = 7 +3 %; p = 8 loses to register pressure
 #pragma unroll 1
         for (int L = tid; L < nel * Q2; L += NT) {
           const int el = L / Q2, ba = L - el * Q2;
           double* col = smem + el * ES + IX(0, ba / Q, ba % Q);
           const double* __restrict__ f =
               Sh::FSTAGE ? fsm + el * FACP + ba : P.fac + (e0 + el) * FACP + ba;
-#pragma unroll 2
+#pragma unroll P5U
           for (int c = 0; c < Q; ++c) {
             const double* fc = f + c * Q2;
             double* pt = col + c * YP;
