@@ -54,6 +54,7 @@ struct fb_blockilu {
   fb::DevBuf<int> new2old;    // new -> original DoF index
   TriPart L, U, Ut, Lt;       // forward: L (unit) then U; backward: U^T then L^T (unit)
   int ell_w = 0;              // padded-row width of all parts (0: CSR sweeps)
+  int max_grp = 0;            // most level groups of one block over the four parts
 };
 
 static int build_ell(fb_blockilu* B);
@@ -288,19 +289,34 @@ __device__ __forceinline__ void block_tri_quad(const TriView& T, bool live, int 
   }
 }
 
+// One block's shared-memory region (bytes): y (8 B per row), the level-group
+// offsets (max_grp + 1 ints: sized by the deepest block, not by its rows),
+// the row entry offsets (CSR sweep only, 4 B per row) and the level-ordered
+// local rows (2 B per row).  Smaller regions keep more blocks resident per SM
+// (the sweeps are latency bound).  max_grp < 0: unknown, size by rows.
+__host__ __device__ inline size_t block_ilu_smem(int max_block, int max_grp = -1) {
+  const size_t g = size_t(max_grp >= 0 ? max_grp : max_block) + 1;
+  return (size_t(max_block) * 14 + 4 * g + 4 + 15) / 16 * 16;
+}
+__host__ __device__ inline size_t block_ilu_ell_smem(int max_block, int max_grp = -1) {
+  const size_t g = size_t(max_grp >= 0 ? max_grp : max_block) + 1;
+  return (size_t(max_block) * 10 + 4 * g + 15) / 16 * 16;
+}
+
 template <int LPB, bool PIPE>
 __global__ void __launch_bounds__(32) block_ilu_kernel(const int* __restrict__ block_ptr,
                                                        int nblocks,
                                                        const int* __restrict__ new2old,
                                                        TriView A, TriView B,
                                                        const double* __restrict__ r,
-                                                       double* __restrict__ out, int max_block) {
+                                                       double* __restrict__ out, int max_block,
+                                                       int max_grp) {
   extern __shared__ double smem_d[];
   const int j = threadIdx.x / LPB, t = threadIdx.x % LPB;
-  const size_t per = (size_t(max_block) * 18 + 16 + 15) / 16 * 2;  // doubles per block region
+  const size_t per = block_ilu_smem(max_block, max_grp) / 8;  // doubles per block region
   double* y = smem_d + j * per;
   int* sgrp = reinterpret_cast<int*>(y + max_block);
-  int* soff = sgrp + max_block + 1;
+  int* soff = sgrp + max_grp + 1;
   unsigned short* srow = reinterpret_cast<unsigned short*>(soff + max_block + 1);
   const int b = blockIdx.x * (32 / LPB) + j;
   const bool live = b < nblocks;
@@ -415,13 +431,13 @@ __global__ void __launch_bounds__(32) block_ilu_ell_kernel(const int* __restrict
                                                            TriView A, TriView B,
                                                            const double* __restrict__ r,
                                                            double* __restrict__ out,
-                                                           int max_block) {
+                                                           int max_block, int max_grp) {
   extern __shared__ double smem_d[];
   const int j = threadIdx.x / LPB, t = threadIdx.x % LPB;
-  const size_t per = (size_t(max_block) * 14 + 16 + 15) / 16 * 2;  // doubles per block region
+  const size_t per = block_ilu_ell_smem(max_block, max_grp) / 8;  // doubles per block region
   double* y = smem_d + j * per;
   int* sgrp = reinterpret_cast<int*>(y + max_block);
-  unsigned short* srow = reinterpret_cast<unsigned short*>(sgrp + max_block + 1);
+  unsigned short* srow = reinterpret_cast<unsigned short*>(sgrp + max_grp + 1);
   const int b = blockIdx.x * (32 / LPB) + j;
   const bool live = b < nblocks;
   const int bs = live ? block_ptr[b] : 0, be = live ? block_ptr[b + 1] : 0;
@@ -432,9 +448,6 @@ __global__ void __launch_bounds__(32) block_ilu_ell_kernel(const int* __restrict
   for (int i = t; i < be - bs; i += LPB) out[new2old ? new2old[bs + i] : bs + i] = y[i];
 }
 
-inline size_t block_ilu_ell_smem(int max_block) {
-  return (size_t(max_block) * 14 + 16 + 15) / 16 * 16;
-}
 
 __global__ void ell_rowlen_kernel(int64_t n, const int64_t* __restrict__ ip, int* __restrict__ mx) {
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -461,9 +474,6 @@ __global__ void ell_fill_kernel(int64_t n, int nblocks, const int* __restrict__ 
   }
 }
 
-inline size_t block_ilu_smem(int max_block) {
-  return (size_t(max_block) * 18 + 16 + 15) / 16 * 16;  // one block's region
-}
 
 // lanes per block: small blocks (p <= 2 levels, ~1.5 rows per dependency
 // level) share a warp 16 ways; larger blocks are smem-bound (18 B per row)
@@ -480,9 +490,9 @@ int launch_block_ilu(const fb_blockilu* B, TriView a, TriView b, const double* r
     configured = true;
   }
   constexpr int BPW = 32 / LPB;
-  const size_t smem = block_ilu_smem(B->max_block) * BPW;
+  const size_t smem = block_ilu_smem(B->max_block, B->max_grp) * BPW;
   block_ilu_kernel<LPB, PIPE><<<(B->nblocks + BPW - 1) / BPW, 32, smem, st>>>(
-      B->block_ptr.ptr, B->nblocks, B->new2old.ptr, a, b, r, out, B->max_block);
+      B->block_ptr.ptr, B->nblocks, B->new2old.ptr, a, b, r, out, B->max_block, B->max_grp);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
@@ -802,9 +812,9 @@ int launch_ell(const fb_blockilu* B, TriView a, TriView b, const double* r, doub
     configured = true;
   }
   constexpr int BPW = 32 / LPB;
-  const size_t smem = block_ilu_ell_smem(B->max_block) * BPW;
+  const size_t smem = block_ilu_ell_smem(B->max_block, B->max_grp) * BPW;
   block_ilu_ell_kernel<LPB, W><<<(B->nblocks + BPW - 1) / BPW, 32, smem, st>>>(
-      B->block_ptr.ptr, B->nblocks, B->new2old.ptr, a, b, r, out, B->max_block);
+      B->block_ptr.ptr, B->nblocks, B->new2old.ptr, a, b, r, out, B->max_block, B->max_grp);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
@@ -858,6 +868,20 @@ extern "C" {
 // F: the block-diagonal ILU(0) factor in the new (block-major) numbering, as
 // CSR with sorted columns (strict lower part = L, unit diagonal implied;
 // upper part incl. diagonal = U).  block_ptr: (nblocks+1) row offsets.
+// deepest level schedule of one block over the four triangular parts
+static int compute_max_grp(fb_blockilu* B) {
+  int mg = 0;
+  std::vector<int> h(size_t(B->nblocks) + 1);
+  for (const TriPart* P : {&B->L, &B->U, &B->Ut, &B->Lt}) {
+    if (P->blk_grp.n < B->nblocks + 1) continue;
+    FB_TRY_CUDA(cudaMemcpy(h.data(), P->blk_grp.ptr, h.size() * sizeof(int),
+                           cudaMemcpyDeviceToHost));
+    for (int b = 0; b < B->nblocks; ++b) mg = std::max(mg, h[b + 1] - h[b]);
+  }
+  B->max_grp = mg;
+  return FB_OK;
+}
+
 // new2old: new -> original DoF index.
 int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
                        const int64_t* new2old, const int64_t* indptr, const int64_t* indices,
@@ -909,6 +933,10 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
   if (g_bilu_pipe == 2) {
     const int rc_ell = build_ell(B.get());
     if (rc_ell != FB_OK) return rc_ell;
+  }
+  {
+    const int rc_g = compute_max_grp(B.get());
+    if (rc_g != FB_OK) return rc_g;
   }
   *out = B.release();
   return FB_OK;
@@ -1155,6 +1183,10 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
     if (rc_ell != FB_OK) return rc_ell;
   }
   debug_canary_register(B->block_ptr.ptr, int(nblocks + 1));  // FB_DEBUG_SYNC=1 only
+  {
+    const int rc_g = compute_max_grp(B.get());
+    if (rc_g != FB_OK) return rc_g;
+  }
   *out = B.release();  // new2old stays empty: the level is block-major already
   return FB_OK;
 }
