@@ -354,6 +354,84 @@ def lor_pcg_sharded(rank, world, cases=((4, 116, 16), (7, 66, 8)), c=C_HELM):
 METRIC = "fp64 GDoF/s of sum-factorized Helmholtz apply vs p (3D, p=1..8, ~10M DoFs each)"
 
 
+def callers(stokes_cases=((2, 2), (2, 4), (2, 6), (3, 2)), tgv=(5, 16, 4)):
+    """Device time of the cfg4 / cfg5 callers: the
+    lid-driven Stokes cavity by FGMRES with the block-triangular
+    preconditioner (Taylor-Hood, rel_tol 1e-8; iteration counts beside the
+    reference's from tests/golden/manifest.json), and projection steps of the
+    periodic 3D Taylor-Green vortex (p, cells per direction, steps)."""
+    import torch
+    from paper_1910_03032_b200 import geometry, solvers, spaces, stokes, timeint
+    man = {}
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden",
+                               "manifest.json")) as f:
+            man = {c["name"]: c for c in json.load(f).get("stokes", [])}
+    except OSError:
+        pass
+
+    def lid(X):
+        out = np.zeros_like(X)
+        out[np.abs(X[:, 1] - 1.0) < 1e-12, 0] = 1.0
+        return out
+
+    out = {}
+    for d, p in stokes_cases:
+        counts = (8, 8) if d == 2 else (3, 3, 3)
+        m = geometry.cartesian_mesh(counts)
+        vs = spaces.FESpace(m, p, vdim=d)
+        ps = spaces.FESpace(m, p - 1)
+        geom = geometry.compute_geometric_factors(m, vs.basis.quad)
+        t0 = time.perf_counter()
+        S = stokes.StokesSystem(vs, ps, geom, nu=1.0)
+        setup = time.perf_counter() - t0
+        cfg = solvers.SolverConfig(rel_tol=1e-8, max_iters=200)
+        S.solve(g=lid, config=cfg)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, rep = S.solve(g=lid, config=cfg)
+        torch.cuda.synchronize()
+        ms = 1e3 * (time.perf_counter() - t0)
+        ref = man.get(f"cav{d}d_p{p}", {})
+        out[f"stokes_cavity_{d}d_p{p}"] = {
+            "dofs": int(vs.ndofs + ps.ndofs), "iterations": rep.iterations,
+            "reference_iterations": ref.get("iterations"), "solve_ms": round(ms, 2),
+            "setup_s": round(setup, 2), "timing": "host wall clock around StokesSystem.solve "
+            "(host numpy in/out), after one warm-up solve"}
+    p, n, steps = tgv
+    m = geometry.cartesian_mesh((n, n, n), lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                                periodic=(True,) * 3)
+    vs = spaces.FESpace(m, p, vdim=3)
+    ps = spaces.FESpace(m, p)
+    geom = geometry.compute_geometric_factors(m, vs.basis.quad)
+    t0 = time.perf_counter()
+    st = timeint.ProjectionStepper(vs, ps, geom, k=3, dt=0.02, nu=1.0 / 1600.0)
+
+    def tgv_u(x):
+        X, Y, Z = x[:, 0], x[:, 1], x[:, 2]
+        return np.stack([np.sin(X) * np.cos(Y) * np.cos(Z), -np.cos(X) * np.sin(Y) * np.cos(Z),
+                         np.zeros_like(X)], axis=1)
+
+    st.initialize(vs.project(tgv_u))
+    for _ in range(3):  # BDF1..3 start-up: each new order builds its Helmholtz LOR hierarchy
+        st.step()
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    its = []
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = st.step()
+        its.append([r.mass_iters, r.pressure_iters, r.helmholtz_iters])
+    torch.cuda.synchronize()
+    ms = 1e3 * (time.perf_counter() - t0) / steps
+    out[f"tgv3d_projection_p{p}_{n}^3"] = {
+        "velocity_dofs": int(vs.ndofs), "pressure_dofs": int(ps.ndofs), "ms_per_step": round(ms, 2),
+        "steps": steps, "iterations_mass_pressure_helmholtz": its, "setup_s": round(setup, 2),
+        "kinetic_energy": st.kinetic_energy(),
+        "scheme": "BDF3/EXT3, dt 0.02, nu 1/1600; timed after the 3 start-up steps (setup_s)"}
+    return out
+
+
 def config_block(world):
     return {"workload": "cfg2-shape 3D Helmholtz apply sweep p=1..8, ~10M DoFs per degree, "
                         "perturbed unit-cube hex mesh, n_q=p+2 Gauss-Legendre, stored factors",
@@ -554,6 +632,11 @@ def run_ours(args, rank, world):
         line["lor_pcg"] = lor_pcg()
     if sharded is not None:
         line["lor_pcg_cfg3_sharded"] = sharded
+    if not args.no_callers and world == 1:
+        try:
+            line["callers"] = callers()
+        except Exception as exc:  # a caller failure must not drop the headline line
+            line["callers"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if not args.no_cfg3 and world == 1:
         import gc
         import torch
@@ -577,6 +660,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--no-cfg3", action="store_true", help="skip the 100M-DoF LOR-PCG solves")
+    ap.add_argument("--no-callers", action="store_true", help="skip the cfg4/cfg5 caller timings")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

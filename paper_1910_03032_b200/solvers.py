@@ -828,6 +828,21 @@ class LORPreconditioner(_DeviceMixin):
         sm.backward_into(t, t2, st)
         vec.axpby(1.0, t2, 1.0, x, st)
 
+    def clone_workspace(self):
+        """A view of this preconditioner (same matrices, smoothers and coarse
+        inverse) with its own level vectors, so several can run concurrently
+        on different streams; None when a shared handle keeps state between
+        launches (the global ILU's graphs, a sparse-LU coarse solve)."""
+        import copy
+        if self.smoother_kind != "block" or not isinstance(self._bottom, DenseInverseSolver):
+            return None
+        c = copy.copy(self)
+        c._x = [dev.empty(t.shape[0]) for t in self._x]
+        c._r = [dev.empty(t.shape[0]) for t in self._r]
+        c._t = [dev.empty(t.shape[0]) for t in self._t]
+        c._t2 = [dev.empty(t.shape[0]) for t in self._t2]
+        return c
+
     def apply_into(self, r, out, stream=None):
         st = dev.stream_handle() if stream is None else stream
         rr = r
@@ -848,9 +863,29 @@ class BlockDiagonalPreconditioner(_DeviceMixin):
         self.vdim = vdim
         self.ns = ndofs_scalar
         self._apply = _device_apply(scalar_precond)
+        # components are independent: with per-component workspaces the
+        # (latency-bound) V-cycles run concurrently on their own streams
+        self._par = None
+        if vdim > 1 and hasattr(scalar_precond, "clone_workspace"):
+            clones = [scalar_precond.clone_workspace() for _ in range(vdim - 1)]
+            if all(c is not None for c in clones) and torch.cuda.is_available():
+                self._par = [scalar_precond] + clones
+                self._streams = [torch.cuda.Stream(device=dev.device()) for _ in range(vdim)]
+                self._done = [torch.cuda.Event() for _ in range(vdim)]
+                self._fork = torch.cuda.Event()
 
     def apply_into(self, r, out, stream=None):
         ns = self.ns
+        if self._par is not None and stream is None:
+            cur = torch.cuda.current_stream()
+            self._fork.record(cur)
+            for c, (pc, s) in enumerate(zip(self._par, self._streams)):
+                s.wait_event(self._fork)
+                pc.apply_into(r[c * ns:(c + 1) * ns], out[c * ns:(c + 1) * ns], s.cuda_stream)
+                self._done[c].record(s)
+            for e in self._done:
+                cur.wait_event(e)
+            return out
         for c in range(self.vdim):
             self._apply(r[c * ns:(c + 1) * ns], out[c * ns:(c + 1) * ns])
         return out
