@@ -14,6 +14,7 @@
 // scatters the result.  The chain per block is ~89 (p=4) - 131 (p=7) levels
 // regardless of the problem size, and blocks never talk to each other, so the
 // sweep also shards across GPUs with identical math.
+#include <cstdlib>
 #include <algorithm>
 #include <memory>
 #include <vector>
@@ -45,6 +46,7 @@ struct TriPart {
 
 static int g_bilu_pipe = 2;  // 0: CSR sweep, 1: CSR + next-level loads, 2: padded rows for large blocks, else 1
 static int g_bilu_lanes = 0;  // 0 = by block size
+static int g_bilu_deep = 1;   // two-level lookahead for one-wave grids (0: off)
 
 struct fb_blockilu {
   int64_t n = 0;
@@ -132,7 +134,7 @@ __device__ __forceinline__ void row_finish(const TriView& T, const RowLoad& R, i
 // in shared memory and its factor entries prefetched into L2; with PIPE the
 // loads of level g+1 are issued before level g computes.  Every row's sum
 // stays sequential in index order (bitwise the host sweep).
-template <int LPB, bool PIPE>
+template <int LPB, int PIPE>
 __device__ __forceinline__ void block_tri(const TriView& T, bool live, int b, int bs, int nb,
                                           double* y, int* sgrp, unsigned short* srow,
                                           int* soff) {
@@ -156,7 +158,29 @@ __device__ __forceinline__ void block_tri(const TriView& T, bool live, int b, in
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) Gmax = max(Gmax, __shfl_xor_sync(0xffffffffu, Gmax, o));
   __syncwarp();
-  if constexpr (PIPE) {
+  if constexpr (PIPE == 2) {
+    // two levels ahead (small grids, one wave: latency, not occupancy, bounds
+    // the sweep): rows of level g+2 load while level g computes
+    RowLoad cur, n1, n2;
+    if (G > 0 && t < sgrp[1] - sgrp[0]) row_issue(T, srow, soff, ebase, bs, sgrp[0] + t, cur);
+    if (G > 1 && t < sgrp[2] - sgrp[1]) row_issue(T, srow, soff, ebase, bs, sgrp[1] + t, n1);
+    for (int g = 0; g < Gmax; ++g) {
+      if (g < G) {
+        const int r0 = sgrp[g], r1 = sgrp[g + 1];
+        const bool nx = g + 2 < G && t < sgrp[g + 3] - sgrp[g + 2];
+        if (nx) row_issue(T, srow, soff, ebase, bs, sgrp[g + 2] + t, n2);
+        if (t < r1 - r0) row_finish(T, cur, bs, y);
+        for (int k = r0 + t + LPB; k < r1; k += LPB) {  // levels wider than LPB
+          RowLoad w;
+          row_issue(T, srow, soff, ebase, bs, k, w);
+          row_finish(T, w, bs, y);
+        }
+        cur = n1;
+        n1 = n2;
+      }
+      __syncwarp();
+    }
+  } else if constexpr (PIPE == 1) {
     RowLoad cur, nxt;
     if (G > 0 && t < sgrp[1] - sgrp[0]) row_issue(T, srow, soff, ebase, bs, sgrp[0] + t, cur);
     for (int g = 0; g < Gmax; ++g) {
@@ -303,7 +327,7 @@ __host__ __device__ inline size_t block_ilu_ell_smem(int max_block, int max_grp 
   return (size_t(max_block) * 10 + 4 * g + 15) / 16 * 16;
 }
 
-template <int LPB, bool PIPE>
+template <int LPB, int PIPE>
 __global__ void __launch_bounds__(32) block_ilu_kernel(const int* __restrict__ block_ptr,
                                                        int nblocks,
                                                        const int* __restrict__ new2old,
@@ -386,7 +410,7 @@ __device__ __forceinline__ void ell_finish(const TriView& T, const EllRow<W>& R,
   y[R.row - bs] = T.invdiag ? __dmul_rn(r, R.inv) : r;
 }
 
-template <int LPB, int W>
+template <int LPB, int W, int D = 1>
 __device__ __forceinline__ void block_tri_ell(const TriView& T, bool live, int b, int bs, int nb,
                                               double* y, int* sgrp, unsigned short* srow) {
   const int t = threadIdx.x % LPB;
@@ -405,6 +429,28 @@ __device__ __forceinline__ void block_tri_ell(const TriView& T, bool live, int b
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) Gmax = max(Gmax, __shfl_xor_sync(0xffffffffu, Gmax, o));
   __syncwarp();
+  if constexpr (D == 2) {  // two levels ahead (see block_tri)
+    EllRow<W> cur, n1, n2;
+    if (G > 0 && t < sgrp[1] - sgrp[0]) ell_issue<W>(T, srow, bs, sgrp[0] + t, cur);
+    if (G > 1 && t < sgrp[2] - sgrp[1]) ell_issue<W>(T, srow, bs, sgrp[1] + t, n1);
+    for (int g = 0; g < Gmax; ++g) {
+      if (g < G) {
+        const int r0 = sgrp[g], r1 = sgrp[g + 1];
+        const bool nx = g + 2 < G && t < sgrp[g + 3] - sgrp[g + 2];
+        if (nx) ell_issue<W>(T, srow, bs, sgrp[g + 2] + t, n2);
+        if (t < r1 - r0) ell_finish<W>(T, cur, bs, y);
+        for (int k = r0 + t + LPB; k < r1; k += LPB) {
+          EllRow<W> w;
+          ell_issue<W>(T, srow, bs, k, w);
+          ell_finish<W>(T, w, bs, y);
+        }
+        cur = n1;
+        n1 = n2;
+      }
+      __syncwarp();
+    }
+    return;
+  }
   EllRow<W> cur, nxt;
   if (G > 0 && t < sgrp[1] - sgrp[0]) ell_issue<W>(T, srow, bs, sgrp[0] + t, cur);
   for (int g = 0; g < Gmax; ++g) {
@@ -424,7 +470,7 @@ __device__ __forceinline__ void block_tri_ell(const TriView& T, bool live, int b
   }
 }
 
-template <int LPB, int W>
+template <int LPB, int W, int D = 1>
 __global__ void __launch_bounds__(32) block_ilu_ell_kernel(const int* __restrict__ block_ptr,
                                                            int nblocks,
                                                            const int* __restrict__ new2old,
@@ -443,8 +489,8 @@ __global__ void __launch_bounds__(32) block_ilu_ell_kernel(const int* __restrict
   const int bs = live ? block_ptr[b] : 0, be = live ? block_ptr[b + 1] : 0;
   for (int i = t; i < be - bs; i += LPB) y[i] = r[new2old ? new2old[bs + i] : bs + i];
   __syncwarp();
-  block_tri_ell<LPB, W>(A, live, b, bs, be - bs, y, sgrp, srow);
-  block_tri_ell<LPB, W>(B, live, b, bs, be - bs, y, sgrp, srow);
+  block_tri_ell<LPB, W, D>(A, live, b, bs, be - bs, y, sgrp, srow);
+  block_tri_ell<LPB, W, D>(B, live, b, bs, be - bs, y, sgrp, srow);
   for (int i = t; i < be - bs; i += LPB) out[new2old ? new2old[bs + i] : bs + i] = y[i];
 }
 
@@ -480,7 +526,7 @@ __global__ void ell_fill_kernel(int64_t n, int nblocks, const int* __restrict__ 
 // and run one per warp (measured, tools/box_profile.py)
 inline int block_ilu_lanes(int max_block) { return max_block <= 160 ? 2 : 32; }
 
-template <int LPB, bool PIPE>
+template <int LPB, int PIPE>
 int launch_block_ilu(const fb_blockilu* B, TriView a, TriView b, const double* r, double* out,
                      cudaStream_t st) {
   static bool configured = false;
@@ -802,27 +848,44 @@ TriView view(const TriPart& P, bool unit) {
 
 namespace {
 
-template <int LPB, int W>
+template <int LPB, int W, int D = 1>
 int launch_ell(const fb_blockilu* B, TriView a, TriView b, const double* r, double* out,
                cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_ell_kernel<LPB, W>,
+    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_ell_kernel<LPB, W, D>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
   constexpr int BPW = 32 / LPB;
   const size_t smem = block_ilu_ell_smem(B->max_block, B->max_grp) * BPW;
-  block_ilu_ell_kernel<LPB, W><<<(B->nblocks + BPW - 1) / BPW, 32, smem, st>>>(
+  block_ilu_ell_kernel<LPB, W, D><<<(B->nblocks + BPW - 1) / BPW, 32, smem, st>>>(
       B->block_ptr.ptr, B->nblocks, B->new2old.ptr, a, b, r, out, B->max_block, B->max_grp);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
 
+// one-warp sweeps of a grid that fits one wave (<= 8 blocks per SM): the
+// level latency, not occupancy, bounds them, so load two levels ahead
+inline bool small_grid(const fb_blockilu* B) {
+  static int sms = 0;
+  if (sms == 0) {
+    const char* env = getenv("FB_BILU_DEEP");  // A/B switch for tools/box_profile.py
+    if (env && env[0] == '0') g_bilu_deep = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  return g_bilu_deep != 0 && B->nblocks <= 8 * sms;
+}
+
 template <int W>
 int launch_ell_w(const fb_blockilu* B, int lanes, TriView a, TriView b, const double* r,
                  double* out, cudaStream_t st) {
-  return lanes == 2 ? launch_ell<2, W>(B, a, b, r, out, st) : launch_ell<32, W>(B, a, b, r, out, st);
+  if (lanes == 2) return launch_ell<2, W>(B, a, b, r, out, st);
+  return small_grid(B) ? launch_ell<32, W, 2>(B, a, b, r, out, st)
+                       : launch_ell<32, W>(B, a, b, r, out, st);
 }
 
 }  // namespace
@@ -973,7 +1036,9 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
     case 4: return pipe ? launch_block_ilu<4, true>(B, a, b, r, out, st) : launch_block_ilu<4, false>(B, a, b, r, out, st);
     case 8: return pipe ? launch_block_ilu<8, true>(B, a, b, r, out, st) : launch_block_ilu<8, false>(B, a, b, r, out, st);
     case 16: return pipe ? launch_block_ilu<16, true>(B, a, b, r, out, st) : launch_block_ilu<16, false>(B, a, b, r, out, st);
-    default: return pipe ? launch_block_ilu<32, true>(B, a, b, r, out, st) : launch_block_ilu<32, false>(B, a, b, r, out, st);
+    default:
+      if (pipe && small_grid(B)) return launch_block_ilu<32, 2>(B, a, b, r, out, st);
+      return pipe ? launch_block_ilu<32, true>(B, a, b, r, out, st) : launch_block_ilu<32, false>(B, a, b, r, out, st);
   }
 }
 
