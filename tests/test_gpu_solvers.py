@@ -140,3 +140,25 @@ def test_block_ilu_is_exact_on_single_block_and_dense_coarse():
     x_ref = spla.spsolve(Ac.tocsc(), r)
     assert rel_err(solvers.DenseInverseSolver(Ac).solve(r), x_ref) < 1e-10
     assert rel_err(solvers.SparseLUSolver(Ac).solve(r), x_ref) < 1e-10
+
+
+def test_block_diagonal_concurrent_components_equal_sequential():
+    """Per-component V-cycles on their own streams (clone_workspace) give
+    bitwise the sequential result."""
+    import torch
+
+    from paper_1910_03032_b200 import geometry, solvers, spaces
+    m = geometry.perturb_mesh(geometry.cartesian_mesh((4, 4, 3)), 0.05, seed=1)
+    sp = spaces.FESpace(m, 3)
+    cyc = solvers.LORPreconditioner(sp, "helmholtz", c=10.0, dirichlet_attrs="all")
+    P = solvers.BlockDiagonalPreconditioner(cyc, 3, sp.ndofs_scalar)
+    assert P._par is not None
+    r = torch.from_numpy(np.random.default_rng(4).standard_normal(3 * sp.ndofs_scalar)).cuda()
+    z1 = torch.empty_like(r)
+    P.apply_into(r, z1)
+    par, P._par = P._par, None
+    z0 = torch.empty_like(r)
+    P.apply_into(r, z0)
+    P._par = par
+    torch.cuda.synchronize()
+    assert torch.equal(z0, z1)
