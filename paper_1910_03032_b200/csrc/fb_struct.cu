@@ -266,6 +266,10 @@ __device__ __forceinline__ bool owned_local(const int64_t ec[3], int l0, int l1,
 // One warp per fine element, kTE elements per CTA.
 constexpr int kTE = 4;
 
+// NF / NC > 0: compile-time sizes of the common ladder pairs (fully unrolled
+// contractions, constant index arithmetic); 0: runtime sizes.  Same
+// summation order either way.
+template <int NF, int NC>
 __global__ void __launch_bounds__(32 * kTE) transfer_prolong_kernel(TransferView T, int64_t ne,
                                                                     const double* __restrict__ xc,
                                                                     double* __restrict__ xf) {
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(32 * kTE) transfer_prolong_kernel(TransferView
   int64_t ec[3];
   const double* Wa[3];
   transfer_elem(T, e, ec, Wa);
-  const int nc = T.nc, nf = T.nf;
+  const int nc = NC > 0 ? NC : T.nc, nf = NF > 0 ? NF : T.nf;
   const int nc3 = nc * nc * nc, nf3 = nf * nf * nf;
   for (int j = lane; j < nc3; j += 32) xe[j] = __ldg(xc + __ldg(T.hmap + e * nc3 + j));
   for (int j = lane; j < nf * nc; j += 32)
@@ -289,10 +293,13 @@ __global__ void __launch_bounds__(32 * kTE) transfer_prolong_kernel(TransferView
     const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
     if (!owned_local(ec, l0, l1, l2)) continue;
     double acc = 0.0;
+#pragma unroll
     for (int c = 0; c < nc; ++c) {
       double ab = 0.0;
+#pragma unroll
       for (int b = 0; b < nc; ++b) {
         double aa = 0.0;
+#pragma unroll
         for (int a = 0; a < nc; ++a) aa += w[0][l0 * nc + a] * xe[(c * nc + b) * nc + a];
         ab += w[1][l1 * nc + b] * aa;
       }
@@ -302,6 +309,7 @@ __global__ void __launch_bounds__(32 * kTE) transfer_prolong_kernel(TransferView
   }
 }
 
+template <int NF, int NC>
 __global__ void __launch_bounds__(32 * kTE) transfer_restrict_kernel(TransferView T, int64_t ne,
                                                                      const double* __restrict__ xf,
                                                                      double* __restrict__ E) {
@@ -315,7 +323,7 @@ __global__ void __launch_bounds__(32 * kTE) transfer_restrict_kernel(TransferVie
   int64_t ec[3];
   const double* Wa[3];
   transfer_elem(T, e, ec, Wa);
-  const int nc = T.nc, nf = T.nf;
+  const int nc = NC > 0 ? NC : T.nc, nf = NF > 0 ? NF : T.nf;
   const int nc3 = nc * nc * nc, nf3 = nf * nf * nf;
   for (int l = lane; l < nf3; l += 32) {
     const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
@@ -327,10 +335,13 @@ __global__ void __launch_bounds__(32 * kTE) transfer_restrict_kernel(TransferVie
   for (int j = lane; j < nc3; j += 32) {
     const int j0 = j % nc, j1 = (j / nc) % nc, j2 = j / (nc * nc);
     double acc = 0.0;
+#pragma unroll 1  // rolled: the fully unrolled nf^3 body thrashes the instruction cache at nf = 8
     for (int l2 = 0; l2 < nf; ++l2) {
       double s1 = 0.0;
+#pragma unroll
       for (int l1 = 0; l1 < nf; ++l1) {
         double s0 = 0.0;
+#pragma unroll
         for (int l0 = 0; l0 < nf; ++l0) s0 += w[0][l0 * nc + j0] * rf[(l2 * nf + l1) * nf + l0];
         s1 += w[1][l1 * nc + j1] * s0;
       }
@@ -492,14 +503,44 @@ static TransferView transfer_view(const fb_transfer* T) {
                       T->origin[2], T->nf, T->nc};
 }
 
+}  // extern "C"
+
+template <bool PROLONG, int NF, int NC>
+static int launch_transfer_t(const fb_transfer* T, const double* in, double* out,
+                             cudaStream_t st) {
+  if (PROLONG)
+    transfer_prolong_kernel<NF, NC><<<ceil_div(T->ne, kTE), 32 * kTE, 0, st>>>(transfer_view(T),
+                                                                               T->ne, in, out);
+  else
+    transfer_restrict_kernel<NF, NC><<<ceil_div(T->ne, kTE), 32 * kTE, 0, st>>>(transfer_view(T),
+                                                                                T->ne, in, out);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+// the degree ladder p -> ceil(p/2) (p = 2..8) and the Q1 h-coarsening levels
+template <bool PROLONG>
+static int launch_transfer(const fb_transfer* T, const double* in, double* out, cudaStream_t st) {
+  switch (T->nf * 16 + T->nc) {
+    case 2 * 16 + 2: return launch_transfer_t<PROLONG, 2, 2>(T, in, out, st);
+    case 3 * 16 + 2: return launch_transfer_t<PROLONG, 3, 2>(T, in, out, st);
+    case 4 * 16 + 3: return launch_transfer_t<PROLONG, 4, 3>(T, in, out, st);
+    case 5 * 16 + 3: return launch_transfer_t<PROLONG, 5, 3>(T, in, out, st);
+    case 6 * 16 + 4: return launch_transfer_t<PROLONG, 6, 4>(T, in, out, st);
+    case 7 * 16 + 4: return launch_transfer_t<PROLONG, 7, 4>(T, in, out, st);
+    case 8 * 16 + 5: return launch_transfer_t<PROLONG, 8, 5>(T, in, out, st);
+    case 9 * 16 + 5: return launch_transfer_t<PROLONG, 9, 5>(T, in, out, st);
+    default: return launch_transfer_t<PROLONG, 0, 0>(T, in, out, st);
+  }
+}
+
+extern "C" {
+
 // xf (fine L-vector) = P xc: every fine DoF written once, by its owner element
 int fb_transfer_prolong(const fb_transfer* T, const double* xc, double* xf, void* stream) {
   FB_REQUIRE(T != nullptr, "transfer is NULL");
   if (T->ne == 0) return FB_OK;
-  transfer_prolong_kernel<<<ceil_div(T->ne, kTE), 32 * kTE, 0, as_stream(stream)>>>(
-      transfer_view(T), T->ne, xc, xf);
-  FB_CHECK_LAUNCH();
-  return FB_OK;
+  return launch_transfer<true>(T, xc, xf, as_stream(stream));
 }
 
 // xc (coarse L-vector) = P^T xf, deterministic (per-element contributions,
@@ -507,9 +548,8 @@ int fb_transfer_prolong(const fb_transfer* T, const double* xc, double* xf, void
 int fb_transfer_restrict(const fb_transfer* T, const double* xf, double* xc, void* stream) {
   FB_REQUIRE(T != nullptr, "transfer is NULL");
   if (T->ne == 0) return FB_OK;
-  transfer_restrict_kernel<<<ceil_div(T->ne, kTE), 32 * kTE, 0, as_stream(stream)>>>(
-      transfer_view(T), T->ne, xf, T->E.ptr);
-  FB_CHECK_LAUNCH();
+  const int rc = launch_transfer<false>(T, xf, T->E.ptr, as_stream(stream));
+  if (rc != FB_OK) return rc;
   return fb_restriction_scatter_add(T->hmap, T->E.ptr, xc, stream);
 }
 
