@@ -189,6 +189,43 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* ptr, int64_t bytes)
   }
 }
 
+// L2 policy for data read exactly once per apply (the quadrature factors):
+// evict first, so the gathered x and the slot array S stay resident for
+// their reuse (neighbour elements, the E->L sum that follows)
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2_hint(const void* ptr, int64_t bytes,
+                                                      uint64_t pol) {
+  uintptr_t b = reinterpret_cast<uintptr_t>(ptr) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(ptr) + uintptr_t(bytes) + 15) & ~uintptr_t(15);
+  while (b < e) {
+    const uint32_t len = uint32_t((e - b) > (1u << 20) ? (1u << 20) : (e - b));
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(b),
+                 "r"(len), "l"(pol)
+                 : "memory");
+    b += len;
+  }
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes,
+                                              uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ double ld_evict_first(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -244,15 +281,16 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
     bulk_g2s(smem_u32(stage_map(s)), P.map + e0 * NLOCP, mbytes, bar);
     bulk_g2s(smem_u32(stage_pos(s)), P.spos + e0 * NBP, pbytes, bar);
   };
+  const uint64_t fpol = l2_evict_first_policy();
   auto prefetch_factors = [&](int batch) {
     const int64_t e0 = int64_t(batch) * NE;
     if constexpr (Sh::FSTAGE) {  // TMA copy of the whole factor block into shared memory
       const uint32_t bar = smem_u32(&bars[Sh::NSTAGE]);
       const uint32_t bytes = uint32_t(nel_of(batch)) * FACP * 8u;
       mbar_expect_tx(bar, bytes);
-      bulk_g2s(smem_u32(fsm), P.fac + e0 * FACP, bytes, bar);
+      bulk_g2s(smem_u32(fsm), P.fac + e0 * FACP, bytes, bar);  // (an evict-first hint here cost 6 % at p = 4)
     } else {
-      bulk_prefetch_l2(P.fac + e0 * FACP, int64_t(nel_of(batch)) * FACP * 8);
+      bulk_prefetch_l2_hint(P.fac + e0 * FACP, int64_t(nel_of(batch)) * FACP * 8, fpol);
     }
   };
   // all threads: cp.async gathers of component `comp` of `batch` into sx
@@ -442,7 +480,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         if constexpr (Sh::FSTAGE) {
           if (comp == 0) mbar_wait(smem_u32(&bars[Sh::NSTAGE]), uint32_t(it & 1));
         }
-        auto ldf = [&](const double* p_) { return Sh::FSTAGE ? *p_ : __ldg(p_); };
+        auto ldf = [&](const double* p_) { return Sh::FSTAGE ? *p_ : ld_evict_first(p_, fpol); };
         // factors from L2 (no staging): more points per unrolled step keep
         // more loads in flight against the L2 latency
         constexpr int P5U = Sh::FSTAGE ? 2 : ((Q == 9) ? 5 : 2);  // p = 7 +3 %; p = 8 loses to register pressure
@@ -607,7 +645,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         if constexpr (Sh::FSTAGE) {
           if (comp == 0) mbar_wait(smem_u32(&bars[Sh::NSTAGE]), uint32_t(it & 1));
         }
-        auto ldf = [&](const double* p_) { return Sh::FSTAGE ? *p_ : __ldg(p_); };
+        auto ldf = [&](const double* p_) { return Sh::FSTAGE ? *p_ : ld_evict_first(p_, fpol); };
 #pragma unroll 1
         for (int L = tid; L < nel * Q2; L += NT) {
           const int el = L / Q2, ba = L - el * Q2;
