@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(kQ1Threads, 4) sf3_q1_kernel(const __grid_cons
   constexpr int64_t kRowBytes = int64_t(3) * NK * 32 * 8;  // one 3-point row of the warp
   // lane 0 streams rows 0 and 1 of the warp's factor block into L2 now, and
   // row cb+2 while row cb is computed
-  if (lane == 0) bulk_prefetch_l2(fblk, 2 * kRowBytes);
+  const uint64_t fpol = l2_evict_first_policy();  // factors are read once: keep x resident
+  if (lane == 0) bulk_prefetch_l2_hint(fblk, 2 * kRowBytes, fpol);
   double* U = su + tid;
   double* V = sv + tid;
   int m[8], sl[8];
@@ -107,20 +108,23 @@ __global__ void __launch_bounds__(kQ1Threads, 4) sf3_q1_kernel(const __grid_cons
     for (int cb = 0; cb < 9; ++cb) {
       const int c = cb / 3, b = cb - 3 * c;
       if (lane == 0 && comp == 0 && cb + 2 < 9)
-        bulk_prefetch_l2(fblk + (cb + 2) * 3 * NK * 32, kRowBytes);
+        bulk_prefetch_l2_hint(fblk + (cb + 2) * 3 * NK * 32, kRowBytes, fpol);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const int q = cb * 3 + a;
         const double* fq = f + q * NK * 32;
         if (KIND == kMass) {
-          V[q * T] = __ldg(fq) * U[q * T];
+          V[q * T] = ld_evict_first(fq, fpol) * U[q * T];
           continue;
         }
         constexpr int o = (KIND == kHelm) ? 1 : 0;
-        const double w00 = __ldg(fq + (o + 0) * 32), w01 = __ldg(fq + (o + 1) * 32);
-        const double w02 = __ldg(fq + (o + 2) * 32), w11 = __ldg(fq + (o + 3) * 32);
-        const double w12 = __ldg(fq + (o + 4) * 32), w22 = __ldg(fq + (o + 5) * 32);
-        const double wm = (KIND == kHelm) ? __ldg(fq) : 0.0;
+        const double w00 = ld_evict_first(fq + (o + 0) * 32, fpol);
+        const double w01 = ld_evict_first(fq + (o + 1) * 32, fpol);
+        const double w02 = ld_evict_first(fq + (o + 2) * 32, fpol);
+        const double w11 = ld_evict_first(fq + (o + 3) * 32, fpol);
+        const double w12 = ld_evict_first(fq + (o + 4) * 32, fpol);
+        const double w22 = ld_evict_first(fq + (o + 5) * 32, fpol);
+        const double wm = (KIND == kHelm) ? ld_evict_first(fq, fpol) : 0.0;
         double g0 = 0.0, g1 = 0.0, g2 = 0.0;
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
