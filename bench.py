@@ -12,8 +12,12 @@ L2, so no L2 flush is needed between iterations.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-`--impl reference` times the CPU oracle port of the reference's apply
-(oracle/, numpy, all host threads) on a bounded sample of the same workload.
+`--impl reference` times the UNMODIFIED reference (flowbench 0.1.0, built into
+oracle/_ref by oracle/build_ref.py) through its own HelmholtzOperator.apply,
+numba backend, one thread, on a bounded sample of the same workload
+(oracle/ref_bench.py, run as a subprocess: the product package is never
+imported on that arm).  The GPU line's `cpu_baseline` and the LOR-PCG
+reference solve times come from the same reference build, timed in the run.
 """
 
 import argparse
@@ -183,66 +187,112 @@ def cpu_time(problems, reps=1):
     return tot_dofs / tot_t / 1e9, tot_t
 
 
-def cpu_sample(threads, reps=1, target=CPU_SAMPLE_DOFS):
-    """Returns (GDoF/s, timed seconds, description)."""
-    probs = cpu_problems(threads, target)
-    v, t = cpu_time(probs, reps)
-    for r, _, _ in probs:
-        r.close()
-    desc = (f"3D Helmholtz apply, p=1..8, ~{target/1e3:.0f}k DoFs per degree "
-            f"(perturbed cube), {reps} timed rep(s) after 1 warm-up, oracle numpy port, "
-            f"{threads} thread(s)")
-    return v, t, desc
-
-
 def run_reference(args, rank, world):
+    """Reference arm: the UNMODIFIED reference (oracle/_ref, built from
+    /root/reference by oracle/build_ref.py) timed through its own public API
+    in a single-threaded subprocess (oracle/ref_bench.py): stock
+    HelmholtzOperator.apply, FLOWBENCH_BACKEND=numba, on a bounded sample of
+    the workload.  Never imports the product package."""
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    probs = cpu_problems(threads)
-    for _ in range(args.warmup):
-        cpu_time(probs)
-    vals = []
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, _ = cpu_time(probs)
-        vals.append(v)
-    el = time.perf_counter() - t0
-    for r, _, _ in probs:
-        r.close()
-    value = float(np.mean(vals))
-    desc = (f"3D Helmholtz apply, p=1..8, ~{CPU_SAMPLE_DOFS/1e3:.0f}k DoFs per degree "
-            f"(perturbed cube), one apply per degree per step, oracle numpy port of the "
-            f"reference contractions on {threads} threads")
+    from oracle import ref_bench
+    if ref_bench.available():
+        res = ref_bench.run_subprocess(["apply", "--target", str(CPU_SAMPLE_DOFS),
+                                        "--steps", str(args.steps), "--warmup", str(args.warmup)])
+        value, el, cores, kind, desc = (res["value"], res["seconds"], res["cores"], res["kind"],
+                                        res["sample"])
+        extra = {"per_p": res["per_p"], "host_cpus": res["host_cpus"], "setup_s": res["setup_s"]}
+    else:  # no reference build on this host: the oracle port (test infrastructure)
+        threads = os.cpu_count() or 1
+        probs = cpu_problems(threads)
+        for _ in range(args.warmup):
+            cpu_time(probs)
+        t0 = time.perf_counter()
+        vals = [cpu_time(probs)[0] for _ in range(args.steps)]
+        el = time.perf_counter() - t0
+        for r, _, _ in probs:
+            r.close()
+        value, cores, kind = float(np.mean(vals)), threads, "port"
+        desc = (f"3D Helmholtz apply, p=1..8, ~{CPU_SAMPLE_DOFS/1e3:.0f}k DoFs per degree, oracle "
+                f"numpy port of the reference contractions on {threads} threads (oracle/_ref absent)")
+        extra = {}
+    cfg = config_block(world)
+    cfg["sample_dofs_per_degree"] = CPU_SAMPLE_DOFS
+    cfg["sample_note"] = ("the reference arm times a bounded sample (~120k DoFs per degree, "
+                          "same mesh family, c, nu, quadrature) of the 10M-DoF-per-degree workload; "
+                          "GDoF/s is size-normalised")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GDoF/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * el / max(args.steps, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(world),
-        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": threads, "kind": "port",
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": cores, "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
 
 
-def lor_pcg(cases=((4, 25), (7, 14)), c=C_HELM):
-    """LOR-preconditioned CG time-to-solve, 3D Helmholtz (cfg3 shape at ~1M
-    DoFs): device operator + device V-cycle, rel_tol 1e-8."""
+def reference_cpu(what, args, timeout=1800):
+    """The reference's own CPU path on this host (oracle/ref_bench.py), or
+    an error note."""
+    from oracle import ref_bench
+    if not ref_bench.available():
+        return {"error": "oracle/_ref not built (python oracle/build_ref.py)"}
+    try:
+        return ref_bench.run_subprocess([what] + list(args), timeout=timeout)
+    except Exception as exc:  # the CPU leg must not drop the GPU line
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
+PCG_CASES = {  # name -> (counts, p, kind, c); oracle/ref_bench.PCG_CASES
+    "cfg1": ((16, 16), 4, "stiffness", 0.0),
+    "p4_16": ((16, 16, 16), 4, "helmholtz", 10.0),
+    "p7_8": ((8, 8, 8), 7, "helmholtz", 10.0),
+    "p4_25": ((25, 25, 25), 4, "helmholtz", 10.0),
+    "p7_14": ((14, 14, 14), 7, "helmholtz", 10.0),
+}
+REF_PCG_TIMED = ("cfg1", "p4_16", "p7_8")
+
+
+def _golden_iterations():
+    out = {"cfg1": 17}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "manifest.json")) as f:
+            man = json.load(f)
+        for c in man.get("cfg3shape", []):
+            if not c["perturb"]:
+                out[f"p{c['p']}_{c['counts'][0]}"] = c["iterations"]
+    except (OSError, KeyError, ValueError):
+        pass
+    return out
+
+
+def lor_pcg(args, names=tuple(PCG_CASES)):
+    """LOR-preconditioned CG time-to-solve on the device (parity mode:
+    reference numbering, device operator + device V-cycle with the block
+    ILU(0) smoother), rel_tol 1e-8, b = default_rng(0) normal with zero
+    boundary values.  Beside it, the reference's own CPU solve
+    of the same problem timed on this host in the same run (cases
+    REF_PCG_TIMED; the ~1M-DoF cases carry the reference's golden counts)."""
     import torch
     from paper_1910_03032_b200 import geometry, mfop, solvers, spaces
+    ref = reference_cpu("pcg", ["--cases", ",".join(REF_PCG_TIMED)]) if not args.no_cpu else {}
+    gold = _golden_iterations()
     out = {}
-    for p, n in cases:
+    for name in names:
+        counts, p, kind, c = PCG_CASES[name]
         t0 = time.perf_counter()
-        m = geometry.cartesian_mesh((n, n, n))
+        m = geometry.cartesian_mesh(counts)
         sp = spaces.FESpace(m, p)
         geom = geometry.DeviceGeometry(m, sp.basis.quad)
-        op = mfop.HelmholtzOperator(sp, geom, c)
+        op = mfop.setup(kind, space=sp, geom=geom, nu=1.0, c=c)
         bdr = sp.boundary_dof_set()
         A = mfop.ConstrainedOperator(op, bdr)
-        pre = solvers.LORPreconditioner(sp, "helmholtz", c=c, dirichlet_attrs="all")
+        pre = solvers.LORPreconditioner(sp, kind, c=c, dirichlet_attrs="all")
         setup = time.perf_counter() - t0
         b = np.random.default_rng(0).standard_normal(sp.ndofs)
         b[bdr] = 0.0
@@ -257,12 +307,22 @@ def lor_pcg(cases=((4, 25), (7, 14)), c=C_HELM):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        out[f"p{p}_{n}^3"] = {"dofs": sp.ndofs, "iterations": rep.iterations,
-                              "converged": rep.converged, "solve_ms": round(ms, 2),
-                              "ms_per_iteration": round(ms / max(rep.iterations, 1), 3),
-                              "host_setup_s": round(setup, 2),
-                              "reference_cpu_solve_s": {4: 41.7, 7: 53.0}.get(p),
-                              "reference_iterations": {4: 30, 7: 36}.get(p)}
+        ent = {"dofs": sp.ndofs, "iterations": rep.iterations, "converged": rep.converged,
+               "solve_ms": round(ms, 2), "ms_per_iteration": round(ms / max(rep.iterations, 1), 3),
+               "host_setup_s": round(setup, 2), "reference_iterations": gold.get(name)}
+        r = ref.get(name) if isinstance(ref, dict) else None
+        if r:
+            ent["reference_cpu"] = {"iterations": r["iterations"], "solve_s": r["solve_s"],
+                                    "setup_s": r["setup_s"], "cores": 1,
+                                    "x_norm_rel_diff": abs(float(torch.linalg.norm(x)) - r["x_norm"])
+                                    / r["x_norm"]}
+            ent["speedup_solve"] = round(r["solve_s"] / (ms * 1e-3), 1)
+        out[name] = ent
+    if isinstance(ref, dict) and "error" in ref:
+        out["reference_cpu_error"] = ref["error"]
+    out["note"] = ("GPU: CUDA-event time of solvers.cg after one warm solve; reference_cpu: the "
+                   "unmodified reference (oracle/_ref) cg + LORPreconditioner on this host, "
+                   "FLOWBENCH_BACKEND=numba, 1 thread, same mesh / RHS")
     return out
 
 
@@ -305,8 +365,7 @@ def lor_pcg_scale(cases=((4, 116), (7, 66)), c=C_HELM):
             "setup_s": round(setup, 2), "levels": M.describe(),
             "mode": "scale: block-ILU(2^3 elements) smoother, Q1 level coarsened "
                     "geometrically to a dense-inverse bottom",
-            "reference_iterations_1M": {4: 30, 7: 36}.get(p),
-            "reference_cpu_solve_s_1M": {4: 41.7, 7: 53.0}.get(p)}
+            "reference_iterations_1M": _golden_iterations().get({4: "p4_25", 7: "p7_14"}[p])}
         del prob, A, M, b, x, y
         gc.collect()
         torch.cuda.empty_cache()
@@ -629,7 +688,7 @@ def run_ours(args, rank, world):
         "warmup_steps_run": nw,
     }
     if not args.no_pcg and world == 1:
-        line["lor_pcg"] = lor_pcg()
+        line["lor_pcg"] = lor_pcg(args)
     if sharded is not None:
         line["lor_pcg_cfg3_sharded"] = sharded
     if not args.no_callers and world == 1:
@@ -645,9 +704,15 @@ def run_ours(args, rank, world):
         torch.cuda.empty_cache()
         line["lor_pcg_cfg3"] = lor_pcg_scale()
     if not args.no_cpu:
-        v, secs, desc = cpu_sample(1, reps=3)
-        line["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": 1, "kind": "port",
-                                "sample": desc, "seconds": round(secs, 2)}
+        res = reference_cpu("apply", ["--target", str(CPU_SAMPLE_DOFS), "--steps", "2",
+                                      "--warmup", "1"])
+        if "error" not in res:
+            line["cpu_baseline"] = {"value": res["value"], "unit": "GDoF/s", "cores": res["cores"],
+                                    "kind": res["kind"], "sample": res["sample"],
+                                    "seconds": round(res["seconds"], 2),
+                                    "host_cpus": res["host_cpus"], "per_p": res["per_p"]}
+        else:
+            line["cpu_baseline"] = res
     print(json.dumps(line), flush=True)
 
 

@@ -113,9 +113,14 @@ int fb_operator_create_geom(int kind, const fb_restriction* rv, const fb_restric
                             const double* D_host, const double* Bp_host, const double* Dp_host,
                             const double* corners_host, double c, double nu,
                             fb_operator** out);
-/* Select one of the compiled launch shapes of the fused kernel for degree p
- * (0 = default); used by tools/tune_fast.py. */
+/* Select one of the compiled launch shapes (0..7) of the fused kernel for
+ * degree p, or -1 to restore the tuned default; used by tools/tune_fast.py
+ * and the multi-batch parity tests. */
 int fb_set_fast_config(int p, int variant);
+/* Shape of the last persistent fused-kernel launch on the calling thread:
+ * CTAs, element batches and elements per batch (each CTA walks
+ * nbatch / grid batches).  Test/diagnostic query. */
+int fb_last_fast_launch(int* grid, int* nbatch, int* elements_per_batch);
 /* Element-blocked factors (ne, K, nq1^dim) back to host, for verification. */
 int64_t fb_operator_factor_count(const fb_operator* op);
 int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count);
@@ -160,6 +165,12 @@ int fb_dot(int64_t n, const double* x_dev, const double* y_dev, double* partial_
            double* result_dev, void* stream);
 /* y = a*x + b*y  (a, b host scalars) */
 int fb_axpby(int64_t n, double a, const double* x_dev, double b, double* y_dev, void* stream);
+/* Fused PCG update (reference solvers.py:141-150 `alpha = rz / pAp;
+ * x += alpha * p; r -= alpha * Ap`): alpha_out[0] = rz/pAp (0 if pAp <= 0),
+ * x += alpha p and, if update_r, r -= alpha Ap in one pass; numpy rounding. */
+int fb_cg_update(int64_t n, const double* rz_dev, const double* pAp_dev, double* alpha_out_dev,
+                 const double* p_dev, const double* Ap_dev, double* x_dev, double* r_dev,
+                 int update_r, void* stream);
 /* y = a_dev[0]*x + y, scalar read on device (alpha = rz/pAp, kept on device) */
 int fb_axpy_dev(int64_t n, const double* a_dev, int sign, const double* x_dev, double* y_dev,
                 void* stream);

@@ -44,6 +44,7 @@ _SIGS = [
                                        _vp, _dbl, _dbl, C.POINTER(_vp)]),
     ("fb_operator_factor_count", _i64, [_vp]),
     ("fb_set_fast_config", _int, [_int, _int]),
+    ("fb_last_fast_launch", _int, [_vp, _vp, _vp]),
     ("fb_operator_factors", _int, [_vp, _vp, _i64]),
     ("fb_operator_destroy", None, [_vp]),
     ("fb_operator_apply", _int, [_vp, _vp, _vp, _vp]),
@@ -56,6 +57,7 @@ _SIGS = [
     ("fb_number_dofs_host", _i64, [_int, _int, _i64, _i64, _vp, _vp, _pi64, _pi64]),
     ("fb_dot_partials", _i64, [_i64]),
     ("fb_dot", _int, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    ("fb_cg_update", _int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp]),
     ("fb_axpby", _int, [_i64, _dbl, _vp, _dbl, _vp, _vp]),
     ("fb_axpy_dev", _int, [_i64, _vp, _int, _vp, _vp, _vp]),
     ("fb_scalar_div", _int, [_vp, _vp, _vp, _vp]),

@@ -195,6 +195,10 @@ void diff_matrix(const double* x, int n, double* D) {
   }
 }
 
+// shape of the last fused-kernel launch on this host thread (tests: prove the
+// persistent multi-batch path ran; fb_last_fast_launch)
+thread_local int g_last_grid = 0, g_last_nbatch = 0, g_last_ne = 0;
+
 template <int N, int Q, int KIND, int NE, int NT, int MINB, int ZL>
 int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   constexpr size_t smem = SF3Shape<N, Q, KIND, NE, ZL>::SMEM;
@@ -215,6 +219,9 @@ int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_
   p.y = y;
   p.nbatch = ceil_div(op->rv->ne, NE);
   const int grid = p.nbatch < resident ? p.nbatch : resident;
+  g_last_grid = grid;
+  g_last_nbatch = p.nbatch;
+  g_last_ne = NE;
   sf3_fast_kernel<N, Q, KIND, NE, NT, MINB, ZL><<<grid, NT, smem, st>>>(p);
   FB_CHECK_LAUNCH();
   return FB_OK;
@@ -238,6 +245,7 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // with the z-line schedule: +9 %, p = 5:
 // +14 %, p = 2, 6: +1-2 %); at p = 7, 8 the extra 41-56 KB per CTA costs more
 // occupancy than it saves.
+static const int kFastCfgDefault[9] = {0, 0, 3, 5, 6, 5, 4, 0, 0};
 static int g_fast_cfg[9] = {0, 0, 3, 5, 6, 5, 4, 0, 0};
 
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
@@ -394,6 +402,17 @@ static int finish_operator(fb_operator* op, const double* points, const double* 
     diff_matrix(points, nq1, Dq.data());
     for (int a = 0; a < nq1; ++a)
       for (int b = 0; b < nq1; ++b) fp.Dq[a][b] = Dq[a * nq1 + b];
+    {  // even-odd forms (sf3_fast.cuh eo_lines) of B, B^T, Dq, Dq^T
+      std::vector<double> Bt(size_t(n) * nq1), Dt(size_t(nq1) * nq1);
+      for (int q = 0; q < nq1; ++q)
+        for (int i = 0; i < n; ++i) Bt[i * nq1 + q] = B[q * n + i];
+      for (int a = 0; a < nq1; ++a)
+        for (int b = 0; b < nq1; ++b) Dt[b * nq1 + a] = Dq[a * nq1 + b];
+      eo_fill(fp.eB, B, nq1, n);
+      eo_fill(fp.eBt, Bt.data(), n, nq1);
+      eo_fill(fp.eD, Dq.data(), nq1, nq1);
+      eo_fill(fp.eDt, Dt.data(), nq1, nq1);
+    }
     fp.map = rv->map_pad.ptr;
     fp.spos = rv->s_pos.ptr;
     fp.fac = op->fac.ptr;
@@ -731,9 +750,16 @@ int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count) 
 
 int64_t fb_operator_factor_count(const fb_operator* op) { return op ? op->fac.n : 0; }
 
+int fb_last_fast_launch(int* grid, int* nbatch, int* elements_per_batch) {
+  if (grid) *grid = g_last_grid;
+  if (nbatch) *nbatch = g_last_nbatch;
+  if (elements_per_batch) *elements_per_batch = g_last_ne;
+  return FB_OK;
+}
+
 int fb_set_fast_config(int p, int variant) {
-  FB_REQUIRE(p >= 1 && p <= 8 && variant >= 0 && variant <= 7, "bad fast-path config");
-  g_fast_cfg[p] = variant;
+  FB_REQUIRE(p >= 1 && p <= 8 && variant >= -1 && variant <= 7, "bad fast-path config");
+  g_fast_cfg[p] = variant < 0 ? kFastCfgDefault[p] : variant;
   return FB_OK;
 }
 

@@ -73,6 +73,38 @@ __global__ void axpy_dev_kernel(int64_t n, const double* __restrict__ a, double 
   }
 }
 
+// Fused PCG update (solvers.py:141-150): alpha = rz / pAp (0 when pAp <= 0,
+// the loop then stops), x += alpha p and, unless this is a true-residual
+// iteration, r -= alpha Ap -- one pass instead of three launches, with the
+// reference's rounding (numpy: round(x + round(alpha * p))).
+template <bool VEC>
+__global__ void cg_update_kernel(int64_t n, const double* __restrict__ rz,
+                                 const double* __restrict__ pAp, double* __restrict__ alpha_out,
+                                 const double* __restrict__ p, const double* __restrict__ Ap,
+                                 double* __restrict__ x, double* __restrict__ r, int update_r) {
+  const double d = pAp[0];
+  const double al = d > 0.0 ? __ddiv_rn(rz[0], d) : 0.0;
+  const int64_t i0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * (VEC ? 2 : 1);
+  if (i0 == 0) alpha_out[0] = al;
+  if (VEC && i0 + 1 < n) {
+    const double2 pv = *reinterpret_cast<const double2*>(p + i0);
+    double2 xv = *reinterpret_cast<const double2*>(x + i0);
+    xv.x = __dadd_rn(xv.x, __dmul_rn(al, pv.x));
+    xv.y = __dadd_rn(xv.y, __dmul_rn(al, pv.y));
+    *reinterpret_cast<double2*>(x + i0) = xv;
+    if (update_r) {
+      const double2 av = *reinterpret_cast<const double2*>(Ap + i0);
+      double2 rv = *reinterpret_cast<const double2*>(r + i0);
+      rv.x = __dsub_rn(rv.x, __dmul_rn(al, av.x));
+      rv.y = __dsub_rn(rv.y, __dmul_rn(al, av.y));
+      *reinterpret_cast<double2*>(r + i0) = rv;
+    }
+  } else if (i0 < n) {
+    x[i0] = __dadd_rn(x[i0], __dmul_rn(al, p[i0]));
+    if (update_r) r[i0] = __dsub_rn(r[i0], __dmul_rn(al, Ap[i0]));
+  }
+}
+
 __global__ void scalar_div_kernel(const double* num, const double* den, double* out) {
   out[0] = __ddiv_rn(num[0], den[0]);
 }
@@ -169,6 +201,25 @@ int fb_axpy_dev(int64_t n, const double* a, int sign, const double* x, double* y
   if (n <= 0) return FB_OK;
   axpy_dev_kernel<<<ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, a, sign >= 0 ? 1.0 : -1.0,
                                                                     x, y);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+int fb_cg_update(int64_t n, const double* rz, const double* pAp, double* alpha_out,
+                 const double* p, const double* Ap, double* x, double* r, int update_r,
+                 void* stream) {
+  FB_REQUIRE(n >= 0, "negative length");
+  const bool aligned = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(Ap) |
+                         reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r)) & 15) == 0;
+  cudaStream_t st = as_stream(stream);
+  if (aligned) {
+    const int64_t pairs = n > 0 ? (n + 1) / 2 : 1;
+    cg_update_kernel<true><<<ceil_div(pairs, 256), 256, 0, st>>>(n, rz, pAp, alpha_out, p, Ap, x,
+                                                                 r, update_r);
+  } else {
+    cg_update_kernel<false><<<ceil_div(n > 0 ? n : 1, 256), 256, 0, st>>>(n, rz, pAp, alpha_out,
+                                                                          p, Ap, x, r, update_r);
+  }
   FB_CHECK_LAUNCH();
   return FB_OK;
 }

@@ -51,6 +51,89 @@ constexpr int kMaxQ1 = 12;
 
 enum SFKind { kMass = 0, kStiff = 1, kHelm = 2 };
 
+// Even-odd ("symmetry") decomposition of the 1D matrices.  The GLL nodes and
+// the Gauss points are symmetric about 0, so every 1D matrix M (R x C) of the
+// kernel is centrosymmetric or skew-centrosymmetric:
+//   M[R-1-a][C-1-i] = S * M[a][i],  S = +1 for B, B^T;  S = -1 for Dq, Dq^T.
+// With e_i = v_i + v_{C-1-i}, o_i = v_i - v_{C-1-i} (i < C/2) a line
+// contraction out = M v becomes, per output pair (a, R-1-a),
+//   E = sum_i Pe[a][i] e_i + M[a][C/2] v_{C/2},  O = sum_i Po[a][i] o_i,
+//   out[a] = E + O,  out[R-1-a] = S (E - O),
+// Pe/Po = (M[a][i] +- M[a][C-1-i]) / 2: about half the DFMAs and half the
+// coefficient loads of the dense line (R*C/2 + R + C instead of R*C).
+constexpr int kEOR = kMaxQ1 / 2 + 1;
+constexpr int kEOC = kMaxQ1 / 2;
+struct EOMat {
+  double e[kEOR][kEOC];
+  double o[kEOR][kEOC];
+  double m[kEOR];  // M[a][C/2] (odd C)
+};
+
+// host: even-odd form of a row-major R x C matrix
+inline void eo_fill(EOMat& E, const double* M, int R, int C) {
+  for (int a = 0; a < kEOR; ++a) {
+    for (int i = 0; i < kEOC; ++i) E.e[a][i] = E.o[a][i] = 0.0;
+    E.m[a] = 0.0;
+  }
+  const int Rh = R / 2 + (R & 1), Ch = C / 2;
+  for (int a = 0; a < Rh; ++a) {
+    for (int i = 0; i < Ch; ++i) {
+      E.e[a][i] = 0.5 * (M[a * C + i] + M[a * C + C - 1 - i]);
+      E.o[a][i] = 0.5 * (M[a * C + i] - M[a * C + C - 1 - i]);
+    }
+    if (C & 1) E.m[a] = M[a * C + Ch];
+  }
+}
+
+// NL lines of length C -> NL lines of length R through the even-odd form;
+// the coefficient loads are shared by the NL lines.
+template <int R, int C, int S, int NL>
+__device__ __forceinline__ void eo_lines(const EOMat& M, const double (&v)[NL][C],
+                                         double (&out)[NL][R]) {
+  constexpr int Rh = R / 2, Ch = C / 2, CH = Ch > 0 ? Ch : 1;
+  double e[NL][CH], o[NL][CH];
+#pragma unroll
+  for (int l = 0; l < NL; ++l)
+#pragma unroll
+    for (int i = 0; i < Ch; ++i) {
+      e[l][i] = v[l][i] + v[l][C - 1 - i];
+      o[l][i] = v[l][i] - v[l][C - 1 - i];
+    }
+#pragma unroll
+  for (int a = 0; a < Rh; ++a) {
+    double E[NL], O[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      E[l] = (C & 1) ? M.m[a] * v[l][Ch] : 0.0;
+      O[l] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < Ch; ++i) {
+      const double ce = M.e[a][i], co = M.o[a][i];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        E[l] = fma(ce, e[l][i], E[l]);
+        O[l] = fma(co, o[l][i], O[l]);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      out[l][a] = E[l] + O[l];
+      out[l][R - 1 - a] = (S > 0) ? E[l] - O[l] : O[l] - E[l];
+    }
+  }
+  if constexpr ((R & 1) != 0) {  // middle output: pure even (S = +1) or odd (S = -1)
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      double acc = (S > 0 && (C & 1)) ? M.m[Rh] * v[l][Ch] : 0.0;
+#pragma unroll
+      for (int i = 0; i < Ch; ++i)
+        acc = (S > 0) ? fma(M.e[Rh][i], e[l][i], acc) : fma(M.o[Rh][i], o[l][i], acc);
+      out[l][Rh] = acc;
+    }
+  }
+}
+
 struct SF3Params {
   const int* __restrict__ map;     // (ne, NLOCP) L->E map, int32, padded per element
   const int* __restrict__ spos;    // (ne, NBP) transposed-CSR slot of each boundary contribution
@@ -65,6 +148,7 @@ struct SF3Params {
   int nbatch;                      // ceil(ne / NE)
   double B[kMaxQ1][kMaxQ1];        // B[q][i]  basis values at rule points
   double Dq[kMaxQ1][kMaxQ1];       // Dq[q][r] collocated derivative at rule points
+  EOMat eB, eBt, eD, eDt;          // even-odd forms of B, B^T, Dq, Dq^T (eo_fill)
 };
 
 template <int KIND>
@@ -356,16 +440,12 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         const int k = r / N, j = r - k * N;
         const double* in = sx + el * Sh::XBUF + XI(k, j, 0);
         double* out = smem + el * ES + BUF + IX(k, j, 0);
-        double v[N];
+        double v[1][N], w[1][Q];
 #pragma unroll
-        for (int i = 0; i < N; ++i) v[i] = in[i];
+        for (int i = 0; i < N; ++i) v[0][i] = in[i];
+        eo_lines<Q, N, 1, 1>(P.eB, v, w);
 #pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          double acc = 0.0;
-#pragma unroll
-          for (int i = 0; i < N; ++i) acc = fma(P.B[a][i], v[i], acc);
-          out[a] = acc;
-        }
+        for (int a = 0; a < Q; ++a) out[a] = w[0][a];
       }
       __syncthreads();
 
@@ -384,16 +464,12 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         const int k = r / Q, a = r - k * Q;
         const double* in = smem + el * ES + BUF + IX(k, 0, a);
         double* out = smem + el * ES + IX(k, 0, a);
-        double v[N];
+        double v[1][N], w[1][Q];
 #pragma unroll
-        for (int j = 0; j < N; ++j) v[j] = in[j * QP];
+        for (int j = 0; j < N; ++j) v[0][j] = in[j * QP];
+        eo_lines<Q, N, 1, 1>(P.eB, v, w);
 #pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          double acc = 0.0;
-#pragma unroll
-          for (int j = 0; j < N; ++j) acc = fma(P.B[b][j], v[j], acc);
-          out[b * QP] = acc;
-        }
+        for (int b = 0; b < Q; ++b) out[b * QP] = w[0][b];
       }
       __syncthreads();
 
@@ -404,38 +480,26 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         const int el = L / Q2, r = L - el * Q2;
         const int b = r / Q, a = r - b * Q;
         double* base = smem + el * ES;
-        double v[N];
+        double v[1][N], u[1][Q];
 #pragma unroll
-        for (int k = 0; k < N; ++k) v[k] = base[IX(k, b, a)];
-        double u[Q];
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < N; ++k) acc = fma(P.B[c][k], v[k], acc);
-          u[c] = acc;
-        }
+        for (int k = 0; k < N; ++k) v[0][k] = base[IX(k, b, a)];
+        eo_lines<Q, N, 1, 1>(P.eB, v, u);
         if (KIND == kMass) {
           // mass: scale by wdet and contract back along z right here
           const double* __restrict__ f = P.fac + (e0 + el) * FACP + b * Q + a;
           const bool live = el < nel;
 #pragma unroll
-          for (int c = 0; c < Q; ++c) u[c] = (live ? __ldg(f + c * Q2) : 0.0) * u[c];
+          for (int c = 0; c < Q; ++c) u[0][c] = (live ? __ldg(f + c * Q2) : 0.0) * u[0][c];
+          eo_lines<N, Q, 1, 1>(P.eBt, u, v);
 #pragma unroll
-          for (int k = 0; k < N; ++k) {
-            double acc = 0.0;
-#pragma unroll
-            for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], u[c], acc);
-            base[IX(k, b, a)] = acc;
-          }
+          for (int k = 0; k < N; ++k) base[IX(k, b, a)] = v[0][k];
         } else {
+          double g[1][Q];
+          eo_lines<Q, Q, -1, 1>(P.eD, u, g);
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int t = 0; t < Q; ++t) acc = fma(P.Dq[c][t], u[t], acc);
-            base[3 * BUF + IX(c, b, a)] = acc;
-            base[IX(c, b, a)] = u[c];
+            base[3 * BUF + IX(c, b, a)] = g[0][c];
+            base[IX(c, b, a)] = u[0][c];
           }
         }
       }
@@ -451,24 +515,19 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           // the x-line (c, b=t) and the y-line (c, a=t) share Dq coefficients
           const double* inx = base + IX(c, t, 0);
           const double* iny = base + IX(c, 0, t);
-          double vx[Q], vy[Q];
+          double vv[2][Q], w[2][Q];
 #pragma unroll
           for (int s2 = 0; s2 < Q; ++s2) {
-            vx[s2] = inx[s2];
-            vy[s2] = iny[s2 * QP];
+            vv[0][s2] = inx[s2];
+            vv[1][s2] = iny[s2 * QP];
           }
+          eo_lines<Q, Q, -1, 2>(P.eD, vv, w);
           double* ox = base + BUF + IX(c, t, 0);
           double* oy = base + 2 * BUF + IX(c, 0, t);
 #pragma unroll
           for (int a = 0; a < Q; ++a) {
-            double ax = 0.0, ay = 0.0;
-#pragma unroll
-            for (int s2 = 0; s2 < Q; ++s2) {
-              ax = fma(P.Dq[a][s2], vx[s2], ax);
-              ay = fma(P.Dq[a][s2], vy[s2], ay);
-            }
-            ox[a] = ax;
-            oy[a * QP] = ay;
+            ox[a] = w[0][a];
+            oy[a * QP] = w[1][a];
           }
         }
         __syncthreads();
@@ -520,26 +579,19 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           double* io0 = base + BUF + IX(c, t, 0);
           double* io1 = base + 2 * BUF + IX(c, 0, t);
           double* io2 = base + 3 * BUF + IX(0, c, t);
-          double v0[Q], v1[Q], v2[Q];
+          double vv[3][Q], w[3][Q];
 #pragma unroll
           for (int s2 = 0; s2 < Q; ++s2) {
-            v0[s2] = io0[s2];
-            v1[s2] = io1[s2 * QP];
-            v2[s2] = io2[s2 * YP];
+            vv[0][s2] = io0[s2];
+            vv[1][s2] = io1[s2 * QP];
+            vv[2][s2] = io2[s2 * YP];
           }
+          eo_lines<Q, Q, -1, 3>(P.eDt, vv, w);
 #pragma unroll
           for (int a = 0; a < Q; ++a) {
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll
-            for (int s2 = 0; s2 < Q; ++s2) {
-              const double d = P.Dq[s2][a];
-              a0 = fma(d, v0[s2], a0);
-              a1 = fma(d, v1[s2], a1);
-              a2 = fma(d, v2[s2], a2);
-            }
-            io0[a] = a0;
-            io1[a * QP] = a1;
-            io2[a * YP] = a2;
+            io0[a] = w[0][a];
+            io1[a * QP] = w[1][a];
+            io2[a * YP] = w[2][a];
           }
         }
         __syncthreads();
@@ -550,20 +602,16 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           const int el = L / Q2, r = L - el * Q2;
           const int b = r / Q, a = r - b * Q;
           double* base = smem + el * ES;
-          double v[Q];
+          double v[1][Q], w[1][N];
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
             const int ix = IX(c, b, a);
             const double fu = (KIND == kHelm) ? base[ix] : 0.0;  // stiffness: no mass term
-            v[c] = ((fu + base[BUF + ix]) + base[2 * BUF + ix]) + base[3 * BUF + ix];
+            v[0][c] = ((fu + base[BUF + ix]) + base[2 * BUF + ix]) + base[3 * BUF + ix];
           }
+          eo_lines<N, Q, 1, 1>(P.eBt, v, w);
 #pragma unroll
-          for (int k = 0; k < N; ++k) {
-            double acc = 0.0;
-#pragma unroll
-            for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], v[c], acc);
-            base[IX(k, b, a)] = acc;
-          }
+          for (int k = 0; k < N; ++k) base[IX(k, b, a)] = w[0][k];
         }
         __syncthreads();
       }
@@ -575,33 +623,22 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         const int el = L / Q2, r = L - el * Q2;
         const int b = r / Q, a = r - b * Q;
         double* base = smem + el * ES;
-        double v[N];
+        double v[1][N], u[1][Q];
 #pragma unroll
-        for (int k = 0; k < N; ++k) v[k] = base[IX(k, b, a)];
-        double u[Q];
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < N; ++k) acc = fma(P.B[c][k], v[k], acc);
-          u[c] = acc;
-        }
+        for (int k = 0; k < N; ++k) v[0][k] = base[IX(k, b, a)];
+        eo_lines<Q, N, 1, 1>(P.eB, v, u);
         if (KIND == kMass) {
           // mass: scale by wdet and contract back along z right here
           const double* __restrict__ f = P.fac + (e0 + el) * FACP + b * Q + a;
           const bool live = el < nel;
 #pragma unroll
-          for (int c = 0; c < Q; ++c) u[c] = (live ? __ldg(f + c * Q2) : 0.0) * u[c];
+          for (int c = 0; c < Q; ++c) u[0][c] = (live ? __ldg(f + c * Q2) : 0.0) * u[0][c];
+          eo_lines<N, Q, 1, 1>(P.eBt, u, v);
 #pragma unroll
-          for (int k = 0; k < N; ++k) {
-            double acc = 0.0;
-#pragma unroll
-            for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], u[c], acc);
-            base[IX(k, b, a)] = acc;
-          }
+          for (int k = 0; k < N; ++k) base[IX(k, b, a)] = v[0][k];
         } else {
 #pragma unroll
-          for (int c = 0; c < Q; ++c) base[IX(c, b, a)] = u[c];
+          for (int c = 0; c < Q; ++c) base[IX(c, b, a)] = u[0][c];
         }
       }
       __syncthreads();
@@ -616,24 +653,19 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           // the x-line (c, b=t) and the y-line (c, a=t) share Dq coefficients
           const double* inx = base + IX(c, t, 0);
           const double* iny = base + IX(c, 0, t);
-          double vx[Q], vy[Q];
+          double vv[2][Q], w[2][Q];
 #pragma unroll
           for (int s2 = 0; s2 < Q; ++s2) {
-            vx[s2] = inx[s2];
-            vy[s2] = iny[s2 * QP];
+            vv[0][s2] = inx[s2];
+            vv[1][s2] = iny[s2 * QP];
           }
+          eo_lines<Q, Q, -1, 2>(P.eD, vv, w);
           double* ox = base + BUF + IX(c, t, 0);
           double* oy = base + 2 * BUF + IX(c, 0, t);
 #pragma unroll
           for (int a = 0; a < Q; ++a) {
-            double ax = 0.0, ay = 0.0;
-#pragma unroll
-            for (int s2 = 0; s2 < Q; ++s2) {
-              ax = fma(P.Dq[a][s2], vx[s2], ax);
-              ay = fma(P.Dq[a][s2], vy[s2], ay);
-            }
-            ox[a] = ax;
-            oy[a * QP] = ay;
+            ox[a] = w[0][a];
+            oy[a * QP] = w[1][a];
           }
         }
         __syncthreads();
@@ -653,16 +685,10 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           double* col = smem + el * ES + IX(0, b, a);
           const double* __restrict__ f =
               Sh::FSTAGE ? fsm + el * FACP + ba : P.fac + (e0 + el) * FACP + ba;
-          double u[Q], g[Q];
+          double u[1][Q], g[1][Q];
 #pragma unroll
-          for (int c = 0; c < Q; ++c) u[c] = col[c * YP];
-#pragma unroll
-          for (int c = 0; c < Q; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int s2 = 0; s2 < Q; ++s2) acc = fma(P.Dq[c][s2], u[s2], acc);
-            g[c] = acc;
-          }
+          for (int c = 0; c < Q; ++c) u[0][c] = col[c * YP];
+          eo_lines<Q, Q, -1, 1>(P.eD, u, g);
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
             const double* fc = f + c * Q2;
@@ -670,19 +696,16 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
             const double w02 = ldf(fc + (o + 2) * Q3), w11 = ldf(fc + (o + 3) * Q3);
             const double w12 = ldf(fc + (o + 4) * Q3), w22 = ldf(fc + (o + 5) * Q3);
             double* pt = col + c * YP;
-            const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = g[c];
+            const double g0 = pt[BUF], g1 = pt[2 * BUF], g2 = g[0][c];
             pt[BUF] = w00 * g0 + w01 * g1 + w02 * g2;
             pt[2 * BUF] = w01 * g0 + w11 * g1 + w12 * g2;
-            g[c] = w02 * g0 + w12 * g1 + w22 * g2;
-            u[c] = (KIND == kHelm) ? ldf(fc) * u[c] : 0.0;
+            g[0][c] = w02 * g0 + w12 * g1 + w22 * g2;
+            u[0][c] = (KIND == kHelm) ? ldf(fc) * u[0][c] : 0.0;
           }
+          double h[1][Q];
+          eo_lines<Q, Q, -1, 1>(P.eDt, g, h);
 #pragma unroll
-          for (int c = 0; c < Q; ++c) {
-            double acc = u[c];
-#pragma unroll
-            for (int s2 = 0; s2 < Q; ++s2) acc = fma(P.Dq[s2][c], g[s2], acc);
-            col[c * YP] = acc;
-          }
+          for (int c = 0; c < Q; ++c) col[c * YP] = u[0][c] + h[0][c];
         }
         __syncthreads();
         if constexpr (Sh::FSTAGE) {  // factor buffer free: stage the next batch's block
@@ -697,23 +720,17 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           double* base = smem + el * ES;
           double* io0 = base + BUF + IX(c, t, 0);
           double* io1 = base + 2 * BUF + IX(c, 0, t);
-          double v0[Q], v1[Q];
+          double vv[2][Q], w[2][Q];
 #pragma unroll
           for (int s2 = 0; s2 < Q; ++s2) {
-            v0[s2] = io0[s2];
-            v1[s2] = io1[s2 * QP];
+            vv[0][s2] = io0[s2];
+            vv[1][s2] = io1[s2 * QP];
           }
+          eo_lines<Q, Q, -1, 2>(P.eDt, vv, w);
 #pragma unroll
           for (int a = 0; a < Q; ++a) {
-            double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-            for (int s2 = 0; s2 < Q; ++s2) {
-              const double dd = P.Dq[s2][a];
-              a0 = fma(dd, v0[s2], a0);
-              a1 = fma(dd, v1[s2], a1);
-            }
-            io0[a] = a0;
-            io1[a * QP] = a1;
+            io0[a] = w[0][a];
+            io1[a * QP] = w[1][a];
           }
         }
         __syncthreads();
@@ -724,19 +741,15 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
           const int el = L / Q2, r = L - el * Q2;
           const int b = r / Q, a = r - b * Q;
           double* base = smem + el * ES;
-          double v[Q];
+          double v[1][Q], w[1][N];
 #pragma unroll
           for (int c = 0; c < Q; ++c) {
             const int ix = IX(c, b, a);
-            v[c] = (base[ix] + base[BUF + ix]) + base[2 * BUF + ix];
+            v[0][c] = (base[ix] + base[BUF + ix]) + base[2 * BUF + ix];
           }
+          eo_lines<N, Q, 1, 1>(P.eBt, v, w);
 #pragma unroll
-          for (int k = 0; k < N; ++k) {
-            double acc = 0.0;
-#pragma unroll
-            for (int c = 0; c < Q; ++c) acc = fma(P.B[c][k], v[c], acc);
-            base[IX(k, b, a)] = acc;
-          }
+          for (int k = 0; k < N; ++k) base[IX(k, b, a)] = w[0][k];
         }
         __syncthreads();
       }
@@ -749,16 +762,12 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         const int k = r / Q, a = r - k * Q;
         const double* in = smem + el * ES + IX(k, 0, a);
         double* out = smem + el * ES + BUF + IX(k, 0, a);
-        double v[Q];
+        double v[1][Q], w[1][N];
 #pragma unroll
-        for (int b = 0; b < Q; ++b) v[b] = in[b * QP];
+        for (int b = 0; b < Q; ++b) v[0][b] = in[b * QP];
+        eo_lines<N, Q, 1, 1>(P.eBt, v, w);
 #pragma unroll
-        for (int j = 0; j < N; ++j) {
-          double acc = 0.0;
-#pragma unroll
-          for (int b = 0; b < Q; ++b) acc = fma(P.B[b][j], v[b], acc);
-          out[j * QP] = acc;
-        }
+        for (int j = 0; j < N; ++j) out[j * QP] = w[0][j];
       }
       __syncthreads();
 
@@ -768,17 +777,16 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         const int el = L / (N * N), r = L - el * N * N;
         const int k = r / N, j = r - k * N;
         const double* in = smem + el * ES + BUF + IX(k, j, 0);
-        double v[Q];
+        double v[1][Q], w[1][N];
 #pragma unroll
-        for (int a = 0; a < Q; ++a) v[a] = in[a];
+        for (int a = 0; a < Q; ++a) v[0][a] = in[a];
+        eo_lines<N, Q, 1, 1>(P.eBt, v, w);
         const bool edge_line = (k == 0 || k == N - 1 || j == 0 || j == N - 1);
         const int* mrow = smap + el * NLOCP + (k * N + j) * N;
         const int* prow = spos + el * NBP;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          double acc = 0.0;
-#pragma unroll
-          for (int a = 0; a < Q; ++a) acc = fma(P.B[a][i], v[a], acc);
+          const double acc = w[0][i];
           if (!edge_line && i > 0 && i < N - 1) {
             y[mrow[i]] = 0.0 + acc;  // bincount semantics: 0.0 + contribution
           } else {

@@ -230,27 +230,28 @@ def cg(A, b, precond=None, config=None, x0=None, project=None, inner=None):
     relres = 1.0
     it = 0
     converged = False
+    old, new = 0, 3  # device slots of rz and rz_new, swapped every iteration (no copy)
     for it in range(1, cfg.max_iters + 1):
         apply_A(p, Ap)
         dot_into(p, Ap, s[1:2])
-        vec.safe_div(s[0:1], s[1:2], s[2:3])  # alpha = rz / pAp (0 if pAp <= 0)
-        vec.axpy_dev(s[2:3], p, x, +1)
-        if it % 50 == 0:
+        # fused: alpha = rz / pAp (0 if pAp <= 0); x += alpha p; r -= alpha Ap
+        true_res = it % 50 == 0
+        vec.cg_update(s[old:old + 1], s[1:2], s[2:3], p, Ap, x, r, update_r=not true_res)
+        if true_res:
             apply_A(x, tmp)
             vec.copy(bd, r)
             vec.axpby(-1.0, tmp, 1.0, r)
             if proj is not None:
                 proj(r, r)
-        else:
-            vec.axpy_dev(s[2:3], Ap, r, -1)
         if M is not None:
             M(r, z)
         else:
             vec.copy(r, z)
         if proj is not None:
             proj(z, z)
-        dot_into(r, z, s[3:4])
-        pAp, _, rz_new = s[1:4].tolist()
+        dot_into(r, z, s[new:new + 1])
+        vals = s.tolist()
+        pAp, rz_new = vals[1], vals[new]
         if pAp <= 0.0:
             break
         relres = math.sqrt(abs(rz_new)) / norm0
@@ -261,8 +262,8 @@ def cg(A, b, precond=None, config=None, x0=None, project=None, inner=None):
         if rz_new == 0.0:
             converged = True
             break
-        vec.xpby_ratio(z, s[3:4], s[0:1], p)  # p = z + (rz_new / rz) p
-        vec.copy(s[3:4], s[0:1])
+        vec.xpby_ratio(z, s[new:new + 1], s[old:old + 1], p)  # p = z + (rz_new / rz) p
+        old, new = new, old
     if cfg.rel_tol == 0.0:
         converged = True
     return done(converged, it, relres)

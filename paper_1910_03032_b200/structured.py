@@ -48,6 +48,8 @@ from . import vec
 from .quadrature import build_eval_matrices, make_basis
 
 
+DEFAULT_COARSE_CYCLES = 2
+
 # ---------------------------------------------------------------------------
 # block-major first-touch numbering of a structured box
 # ---------------------------------------------------------------------------
@@ -347,7 +349,7 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
     cube edge of the smoother blocks on p >= 2 / Q1 levels."""
 
     def __init__(self, space, kind, nu=1.0, c=0.0, dirichlet_attrs="all", block=2,
-                 q1_block=4, max_coarse=20000):
+                 q1_block=4, max_coarse=20000, coarse_cycles=None):
         if dirichlet_attrs != "all":
             raise ValueError("scale mode supports Dirichlet conditions on the whole boundary")
         t0 = time.perf_counter()
@@ -359,9 +361,18 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
         for deg in lor_mod.degree_ladder(space.p)[1:]:
             spaces.append(BoxSpace(space.mesh, deg, block=block if deg > 1 else q1_block,
                                    device=ddev))
+        self.q1_index = len(spaces) - 1  # the ladder's Q1 level on the original mesh
         while spaces[-1].ndofs_scalar > max_coarse and min(spaces[-1].counts) >= 2:
             spaces.append(BoxSpace(coarsen_box(spaces[-1].mesh), 1, block=q1_block, device=ddev))
         self.spaces = spaces
+        # near-exact Q1 solve (SURVEY 8(e')): when the Q1 level is coarsened
+        # geometrically, the reference's exact SuperLU bottom (solvers.py:372,
+        # 376) is replaced by `coarse_cycles` stationary h-multigrid V-cycles
+        # on the Q1 hierarchy -- a fixed linear (and symmetric) operator, so
+        # the outer CG stays a CG
+        if coarse_cycles is None:
+            coarse_cycles = DEFAULT_COARSE_CYCLES
+        self.coarse_cycles = int(coarse_cycles) if len(spaces) - 1 > self.q1_index else 1
         self._A = [DeviceLevelMatrix(s, kind, nu=nu, c=c) for s in spaces]
         self.levels = list(zip(spaces, self._A))
         self.smoothers = [DeviceBlockILU0(A, s.block_ptr) for s, A in self.levels[:-1]]
@@ -374,16 +385,36 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
         self._r = [dev.empty(n) for n in sizes]
         self._t = [dev.empty(n) for n in sizes]
         self._t2 = [dev.empty(n) for n in sizes]
+        self._rk = self._dk = None
         torch.cuda.synchronize()
         self.setup_seconds = time.perf_counter() - t0
 
+    def _cycle(self, level, r, x, st):
+        super()._cycle(level, r, x, st)
+        if level != self.q1_index or self.coarse_cycles <= 1:
+            return
+        A = self._A[level]
+        if self._rk is None:
+            self._rk, self._dk = dev.empty(r.shape[0]), dev.empty(r.shape[0])
+        for _ in range(self.coarse_cycles - 1):  # x += V_h (r - A x)
+            A.residual_into(r, x, self._rk, st)
+            super()._cycle(level, self._rk, self._dk, st)
+            vec.axpby(1.0, self._dk, 1.0, x, st)
+
+    def clone_workspace(self):
+        c = super().clone_workspace()
+        if c is not None:
+            c._rk = c._dk = None
+        return c
+
     def describe(self):
-        return [{"p": s.p, "counts": list(s.counts), "rows": s.ndofs_scalar, "nnz": A.nnz}
-                for s, A in self.levels]
+        return {"coarse_cycles": self.coarse_cycles, "q1_index": self.q1_index,
+                "levels": [{"p": s.p, "counts": list(s.counts), "rows": s.ndofs_scalar,
+                            "nnz": A.nnz} for s, A in self.levels]}
 
 
 def helmholtz_box_problem(counts, p, c=10.0, nu=1.0, perturb=0.05, seed=1, block=2,
-                          q1_block=4, max_coarse=20000, rhs_seed=0):
+                          q1_block=4, max_coarse=20000, rhs_seed=0, coarse_cycles=None):
     """cfg3 building blocks on one device: box mesh, block-major space,
     constrained Helmholtz operator, scale-mode LOR preconditioner and a
     random right-hand side with zero boundary values."""
@@ -397,7 +428,7 @@ def helmholtz_box_problem(counts, p, c=10.0, nu=1.0, perturb=0.05, seed=1, block
     A = mfop.ConstrainedOperator(op, bdr)
     t1 = time.perf_counter()
     M = BoxLORPreconditioner(space, "helmholtz", nu=nu, c=c, block=block, q1_block=q1_block,
-                             max_coarse=max_coarse)
+                             max_coarse=max_coarse, coarse_cycles=coarse_cycles)
     g = torch.Generator(device=ddev)
     g.manual_seed(rhs_seed)
     b = torch.randn(space.ndofs_scalar, generator=g, dtype=torch.float64, device=ddev)

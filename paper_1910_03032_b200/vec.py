@@ -76,6 +76,14 @@ def axpy_dev(alpha, x, y, sign=1, stream=None):
     return y
 
 
+def cg_update(rz, pAp, alpha, p, Ap, x, r, update_r=True, stream=None):
+    """alpha = rz/pAp (0 if pAp <= 0); x += alpha p; r -= alpha Ap (fused)."""
+    _lib.check(_lib.lib.fb_cg_update(x.shape[0], rz.data_ptr(), pAp.data_ptr(), alpha.data_ptr(),
+                                     p.data_ptr(), Ap.data_ptr(), x.data_ptr(), r.data_ptr(),
+                                     int(bool(update_r)), _st(stream)))
+    return x
+
+
 def safe_div(num, den, out, stream=None):
     _lib.check(_lib.lib.fb_safe_div(num.data_ptr(), den.data_ptr(), out.data_ptr(), _st(stream)))
     return out

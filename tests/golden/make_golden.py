@@ -201,6 +201,53 @@ def make_solvers():
     return {"solvers": manifest}
 
 
+# cfg3-shape LOR-PCG at ~1M DoFs: (name, counts, perturb, perturb_seed, p, c)
+CFG3_CASES = [
+    ("cfg3s_p4_25", (25, 25, 25), 0.0, 0, 4, 10.0),
+    ("cfg3s_p7_14", (14, 14, 14), 0.0, 0, 7, 10.0),
+    ("cfg3s_p4_16_pert", (16, 16, 16), 0.05, 1, 4, 10.0),
+    ("cfg3s_p7_9_pert", (9, 9, 9), 0.05, 1, 7, 10.0),
+]
+
+
+def make_cfg3shape():
+    """Reference iteration counts (and a solution fingerprint) of the
+    Helmholtz LOR-PCG at the cfg3 shape, ~0.3-1M DoFs, b = default_rng(0)
+    normal with zero boundary values, rel_tol 1e-8 (app.py:453-496 protocol).
+    Perturbed cases use perturb_mesh(m, 0.05, seed=1) like bench.py."""
+    import time
+    mesh, fespace, mfop, solvers, lor, _ = ref_modules()
+    out, manifest = {}, []
+    for (name, counts, perturb, pseed, p, c) in CFG3_CASES:
+        t0 = time.perf_counter()
+        m = mesh.cartesian_mesh(counts)
+        if perturb:
+            m = mesh.perturb_mesh(m, perturb, seed=pseed)
+        sp_ = fespace.FESpace(m, p)
+        geom = mesh.compute_geometric_factors(m, sp_.basis.quad)
+        op = mfop.HelmholtzOperator(sp_, geom, c=c, nu=1.0)
+        bdr = sp_.boundary_dof_set()
+        A = mfop.ConstrainedOperator(op, bdr)
+        pre = solvers.LORPreconditioner(sp_, "helmholtz", nu=1.0, c=c, dirichlet_attrs="all")
+        t1 = time.perf_counter()
+        b = np.random.default_rng(0).standard_normal(sp_.ndofs)
+        b[bdr] = 0.0
+        x, rep = solvers.cg(A, b, precond=pre,
+                            config=solvers.SolverConfig(rel_tol=1e-8, max_iters=300))
+        t2 = time.perf_counter()
+        idx = np.random.default_rng(1).choice(sp_.ndofs, 4096, replace=False)
+        out[f"{name}/idx"] = idx
+        out[f"{name}/x_sample"] = x[idx]
+        out[f"{name}/hist"] = np.array(rep.residuals)
+        manifest.append(dict(name=name, counts=list(counts), perturb=perturb, perturb_seed=pseed,
+                             p=p, c=c, ndofs=int(sp_.ndofs), iterations=rep.iterations,
+                             x_norm=float(np.linalg.norm(x)), setup_s=round(t1 - t0, 1),
+                             solve_s=round(t2 - t1, 1)))
+        print(manifest[-1], flush=True)
+    np.savez_compressed(os.path.join(HERE, "cfg3shape.npz"), **out)
+    return {"cfg3shape": manifest}
+
+
 # (name, d, counts, p, alpha_dt)
 STOKES_CASES = [
     ("cav2d_p2", 2, (8, 8), 2, None),
@@ -382,7 +429,8 @@ def make_boundary():
 
 
 GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers, "stokes": make_stokes,
-          "extras": make_extras, "boundary": make_boundary}
+          "extras": make_extras, "boundary": make_boundary,
+          "cfg3shape": make_cfg3shape}
 
 
 def main(argv):

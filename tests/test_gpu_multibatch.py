@@ -1,0 +1,118 @@
+"""Oracle parity of the BENCHMARKED fused-kernel path.
+
+The bench's fused kernel (csrc/sf3_fast.cuh) is persistent: each CTA walks
+batches blockIdx.x, +gridDim.x, ... through a 3-slot TMA map/slot ring with
+mbarrier parity flips, cp.async gathers of the next batch and (ZL = 2/3)
+TMA-staged factor blocks.  Golden meshes have <= 36 elements, so there each
+CTA runs ONE batch.  Here every degree p = 2..8 runs on a mesh large enough
+that every CTA walks >= 4 batches (asserted from the launch shape the
+library reports, fb_last_fast_launch), for EVERY compiled launch shape of the
+degree (g_fast_cfg variants 0-7, incl. the ZL = 2/3 factor-staged ones), and
+the result is compared with the numpy oracle (oracle/sumfact.py, pinned to
+the reference's goldens) at 1e-12: Helmholtz c = 10 on a perturbed mesh with
+device-built factors (the bench's configuration), vdim 1 and 3, plus
+stiffness / mass at the default shape.  Meshes are non-cubic so the last
+batch is ragged.  p = 1 (trilinear one-thread-per-element kernel) runs with
+an element count that is not a multiple of the 32-element interleave.
+Reference: mfop.py:190-244, fespace.py:282-292."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from tests.cases import rel_err
+
+# p -> element counts (>= 4 batches per persistent CTA for every variant)
+COUNTS = {1: (40, 37, 33), 2: (37, 35, 34), 3: (30, 29, 28), 4: (25, 24, 23), 5: (22, 21, 20),
+          6: (21, 20, 20), 7: (18, 17, 17), 8: (16, 15, 14)}
+VDIM3_COUNTS = {2: (37, 35, 34), 4: (25, 24, 23), 5: (22, 21, 20), 7: (18, 17, 17),
+                8: (16, 15, 14)}
+
+_cache = {}
+
+
+def _problem(p, counts, kind="helmholtz", vdim=1):
+    key = (p, counts, kind, vdim)
+    if key in _cache:
+        return _cache[key]
+    from oracle import sumfact
+    from paper_1910_03032_b200 import geometry, mfop, spaces
+    m = geometry.perturb_mesh(geometry.cartesian_mesh(counts), 0.05, seed=3)
+    sp = spaces.FESpace(m, p, vdim=vdim)
+    hg = geometry.compute_geometric_factors(m, sp.basis.quad)
+    dg = geometry.DeviceGeometry(m, sp.basis.quad)
+    kw = {"mass": {}, "stiffness": {"nu": 1.0}, "helmholtz": {"c": 10.0, "nu": 1.0}}[kind]
+    op = mfop.setup(kind, space=sp, geom=dg, **kw)
+    assert op.fast_path
+    x = np.random.default_rng(p).standard_normal(sp.ndofs)
+    want = sumfact.make_square(kind, sp, hg, c=kw.get("c", 0.0), nu=kw.get("nu", 1.0))(x)
+    _cache.clear()
+    _cache[key] = (op, x, want)
+    return _cache[key]
+
+
+def _launch():
+    from paper_1910_03032_b200 import _lib
+    g, nb, ne = C.c_int(0), C.c_int(0), C.c_int(0)
+    _lib.check(_lib.lib.fb_last_fast_launch(C.byref(g), C.byref(nb), C.byref(ne)))
+    return g.value, nb.value, ne.value
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,variant", [(p, v) for p in range(2, 9) for v in range(8)])
+def test_fused_kernel_multibatch_matches_oracle(p, variant):
+    from paper_1910_03032_b200 import _lib
+    op, x, want = _problem(p, COUNTS[p])
+    try:
+        _lib.check(_lib.lib.fb_set_fast_config(p, variant))
+        y = op.apply(x)
+        grid, nbatch, ne_b = _launch()
+    finally:
+        _lib.check(_lib.lib.fb_set_fast_config(p, -1))
+    ne = op.space.mesh.num_elements
+    assert nbatch == -(-ne // ne_b)
+    assert nbatch >= 4 * grid, (grid, nbatch)  # every CTA walks >= 4 batches
+    assert rel_err(y, want) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", sorted(VDIM3_COUNTS))
+def test_fused_kernel_multibatch_vector_matches_oracle(p):
+    op, x, want = _problem(p, VDIM3_COUNTS[p], vdim=3)
+    y = op.apply(x)
+    grid, nbatch, _ = _launch()
+    assert nbatch >= 4 * grid, (grid, nbatch)
+    assert rel_err(y, want) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+@pytest.mark.parametrize("kind", ["mass", "stiffness"])
+def test_fused_kernel_multibatch_kinds(p, kind):
+    # mass keeps two work buffers per element: more CTAs are resident
+    counts = tuple(int(round(c * 1.15)) for c in COUNTS[p]) if kind == "mass" else COUNTS[p]
+    op, x, want = _problem(p, counts, kind=kind)
+    y = op.apply(x)
+    grid, nbatch, _ = _launch()
+    assert nbatch >= 4 * grid, (grid, nbatch)
+    assert rel_err(y, want) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["helmholtz", "stiffness", "mass"])
+def test_trilinear_kernel_ragged_matches_oracle(kind):
+    op, x, want = _problem(1, COUNTS[1], kind=kind)
+    assert op.space.mesh.num_elements % 32 != 0
+    y = op.apply(x)
+    assert rel_err(y, want) < 1e-12
+
+
+@pytest.mark.gpu
+def test_multibatch_apply_is_bitwise_deterministic():
+    import torch
+    op, x, _ = _problem(5, COUNTS[5])
+    xd = torch.from_numpy(x).cuda()
+    y0 = op.apply(xd)
+    for _ in range(3):
+        assert torch.equal(op.apply(xd), y0)
