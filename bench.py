@@ -357,14 +357,24 @@ def lor_pcg_scale(cases=((4, 116), (7, 66)), c=C_HELM):
         torch.cuda.synchronize()
         ms = e[0].elapsed_time(e[1])
         N = prob["space"].ndofs_scalar
+        peak, _ = load_peaks()
+        lv = M.level_bytes()
+        vbytes = sum(l["bytes"] for l in lv)
+        vms = e[3].elapsed_time(e[4])
+        ams = e[2].elapsed_time(e[3])
+        abytes = algorithmic_bytes(N, prob["mesh"].num_elements, p)
         out[f"p{p}_{n}^3"] = {
             "dofs": N, "iterations": rep.iterations, "converged": rep.converged,
             "solve_ms": round(ms, 2), "ms_per_iteration": round(ms / max(rep.iterations, 1), 3),
-            "apply_ms": round(e[2].elapsed_time(e[3]), 3),
-            "vcycle_ms": round(e[3].elapsed_time(e[4]), 3),
+            "apply_ms": round(ams, 3), "apply_hbm_frac": round(abytes / (ams * 1e-3) / 1e9 / peak, 4),
+            "vcycle_ms": round(vms, 3), "vcycle_algorithmic_bytes": int(vbytes),
+            "vcycle_hbm_frac": round(vbytes / (vms * 1e-3) / 1e9 / peak, 4),
+            "vcycle_levels": [{k2: (int(v) if k2 != "kind" else v) for k2, v in l.items()}
+                              for l in lv],
             "setup_s": round(setup, 2), "levels": M.describe(),
             "mode": "scale: block-ILU(2^3 elements) smoother, Q1 level coarsened "
-                    "geometrically to a dense-inverse bottom",
+                    "geometrically (near-exact: coarse_cycles stationary h-cycles) to a "
+                    "dense-inverse bottom",
             "reference_iterations_1M": _golden_iterations().get({4: "p4_25", 7: "p7_14"}[p])}
         del prob, A, M, b, x, y
         gc.collect()
@@ -488,6 +498,62 @@ def callers(stokes_cases=((2, 2), (2, 4), (2, 6), (3, 2)), tgv=(5, 16, 4)):
         "steps": steps, "iterations_mass_pressure_helmholtz": its, "setup_s": round(setup, 2),
         "kinetic_energy": st.kinetic_energy(),
         "scheme": "BDF3/EXT3, dt 0.02, nu 1/1600; timed after the 3 start-up steps (setup_s)"}
+    return out
+
+
+def mixed_and_vector_ops(reps=10, target=TARGET_DOFS / 3):
+    """Device time and HBM-roofline fraction of the Stokes / projection
+    blocks: the fused mixed-degree kernel's G, G^T, D and
+    the vdim = 3 vector Laplacian, on perturbed cubes with ~`target` DoFs per
+    velocity component (cfg4 Taylor-Hood p=4/3, cfg5 equal order p=5).
+    Algorithmic bytes (k = d^2 = 9 for G/D): input + output
+    vectors + int32 maps of both spaces + stored factors."""
+    import torch
+    from paper_1910_03032_b200 import _lib, geometry, mfop, spaces
+    peak, _ = load_peaks()
+    out = {}
+    for pv, pp in ((4, 3), (5, 5)):
+        n = mesh_cells(pv, target)
+        m = geometry.perturb_mesh(geometry.cartesian_mesh((n, n, n)), 0.05, seed=1)
+        vs = spaces.FESpace(m, pv, vdim=3)
+        ps = spaces.FESpace(m, pp)
+        g = geometry.DeviceGeometry(m, vs.basis.quad)
+        ne, q3 = m.num_elements, (pv + 2) ** 3
+        nv, npd = vs.ndofs_scalar, ps.ndofs_scalar
+        G = mfop.GradientOperator(vs, ps, g)
+        D = mfop.DivergenceOperator(vs, ps, g)
+        L = mfop.StiffnessOperator(vs, g)
+        maps = 4.0 * ne * ((pv + 1) ** 3 + (pp + 1) ** 3)
+        cases = {
+            "G": (lambda a, b: G.apply_into(a, b), npd, 3 * nv,
+                  8.0 * (npd + 3 * nv) + maps + 72.0 * ne * q3),
+            "Gt": (lambda a, b: G.apply_transpose_into(a, b), 3 * nv, npd,
+                   8.0 * (npd + 3 * nv) + maps + 72.0 * ne * q3),
+            "D": (lambda a, b: D.apply_into(a, b), 3 * nv, npd,
+                  8.0 * (npd + 3 * nv) + maps + 72.0 * ne * q3),
+            "vector_laplacian": (lambda a, b: L.apply_into(a, b), 3 * nv, 3 * nv,
+                                 48.0 * nv + 4.0 * ne * (pv + 1) ** 3 + 48.0 * ne * q3),
+        }
+        res = {"velocity_dofs": 3 * nv, "pressure_dofs": npd, "elements": ne,
+               "fused_mixed": bool(_lib.lib.fb_operator_fast_path(G.handle) == 2)}
+        for name, (fn, nin, nout, by) in cases.items():
+            xa = torch.randn(nin, dtype=torch.float64, device="cuda")
+            ya = torch.empty(nout, dtype=torch.float64, device="cuda")
+            for _ in range(3):
+                fn(xa, ya)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                fn(xa, ya)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            res[name] = {"ms": round(ms, 4), "gdofs_in_plus_out": round((nin + nout) / ms / 1e6, 3),
+                         "hbm_frac": round(by / (ms * 1e-3) / 1e9 / peak, 4),
+                         "algorithmic_bytes": int(by)}
+        out[f"3d_pv{pv}_pp{pp}"] = res
+        del G, D, L, g
     return out
 
 
@@ -692,6 +758,10 @@ def run_ours(args, rank, world):
     if sharded is not None:
         line["lor_pcg_cfg3_sharded"] = sharded
     if not args.no_callers and world == 1:
+        try:
+            line["mixed_and_vector_ops"] = mixed_and_vector_ops()
+        except Exception as exc:
+            line["mixed_and_vector_ops"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         try:
             line["callers"] = callers()
         except Exception as exc:  # a caller failure must not drop the headline line

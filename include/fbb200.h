@@ -121,6 +121,10 @@ int fb_set_fast_config(int p, int variant);
  * CTAs, element batches and elements per batch (each CTA walks
  * nbatch / grid batches).  Test/diagnostic query. */
 int fb_last_fast_launch(int* grid, int* nbatch, int* elements_per_batch);
+/* Diagnostics (tools/pass_cost.py): skip the arithmetic of the fused
+ * kernel's passes P1..P9 whose bits are set in `mask` (results invalid);
+ * 0 restores normal operation. */
+int fb_set_fast_skip(int mask);
 /* Element-blocked factors (ne, K, nq1^dim) back to host, for verification. */
 int64_t fb_operator_factor_count(const fb_operator* op);
 int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count);
@@ -138,7 +142,8 @@ int fb_operator_apply_transpose(const fb_operator* op, const double* x_dev, doub
                                 void* stream);
 /* Bytes of device memory the operator owns (factors + matrices). */
 int64_t fb_operator_device_bytes(const fb_operator* op);
-/* 1 if the fused sm_100a fast path serves this operator, 0 for the general kernel. */
+/* 1 if the fused sm_100a kernel serves this square operator, 2 if the fused
+ * mixed-degree kernel serves this gradient / divergence, 0 for the general kernel. */
 int fb_operator_fast_path(const fb_operator* op);
 
 /* ConstrainedOperator.apply (mfop.py:428-433) around any operator apply:
@@ -228,6 +233,10 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr_host,
                        const int64_t* new2old_host, const int64_t* indptr_host,
                        const int64_t* indices_host, const double* data_host, fb_blockilu** out);
 void fb_blockilu_destroy(fb_blockilu* B);
+/* Sizes of the factor: rows, strict-lower / strict-upper entries (the
+ * V-cycle's algorithmic bytes), padded row width of the sweeps (0: CSR). */
+int fb_blockilu_info(const fb_blockilu* B, int64_t* n, int64_t* nnz_lower, int64_t* nnz_upper,
+                     int* ell_width);
 int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r_dev, double* out_dev,
                       void* stream);
 /* y = M x for a dense row-major n x n matrix (coarse-level inverse). */

@@ -45,6 +45,7 @@ _SIGS = [
     ("fb_operator_factor_count", _i64, [_vp]),
     ("fb_set_fast_config", _int, [_int, _int]),
     ("fb_last_fast_launch", _int, [_vp, _vp, _vp]),
+    ("fb_set_fast_skip", _int, [_int]),
     ("fb_operator_factors", _int, [_vp, _vp, _i64]),
     ("fb_operator_destroy", None, [_vp]),
     ("fb_operator_apply", _int, [_vp, _vp, _vp, _vp]),
@@ -82,6 +83,7 @@ _SIGS = [
                                     _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
     ("fb_host_free", None, [_vp]),
     ("fb_blockilu_create", _int, [_i64, _int, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)]),
+    ("fb_blockilu_info", _int, [_vp, _vp, _vp, _vp, _vp]),
     ("fb_blockilu_destroy", None, [_vp]),
     ("fb_blockilu_apply", _int, [_vp, _int, _vp, _vp, _vp]),
     ("fb_dense_mv", _int, [_i64, _vp, _vp, _vp, _vp]),

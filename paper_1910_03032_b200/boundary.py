@@ -302,14 +302,24 @@ class RotationalMatrix:
         return dev.to_host(y) if host else y
 
 
-_CACHE = {}
+# Face matrices are cached ON the space objects they belong to (attribute
+# `_fb_face_cache`), so a cached matrix lives exactly as long as its space and
+# a new space can never pick up a stale matrix through a recycled id().
+_CACHE_ATTR = "_fb_face_cache"
 
 
-def _cached(key, make):
-    obj = _CACHE.get(key)
+def _cached(owner, key, make):
+    cache = getattr(owner, _CACHE_ATTR, None)
+    if cache is None:
+        cache = {}
+        try:
+            setattr(owner, _CACHE_ATTR, cache)
+        except AttributeError:  # an object without a __dict__: no caching
+            return make()
+    obj = cache.get(key)
     if obj is None:
         obj = make()
-        _CACHE[key] = obj
+        cache[key] = obj
     return obj
 
 
@@ -319,8 +329,8 @@ def _attr_key(attributes):
 
 def flux_matrix(space, attributes=None, n_quad=None):
     """The cached NormalFluxMatrix of (space, attributes, n_quad)."""
-    key = ("flux", id(space), _attr_key(attributes), n_quad)
-    return _cached(key, lambda: NormalFluxMatrix(space, attributes, n_quad))
+    key = ("flux", _attr_key(attributes), n_quad)
+    return _cached(space, key, lambda: NormalFluxMatrix(space, attributes, n_quad))
 
 
 def boundary_normal_flux(space, g, attributes=None, n_quad=None):
@@ -332,13 +342,20 @@ def boundary_normal_flux(space, g, attributes=None, n_quad=None):
 def boundary_rotational_rhs(vspace, pspace, u, nu=1.0, attributes=None, n_quad=None):
     """r_j = -nu sum_faces int (n x curl u) . grad psi_j (mfop.py:687-807).
     A device tensor u gives a device result; a host array gives a host array."""
-    key = ("rot", id(vspace), id(pspace), float(nu), _attr_key(attributes), n_quad)
-    M = _cached(key, lambda: RotationalMatrix(vspace, pspace, nu, attributes, n_quad))
+    # keyed on the pressure space too, held strongly by the matrix (M.pspace)
+    key = ("rot", id(pspace), float(nu), _attr_key(attributes), n_quad)
+    M = _cached(vspace, key, lambda: RotationalMatrix(vspace, pspace, nu, attributes, n_quad))
+    if getattr(M, "_pspace_ref", pspace) is not pspace:  # a recycled id(): rebuild
+        M = RotationalMatrix(vspace, pspace, nu, attributes, n_quad)
+        getattr(vspace, _CACHE_ATTR)[key] = M
+    M._pspace_ref = pspace
     return M(u)
 
 
-def clear_cache():
-    _CACHE.clear()
+def clear_cache(*spaces):
+    for sp_ in spaces:
+        if hasattr(sp_, _CACHE_ATTR):
+            getattr(sp_, _CACHE_ATTR).clear()
 
 
 __all__ = ["NormalFluxMatrix", "RotationalMatrix", "boundary_normal_flux", "flux_matrix",

@@ -1005,6 +1005,16 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
   return FB_OK;
 }
 
+int fb_blockilu_info(const fb_blockilu* B, int64_t* n, int64_t* nnz_lower, int64_t* nnz_upper,
+                     int* ell_width) {
+  FB_REQUIRE(B != nullptr, "block ILU is NULL");
+  if (n) *n = B->n;
+  if (nnz_lower) *nnz_lower = B->L.ix.n;   // strict lower triangle (unit diagonal)
+  if (nnz_upper) *nnz_upper = B->U.ix.n;   // strict upper triangle (+ inverse diagonal)
+  if (ell_width) *ell_width = B->ell_w;
+  return FB_OK;
+}
+
 void fb_blockilu_destroy(fb_blockilu* B) {
   if (B) debug_canary_unregister(B->block_ptr.ptr);
   delete B;

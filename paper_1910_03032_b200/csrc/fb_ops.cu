@@ -11,6 +11,7 @@
 #include "fb_common.cuh"
 #include "fb_internal.cuh"
 #include "sf3_fast.cuh"
+#include "sf3_mixed.cuh"
 #include "sf3_q1.cuh"
 #include "sf_general.cuh"
 
@@ -161,7 +162,19 @@ struct fb_operator {
   int64_t S_comp_stride = 0;
   int gen_kind = 0;
   size_t gen_smem = 0;
+  bool mixed = false;  // fused 3D G / G^T / D kernel (sf3_mixed.cuh)
+  SF3MParams mp;
 };
+
+extern "C" {
+static int mixed_apply(const fb_operator* op, int mkind, const double* x, double* y, int part,
+                       cudaStream_t st);
+}
+
+namespace fb {
+bool mixed_supported(int nv, int np, int nq);
+int launch_mixed(int nv, int np, int kind, const SF3MParams& P, cudaStream_t st);
+}  // namespace fb
 
 namespace {
 
@@ -198,6 +211,7 @@ void diff_matrix(const double* x, int n, double* D) {
 // shape of the last fused-kernel launch on this host thread (tests: prove the
 // persistent multi-batch path ran; fb_last_fast_launch)
 thread_local int g_last_grid = 0, g_last_nbatch = 0, g_last_ne = 0;
+int g_fast_skip = 0;  // diagnostics only (fb_set_fast_skip): passes to skip
 
 template <int N, int Q, int KIND, int NE, int NT, int MINB, int ZL>
 int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
@@ -218,6 +232,7 @@ int launch_fast_t(const fb_operator* op, const double* x, double* y, cudaStream_
   p.x = x;
   p.y = y;
   p.nbatch = ceil_div(op->rv->ne, NE);
+  p.skip = g_fast_skip;
   const int grid = p.nbatch < resident ? p.nbatch : resident;
   g_last_grid = grid;
   g_last_nbatch = p.nbatch;
@@ -245,8 +260,8 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // with the z-line schedule: +9 %, p = 5:
 // +14 %, p = 2, 6: +1-2 %); at p = 7, 8 the extra 41-56 KB per CTA costs more
 // occupancy than it saves.
-static const int kFastCfgDefault[9] = {0, 0, 3, 5, 6, 5, 4, 0, 0};
-static int g_fast_cfg[9] = {0, 0, 3, 5, 6, 5, 4, 0, 0};
+static const int kFastCfgDefault[9] = {0, 0, 0, 5, 6, 5, 0, 0, 6};
+static int g_fast_cfg[9] = {0, 0, 0, 5, 6, 5, 0, 0, 6};
 
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   const int v = g_fast_cfg[op->rv->p < 9 ? op->rv->p : 0];
@@ -423,6 +438,33 @@ static int finish_operator(fb_operator* op, const double* points, const double* 
     op->S_comp_stride = ne * rv->nb;  // == number of transposed-CSR slots
     FB_TRY_CUDA(op->S.alloc(op->S_comp_stride * vdim));
     fp.S = op->S.ptr;
+  } else if ((kind == FB_GRADIENT || kind == FB_DIVERGENCE) && dim == 3 && rp != nullptr &&
+             mixed_supported(rv->n, rp->n, nq1) && rv->split_ok && rp->split_ok) {
+    // fused mixed-degree path (K1g): even-odd forms of B_v, B_p, Dq and transposes
+    op->mixed = true;
+    SF3MParams& mp = op->mp;
+    std::memset(&mp, 0, sizeof(mp));
+    const int nv = rv->n, np = rp->n;
+    std::vector<double> Dq(nq1 * nq1), Dt(nq1 * nq1), Bvt(size_t(nv) * nq1), Bpt(size_t(np) * nq1);
+    diff_matrix(points, nq1, Dq.data());
+    for (int a = 0; a < nq1; ++a)
+      for (int b = 0; b < nq1; ++b) Dt[b * nq1 + a] = Dq[a * nq1 + b];
+    for (int q = 0; q < nq1; ++q) {
+      for (int i = 0; i < nv; ++i) Bvt[i * nq1 + q] = B[q * nv + i];
+      for (int i = 0; i < np; ++i) Bpt[i * nq1 + q] = Bp[q * np + i];
+    }
+    eo_fill(mp.eBv, B, nq1, nv);
+    eo_fill(mp.eBvt, Bvt.data(), nv, nq1);
+    eo_fill(mp.eBp, Bp, nq1, np);
+    eo_fill(mp.eBpt, Bpt.data(), np, nq1);
+    eo_fill(mp.eD, Dq.data(), nq1, nq1);
+    eo_fill(mp.eDt, Dt.data(), nq1, nq1);
+    mp.fac = op->fac.ptr;
+    mp.ne = ne;
+    mp.fstride = op->fstride;
+    const int64_t sv = ne * rv->nb, sp_ = ne * rp->nb;
+    FB_TRY_CUDA(op->S.alloc(std::max(3 * sv, sp_)));
+    mp.S = op->S.ptr;
   } else {
     // general path
     const int nv = rv->n, np = op->np;
@@ -750,6 +792,11 @@ int fb_operator_factors(const fb_operator* op, double* host_out, int64_t count) 
 
 int64_t fb_operator_factor_count(const fb_operator* op) { return op ? op->fac.n : 0; }
 
+int fb_set_fast_skip(int mask) {
+  g_fast_skip = mask;
+  return FB_OK;
+}
+
 int fb_last_fast_launch(int* grid, int* nbatch, int* elements_per_batch) {
   if (grid) *grid = g_last_grid;
   if (nbatch) *nbatch = g_last_nbatch;
@@ -770,7 +817,7 @@ int64_t fb_operator_device_bytes(const fb_operator* op) {
   return int64_t(op->fac.bytes() + op->mats.bytes() + op->S.bytes());
 }
 
-int fb_operator_fast_path(const fb_operator* op) { return op && op->fast ? 1 : 0; }
+int fb_operator_fast_path(const fb_operator* op) { return !op ? 0 : op->fast ? 1 : op->mixed ? 2 : 0; }
 
 static int general_apply(const fb_operator* op, int gkind, const double* x, double* y,
                          cudaStream_t st) {
@@ -848,14 +895,44 @@ int fb_operator_apply_part(const fb_operator* op, const double* x, double* y, in
     return scatter_rows(op->rv, true, op->S.ptr, op->S_comp_stride, y, op->rv->ndofs,
                         op->vdim, st);
   }
+  if (op->mixed)
+    return mixed_apply(op, op->kind == FB_GRADIENT ? kMxGrad : kMxDiv, x, y, part, st);
   FB_REQUIRE(part == 0, "split apply is only available on the fused path");
   return fb_operator_apply(op, x, y, stream);
+}
+
+// fused mixed-degree apply: kernel (part != 2), then the output space's slot sum
+static int mixed_apply(const fb_operator* op, int mkind, const double* x, double* y, int part,
+                       cudaStream_t st) {
+  const fb_restriction* rv = op->rv;
+  const fb_restriction* rp = op->rp;
+  const fb_restriction* rin = (mkind == kMxGrad) ? rp : rv;
+  const fb_restriction* rout = (mkind == kMxGrad) ? rv : rp;
+  SF3MParams P = op->mp;
+  P.x = x;
+  P.y = y;
+  P.map_in = rin->map.ptr;
+  P.map_out = rout->map.ptr;
+  P.spos_out = rout->s_pos.ptr;
+  P.nbp_out = rout->nbp;
+  P.in_comp_stride = rin->ndofs;
+  P.out_comp_stride = rout->ndofs;
+  P.S_comp_stride = rv->ne * rout->nb;
+  const int ncomp = (mkind == kMxGrad) ? 3 : 1;
+  if (part != 2 && rv->ne > 0) {
+    int rc = launch_mixed(rv->n, rp->n, mkind, P, st);
+    if (rc != FB_OK) return rc;
+  }
+  if (part == 1) return FB_OK;
+  return scatter_rows(rout, true, op->S.ptr, P.S_comp_stride, y, rout->ndofs, ncomp, st);
 }
 
 int fb_operator_apply(const fb_operator* op, const double* x, double* y, void* stream) {
   FB_REQUIRE(op != nullptr, "operator is NULL");
   cudaStream_t st = as_stream(stream);
   if (op->fast) return fb_operator_apply_part(op, x, y, 0, stream);
+  if (op->mixed)
+    return mixed_apply(op, op->kind == FB_GRADIENT ? kMxGrad : kMxDiv, x, y, 0, st);
   int gk = kgMass;
   switch (op->kind) {
     case FB_MASS: gk = kgMass; break;
@@ -873,6 +950,7 @@ int fb_operator_apply_transpose(const fb_operator* op, const double* x, double* 
                                 void* stream) {
   FB_REQUIRE(op != nullptr, "operator is NULL");
   FB_REQUIRE(op->kind == FB_GRADIENT, "apply_transpose is defined for the gradient only");
+  if (op->mixed) return mixed_apply(op, kMxGradT, x, y, 0, as_stream(stream));
   return general_apply(op, kgGradT, x, y, as_stream(stream));
 }
 

@@ -146,6 +146,7 @@ struct SF3Params {
   int64_t S_comp_stride;
   int vdim;
   int nbatch;                      // ceil(ne / NE)
+  int skip;                        // diagnostics: bit k skips the work of pass Pk (fb_set_fast_skip)
   double B[kMaxQ1][kMaxQ1];        // B[q][i]  basis values at rule points
   double Dq[kMaxQ1][kMaxQ1];       // Dq[q][r] collocated derivative at rule points
   EOMat eB, eBt, eD, eDt;          // even-odd forms of B, B^T, Dq, Dq^T (eo_fill)
@@ -213,7 +214,9 @@ struct SF3Shape {
   static constexpr int OFF_WORK = round_up(OFF_X + NE * XBUF * 8, 16);
   static constexpr int ES = NBUF * BUF + SF3Pitch<Q>::PAD;  // element stride (doubles)
   static constexpr int OFF_FAC = round_up(OFF_WORK + NE * ES * 8, 16);
-  static constexpr int SMEM = OFF_FAC + (FSTAGE ? NE * FACP * 8 : 0);
+  // per local DoF: -1 (element interior) or its element-boundary rank
+  static constexpr int OFF_TBL = round_up(OFF_FAC + (FSTAGE ? NE * FACP * 8 : 0), 16);
+  static constexpr int SMEM = OFF_TBL + round_up(NLOC * 2, 16);
 };
 
 // rank of lattice position (k,j,i) among the element-boundary positions of
@@ -395,6 +398,13 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
     for (int h = 0; h < Sh::NSTAGE + (Sh::FSTAGE ? 1 : 0); ++h) mbar_init(smem_u32(&bars[h]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  int16_t* btbl = reinterpret_cast<int16_t*>(smem_raw + Sh::OFF_TBL);
+  for (int l = tid; l < NLOC; l += NT) {
+    const int i = l % N, j = (l / N) % N, k = l / (N * N);
+    const bool inner = i > 0 && i < N - 1 && j > 0 && j < N - 1 && k > 0 && k < N - 1;
+    btbl[l] = inner ? int16_t(-1) : int16_t(boundary_rank3<N>(k, j, i));
+  }
+  const bool direct_out = (P.skip >> 12) & 1;  // diagnostics: the line-order stores
   __syncthreads();
 
   int batch = blockIdx.x;
@@ -435,7 +445,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 
       // ---- P1: x-lines (k,j): gather buffer -> b1 --------------------------
 #pragma unroll 1
-      for (int L = tid; L < NE * N * N; L += NT) {
+      for (int L = tid + (((P.skip >> 1) & 1) << 28); L < NE * N * N; L += NT) {
         const int el = L / (N * N), r = L - el * N * N;
         const int k = r / N, j = r - k * N;
         const double* in = sx + el * Sh::XBUF + XI(k, j, 0);
@@ -459,7 +469,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 
       // ---- P2: y-lines (k,a): b1 -> b0 ------------------------------------
 #pragma unroll 1
-      for (int L = tid; L < NE * N * Q; L += NT) {
+      for (int L = tid + (((P.skip >> 2) & 1) << 28); L < NE * N * Q; L += NT) {
         const int el = L / (N * Q), r = L - el * N * Q;
         const int k = r / Q, a = r - k * Q;
         const double* in = smem + el * ES + BUF + IX(k, 0, a);
@@ -476,7 +486,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       if constexpr (ZL != 1 && ZL != 3) {
       // ---- P3: z-lines (b,a): b0 -> U (b0 in place), Gz = Dq_z U (b3) -------
 #pragma unroll 1
-      for (int L = tid; L < NE * Q2; L += NT) {
+      for (int L = tid + (((P.skip >> 3) & 1) << 28); L < NE * Q2; L += NT) {
         const int el = L / Q2, r = L - el * Q2;
         const int b = r / Q, a = r - b * Q;
         double* base = smem + el * ES;
@@ -508,7 +518,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       if (KIND != kMass) {
         // ---- P4: derivative lines: x (c,b) b0 -> b1; y (c,a) b0 -> b2 -----
 #pragma unroll 1
-        for (int L = tid; L < NE * Q2; L += NT) {
+        for (int L = tid + (((P.skip >> 4) & 1) << 28); L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int c = r / Q, t = r - c * Q;
           double* base = smem + el * ES;
@@ -544,7 +554,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         // more loads in flight against the L2 latency
         constexpr int P5U = Sh::FSTAGE ? 2 : ((Q == 9) ? 5 : 2);  // p = 7 +3 %; p = 8 loses to register pressure
 #pragma unroll 1
-        for (int L = tid; L < nel * Q2; L += NT) {
+        for (int L = tid + (((P.skip >> 5) & 1) << 28); L < nel * Q2; L += NT) {
           const int el = L / Q2, ba = L - el * Q2;
           double* col = smem + el * ES + IX(0, ba / Q, ba % Q);
           const double* __restrict__ f =
@@ -571,7 +581,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 
         // ---- P6: transposed derivative lines, in place: x b1, y b2, z b3 ---
 #pragma unroll 1
-        for (int L = tid; L < NE * Q2; L += NT) {
+        for (int L = tid + (((P.skip >> 6) & 1) << 28); L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int c = r / Q, t = r - c * Q;
           double* base = smem + el * ES;
@@ -598,7 +608,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 
         // ---- P7: transposed z-lines (b,a): (b0+b1+b2+b3) -> b0[k<N] --------
 #pragma unroll 1
-        for (int L = tid; L < NE * Q2; L += NT) {
+        for (int L = tid + (((P.skip >> 7) & 1) << 28); L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int b = r / Q, a = r - b * Q;
           double* base = smem + el * ES;
@@ -619,7 +629,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       } else {
       // ---- P3: z-lines (b,a): b0 -> U (b0 in place) ---------------------------
 #pragma unroll 1
-      for (int L = tid; L < NE * Q2; L += NT) {
+      for (int L = tid + (((P.skip >> 3) & 1) << 28); L < NE * Q2; L += NT) {
         const int el = L / Q2, r = L - el * Q2;
         const int b = r / Q, a = r - b * Q;
         double* base = smem + el * ES;
@@ -646,7 +656,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       if (KIND != kMass) {
         // ---- P4: derivative lines: x (c,b) b0 -> b1; y (c,a) b0 -> b2 -----
 #pragma unroll 1
-        for (int L = tid; L < NE * Q2; L += NT) {
+        for (int L = tid + (((P.skip >> 4) & 1) << 28); L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int c = r / Q, t = r - c * Q;
           double* base = smem + el * ES;
@@ -679,7 +689,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         }
         auto ldf = [&](const double* p_) { return Sh::FSTAGE ? *p_ : ld_evict_first(p_, fpol); };
 #pragma unroll 1
-        for (int L = tid; L < nel * Q2; L += NT) {
+        for (int L = tid + (((P.skip >> 5) & 1) << 28); L < nel * Q2; L += NT) {
           const int el = L / Q2, ba = L - el * Q2;
           const int b = ba / Q, a = ba - b * Q;
           double* col = smem + el * ES + IX(0, b, a);
@@ -714,7 +724,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 
         // ---- P6: transposed derivative lines, in place: x b1, y b2 ---------
 #pragma unroll 1
-        for (int L = tid; L < NE * Q2; L += NT) {
+        for (int L = tid + (((P.skip >> 6) & 1) << 28); L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int c = r / Q, t = r - c * Q;
           double* base = smem + el * ES;
@@ -737,7 +747,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 
         // ---- P7: transposed z-lines (b,a): (b0+b1+b2) -> b0[k<N] -----------
 #pragma unroll 1
-        for (int L = tid; L < NE * Q2; L += NT) {
+        for (int L = tid + (((P.skip >> 7) & 1) << 28); L < NE * Q2; L += NT) {
           const int el = L / Q2, r = L - el * Q2;
           const int b = r / Q, a = r - b * Q;
           double* base = smem + el * ES;
@@ -757,7 +767,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       }
       // ---- P8: transposed y-lines (k,a): b0[k][b<Q][a] -> b1[k][j<N][a] ----
 #pragma unroll 1
-      for (int L = tid; L < NE * N * Q; L += NT) {
+      for (int L = tid + (((P.skip >> 8) & 1) << 28); L < NE * N * Q; L += NT) {
         const int el = L / (N * Q), r = L - el * N * Q;
         const int k = r / Q, a = r - k * Q;
         const double* in = smem + el * ES + IX(k, 0, a);
@@ -773,7 +783,7 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 
       // ---- P9: transposed x-lines (k,j): b1[k][j][a<Q] -> y_e, then E->L --
 #pragma unroll 1
-      for (int L = tid; L < nel * N * N; L += NT) {
+      for (int L = tid + (((P.skip >> 9) & 1) << 28); L < nel * N * N; L += NT) {
         const int el = L / (N * N), r = L - el * N * N;
         const int k = r / N, j = r - k * N;
         const double* in = smem + el * ES + BUF + IX(k, j, 0);
@@ -781,17 +791,39 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 #pragma unroll
         for (int a = 0; a < Q; ++a) v[0][a] = in[a];
         eo_lines<N, Q, 1, 1>(P.eBt, v, w);
+        if (!direct_out) {  // element result to b0 (free after P8), stored below
+          double* o = smem + el * ES + (k * N + j) * N;
+#pragma unroll
+          for (int i = 0; i < N; ++i) o[i] = w[0][i];
+          continue;
+        }
         const bool edge_line = (k == 0 || k == N - 1 || j == 0 || j == N - 1);
         const int* mrow = smap + el * NLOCP + (k * N + j) * N;
         const int* prow = spos + el * NBP;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           const double acc = w[0][i];
-          if (!edge_line && i > 0 && i < N - 1) {
+          if ((P.skip >> 10) & 1) {  // diagnostics: keep the result in shared memory
+            sx[i] = acc;
+          } else if (!edge_line && i > 0 && i < N - 1) {
             y[mrow[i]] = 0.0 + acc;  // bincount semantics: 0.0 + contribution
-          } else {
+          } else if (!((P.skip >> 11) & 1)) {
             S[prow[boundary_rank3<N>(k, j, i)]] = acc;
           }
+        }
+      }
+      if (!direct_out) {
+        // ---- output: consecutive threads store consecutive local DoFs, so
+        // an element's interior block (contiguous in y) and its runs of
+        // transposed-map slots are written with coalesced stores
+        __syncthreads();
+#pragma unroll 4
+        for (int L = tid; L < nel * NLOC; L += NT) {
+          const int el = L / NLOC, l = L - el * NLOC;
+          const double v = smem[el * ES + l];
+          const int rk = btbl[l];
+          if (rk < 0) y[smap[el * NLOCP + l]] = 0.0 + v;  // bincount: 0.0 + contribution
+          else S[spos[el * NBP + rk]] = v;
         }
       }
     }

@@ -29,6 +29,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 import torch
 
+from . import _lib
 from . import device as dev
 from . import lor as lor_mod
 from . import vec
@@ -145,6 +146,23 @@ class MeanProjector(_DeviceMixin):
         num = vec.workspace(n).scalars[15:16]
         vec.dot_into(self._w, v, num, stream)
         vec.shift_ratio(v, num, self._den, out, stream)
+        return out
+
+
+class _StreamMeanProjector(MeanProjector):
+    """MeanProjector with private reduction scratch (no shared vec.workspace
+    slot), for preconditioner clones running on concurrent streams."""
+
+    def apply_into(self, v, out, stream=None):
+        n = v.shape[0]
+        if self._w is None or self._w.shape[0] != n:
+            self._w = torch.ones(n, dtype=torch.float64, device=dev.device())
+            self._den = float(n)
+            self._num = dev.zeros(1)
+            self._part = dev.zeros(int(_lib.lib.fb_dot_partials(n)))
+        _lib.check(_lib.lib.fb_dot(n, self._w.data_ptr(), v.data_ptr(), self._part.data_ptr(),
+                                   self._num.data_ptr(), vec._st(stream)))
+        vec.shift_ratio(v, self._num, self._den, out, stream)
         return out
 
 
@@ -838,6 +856,8 @@ class LORPreconditioner(_DeviceMixin):
         if self.smoother_kind != "block" or not isinstance(self._bottom, DenseInverseSolver):
             return None
         c = copy.copy(self)
+        if self._proj is not None:  # own projector: its reduction scratch is per stream
+            c._proj = _StreamMeanProjector()
         c._x = [dev.empty(t.shape[0]) for t in self._x]
         c._r = [dev.empty(t.shape[0]) for t in self._r]
         c._t = [dev.empty(t.shape[0]) for t in self._t]

@@ -407,6 +407,39 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
             c._rk = c._dk = None
         return c
 
+    def level_bytes(self):
+        """Algorithmic HBM bytes of one V-cycle, per level (each datum of the
+        cycle's kernels read or written once; CSR / factor entries 12 B = fp64
+        value + int32 column, vectors 8 B per row):
+          smoother sweep  12 (nnz_L + nnz_U) + 8 n (inverse diagonal) + 16 n (in, out)
+          residual        12 nnz(A) + 24 n  (x, r in; t out)
+          transfers       8 (n + n_coarse) each way;  axpby 24 n (twice)
+        per non-bottom level: 2 sweeps + 2 residuals + both transfers + 2 axpbys;
+        the Q1 sub-hierarchy is traversed `coarse_cycles` times (plus one
+        residual and one axpby per extra cycle); bottom: dense GEMV 8 nc^2."""
+        out = []
+        k = self.coarse_cycles
+        nl = len(self.levels)
+        for i, (sp_, A) in enumerate(self.levels):
+            n = sp_.ndofs_scalar
+            rep = k if i >= self.q1_index else 1
+            if i == nl - 1:
+                out.append({"rows": n, "bytes": rep * (8.0 * n * n + 16.0 * n), "kind": "dense"})
+                continue
+            lo, up = C.c_int64(0), C.c_int64(0)
+            sm = self.smoothers[i]
+            if getattr(sm, "handle", None) is not None:
+                _lib.check(_lib.lib.fb_blockilu_info(sm.handle, None, C.byref(lo), C.byref(up),
+                                                     None))
+            nnz = A.nnz
+            nc = self.spaces[i + 1].ndofs_scalar
+            per = (2 * (12.0 * (lo.value + up.value) + 24.0 * n) + 2 * (12.0 * nnz + 24.0 * n)
+                   + 2 * 8.0 * (n + nc) + 2 * 24.0 * n)
+            extra = (k - 1) * (12.0 * nnz + 24.0 * n + 24.0 * n) if i == self.q1_index else 0.0
+            out.append({"rows": n, "nnz_A": nnz, "nnz_ilu": lo.value + up.value,
+                        "bytes": rep * per + extra})
+        return out
+
     def describe(self):
         return {"coarse_cycles": self.coarse_cycles, "q1_index": self.q1_index,
                 "levels": [{"p": s.p, "counts": list(s.counts), "rows": s.ndofs_scalar,

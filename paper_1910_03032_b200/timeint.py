@@ -253,3 +253,15 @@ class ProjectionStepper:
         """Volume-averaged kinetic energy u' M u / (2 |Omega|)."""
         v = self.u if u is None else u
         return float(vec.dot(v, self.M.apply(v))) / (2.0 * self._volume)
+
+    def divergence_residual(self, u=None):
+        """Euclidean norm of the weak divergence of the current velocity
+        (timeint.py:397-400).  u may be a host array or a device tensor."""
+        v = self.u if u is None else dev.to_device(u)
+        w = self.D.apply(v)
+        return float(torch.linalg.norm(w)) if torch.is_tensor(w) else float(np.linalg.norm(w))
+
+    def state_host(self):
+        """(u, p) as host numpy arrays -- the reference stepper's `u` / `p`
+        attributes are numpy; here they stay device tensors between steps."""
+        return dev.to_host(self.u), dev.to_host(self.p)

@@ -21,6 +21,11 @@ def main(rep, top=40):
             continue
         if kern and h and len(r) == len(h):
             out[kern].append(r)
+    if not out or not any(out.values()):
+        print("unparsed; first rows:")
+        for r in rows[:12]:
+            print(r[:12])
+        return
     for k, v in out.items():
         try:
             si = h.index("Warp Stall Sampling (All Samples)")
