@@ -296,6 +296,9 @@ int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks, const int64_t* bloc
  * warp serves 32/lanes blocks), 0 = chosen from the block size.  Same
  * results in every mode. */
 int fb_set_blockilu_pipeline(int mode, int lanes);
+/* 1 (default): factors created afterwards with blocks of more than 160 rows
+ * use the level-packed layout and the TMA-ring sweep; 0: CSR / ELL sweeps. */
+int fb_set_blockilu_packed(int on);
 /* Nodal interpolation between two levels of a structured box, matrix-free
  * (lor.py:102-123).  fine: map of the fine level (ne, nf^3); hmap: for each
  * fine element the coarse DoFs of its parent coarse element (ne, nc^3);
@@ -316,6 +319,27 @@ int fb_index_add(int64_t n, const int* idx_dev, const double* v_dev, double* y_d
 int fb_transfer_prolong(const fb_transfer* T, const double* xc_dev, double* xf_dev, void* stream);
 /* xc = P^T xf (deterministic) */
 int fb_transfer_restrict(const fb_transfer* T, const double* xf_dev, double* xc_dev, void* stream);
+
+/* ---- device-resident Krylov loops (fb_graph.cu) ---------------------------
+ * A CUDA graph holding one conditional WHILE node; the body is captured from
+ * a stream (begin / launches of one solver iteration / end) and the loop is
+ * continued or stopped on the device by the check kernel. */
+typedef struct fb_while_graph fb_while_graph;
+int fb_while_graph_create(fb_while_graph** out);
+unsigned long long fb_while_graph_handle(const fb_while_graph* G);
+int fb_while_graph_begin(fb_while_graph* G, void* stream);
+int fb_while_graph_end(fb_while_graph* G, void* stream);
+int fb_while_graph_launch(const fb_while_graph* G, void* stream);
+void fb_while_graph_destroy(fb_while_graph* G);
+/* PCG stopping test of solvers.py:141-165 on device scalars s = [rz, pAp,
+ * alpha, rz_new, beta]: state = [iterations, stop reason, max_iters],
+ * hist[it] = relres, cfg = [norm0, rel_tol]; in a graph (in_graph = 1) it
+ * sets the WHILE condition, pausing before every `period`-th iteration. */
+int fb_cg_check(unsigned long long handle, int in_graph, double* s_dev, int* state_dev,
+                double* hist_dev, const double* cfg_dev, int period, void* stream);
+/* p = z + beta_dev[0] p */
+int fb_xpby_dev(int64_t n, const double* z_dev, const double* beta_dev, double* p_dev,
+                void* stream);
 
 #ifdef __cplusplus
 }

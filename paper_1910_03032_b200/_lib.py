@@ -59,6 +59,14 @@ _SIGS = [
     ("fb_dot_partials", _i64, [_i64]),
     ("fb_dot", _int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     ("fb_cg_update", _int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp]),
+    ("fb_while_graph_create", _int, [C.POINTER(_vp)]),
+    ("fb_while_graph_handle", C.c_ulonglong, [_vp]),
+    ("fb_while_graph_begin", _int, [_vp, _vp]),
+    ("fb_while_graph_end", _int, [_vp, _vp]),
+    ("fb_while_graph_launch", _int, [_vp, _vp]),
+    ("fb_while_graph_destroy", None, [_vp]),
+    ("fb_cg_check", _int, [C.c_ulonglong, _int, _vp, _vp, _vp, _vp, _int, _vp]),
+    ("fb_xpby_dev", _int, [_i64, _vp, _vp, _vp, _vp]),
     ("fb_axpby", _int, [_i64, _dbl, _vp, _dbl, _vp, _vp]),
     ("fb_axpy_dev", _int, [_i64, _vp, _int, _vp, _vp, _vp]),
     ("fb_scalar_div", _int, [_vp, _vp, _vp, _vp]),
@@ -93,6 +101,7 @@ _SIGS = [
                                         _i64, C.POINTER(_vp)]),
     ("fb_csr_info", _int, [_vp, _pi64, _pi64, _pi64]),
     ("fb_csr_download", _int, [_vp, _vp, _vp, _vp]),
+    ("fb_set_blockilu_packed", _int, [_int]),
     ("fb_blockilu_create_csr", _int, [_vp, _i64, _vp, _pi64, C.POINTER(_vp)]),
     ("fb_transfer_create", _int, [_vp, _vp, _vp, _int, _vp, _vp, C.POINTER(_vp)]),
     ("fb_transfer_destroy", None, [_vp]),

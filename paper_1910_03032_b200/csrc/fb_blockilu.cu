@@ -40,6 +40,18 @@ struct TriPart {
   int width = 0;
   fb::DevBuf<double> ev;
   fb::DevBuf<unsigned short> eo;
+  // level-packed layout (block_ilu_packed_kernel): one contiguous, 16-byte
+  // aligned chunk per dependency level of every block
+  //   [values E x f64 | inverse diagonal R x f64 (U parts) | local columns
+  //    E x u16 | local rows R x u16 | row starts R x u16 | row lengths R x u16]
+  // so a TMA bulk copy stages one level into a shared-memory ring
+  fb::DevBuf<unsigned char> pk;
+  fb::DevBuf<int64_t> loff;   // (levels + 1) byte offsets of the chunks
+  fb::DevBuf<int> lne;        // entries per level
+  int max_chunk = 0;
+  int lev_group = 1;          // levels staged per bulk copy
+  int max_group = 0;          // largest staged span (bytes)
+  int64_t nnz = 0;            // strict-triangle entries (kept when the CSR is freed)
 };
 
 }  // namespace
@@ -47,6 +59,7 @@ struct TriPart {
 static int g_bilu_pipe = 2;  // 0: CSR sweep, 1: CSR + next-level loads, 2: padded rows for large blocks, else 1
 static int g_bilu_lanes = 0;  // 0 = by block size
 static int g_bilu_deep = 1;   // two-level lookahead for one-wave grids (0: off)
+static int g_bilu_packed = 1; // level-packed TMA-ring sweep for blocks > 160 rows (0: off)
 
 struct fb_blockilu {
   int64_t n = 0;
@@ -918,11 +931,329 @@ static int build_ell(fb_blockilu* B) {
     FB_CHECK_LAUNCH();
     FB_TRY_CUDA(cudaDeviceSynchronize());
     P->width = W;
+    P->nnz = P->ix.n;
     P->ix.reset();
     P->v.reset();
     P->ip.reset();
   }
   B->ell_w = W;
+  return FB_OK;
+}
+
+// ---- level-packed sweep: a TMA ring of dependency levels ------------------
+// The CSR / ELL sweeps load each level's rows with per-lane global loads one
+// (or two) levels ahead, so every level waits out most of a memory latency:
+// at cfg3 the fine-level sweep ran at ~25-35 % of HBM bandwidth with
+// 89-131 levels per block.  Here each level of each block is ONE contiguous
+// chunk (TriPart::pk), and one lane streams chunks NSLOT levels ahead into a
+// shared-memory ring with cp.async.bulk (TMA) + an mbarrier per slot, so the
+// lanes computing level g read everything from shared memory.  Every row's
+// sum is the same sequential, separately rounded multiply-add chain as
+// row_finish (bitwise the CSR sweep).
+namespace {
+
+struct PackView {
+  const unsigned char* pk;
+  const int64_t* loff;
+  const int* lne;
+  const int* grp;
+  const int* blk_grp;
+  int has_inv;
+};
+
+__device__ __forceinline__ uint32_t psmem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void pk_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "PKW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra PKW_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void pk_copy(uint32_t dst, const void* src, uint32_t bytes,
+                                        uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__host__ __device__ inline size_t packed_smem(int nslot, int max_chunk, int max_block,
+                                              int max_grp) {
+  return 128 + size_t(nslot) * size_t(max_chunk) + size_t(max_block) * 8 +
+         size_t(max_grp + 1) * 16;
+}
+
+// Levels are staged K at a time (one bulk copy spans K consecutive chunks of
+// the block; NSLOT spans in flight), so the mbarrier wait and the copy issue
+// are paid once per K levels.
+template <int NSLOT>
+__device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, uint64_t* bars,
+                                           unsigned char* ring, int slot_bytes, int K,
+                                           int64_t* soff, int* sR, int* sE, uint32_t& used) {
+  const int lane = threadIdx.x;
+  const int g0 = T.blk_grp[b], G = T.blk_grp[b + 1] - g0;
+  const int NG = (G + K - 1) / K;
+  __syncwarp();
+  for (int i = lane; i <= G; i += 32) soff[i] = T.loff[g0 + i];
+  for (int i = lane; i < G; i += 32) {
+    sR[i] = T.grp[g0 + i + 1] - T.grp[g0 + i];
+    sE[i] = T.lne[g0 + i];
+  }
+  __syncwarp();
+  auto issue = [&](int j) {
+    const uint32_t slot = (used + uint32_t(j)) % NSLOT;
+    const int a = j * K, z = min(a + K, G);
+    pk_copy(psmem_u32(ring + size_t(slot) * slot_bytes), T.pk + soff[a],
+            uint32_t(soff[z] - soff[a]), psmem_u32(&bars[slot]));
+  };
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int j = 0; j < NG && j < NSLOT; ++j) issue(j);
+  }
+  for (int j = 0; j < NG; ++j) {
+    const uint32_t c = used + uint32_t(j), slot = c % NSLOT;
+    pk_wait(psmem_u32(&bars[slot]), (c / NSLOT) & 1u);
+    const unsigned char* sb = ring + size_t(slot) * slot_bytes;
+    const int a = j * K, z = min(a + K, G);
+    for (int g = a; g < z; ++g) {
+      const unsigned char* ch = sb + (soff[g] - soff[a]);
+      const int R = sR[g], E = sE[g];
+      const double* vals = reinterpret_cast<const double*>(ch);
+      const double* inv = vals + E;
+      const unsigned short* cols =
+          reinterpret_cast<const unsigned short*>(inv + (T.has_inv ? R : 0));
+      const unsigned short* rows = cols + E;
+      const unsigned short* rst = rows + R;  // per row: first entry, entry count
+      const unsigned short* cnt = rst + R;
+      for (int t = lane; t < R; t += 32) {
+        const int start = rst[t], n = cnt[t], row = rows[t];
+        // all loads of the row first (independent), then the sequential chain
+        double av[kRowBuf], yv[kRowBuf];
+#pragma unroll
+        for (int u = 0; u < kRowBuf; ++u) {
+          const bool ok = u < n;
+          av[u] = ok ? vals[start + u] : 0.0;
+          yv[u] = y[ok ? cols[start + u] : row];
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int u = 0; u < kRowBuf; ++u)
+          if (u < n) acc = __dadd_rn(acc, __dmul_rn(av[u], yv[u]));
+        for (int u = kRowBuf; u < n; ++u)  // rows longer than a 27-point triangle
+          acc = __dadd_rn(acc, __dmul_rn(vals[start + u], y[cols[start + u]]));
+        const double res = __dsub_rn(y[row], acc);
+        y[row] = T.has_inv ? __dmul_rn(res, inv[t]) : res;
+      }
+      __syncwarp();
+    }
+    if (lane == 0 && j + NSLOT < NG) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(j + NSLOT);
+    }
+  }
+  used += uint32_t(NG);
+}
+
+template <int NSLOT>
+__global__ void __launch_bounds__(32) block_ilu_packed_kernel(
+    const int* __restrict__ block_ptr, const int* __restrict__ new2old, PackView A, PackView Bv,
+    const double* __restrict__ r, double* __restrict__ out, int slot_bytes, int KA, int KB,
+    int max_block, int max_grp) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(psm);
+  unsigned char* ring = psm + 128;
+  double* y = reinterpret_cast<double*>(ring + size_t(NSLOT) * slot_bytes);
+  int64_t* soff = reinterpret_cast<int64_t*>(y + max_block);
+  int* sR = reinterpret_cast<int*>(soff + max_grp + 1);
+  int* sE = sR + max_grp + 1;
+  const int lane = threadIdx.x;
+  const int b = blockIdx.x;
+  const int bs = block_ptr[b], nb = block_ptr[b + 1] - bs;
+  if (lane == 0) {
+    for (int i = 0; i < NSLOT; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[i])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = lane; i < nb; i += 32) y[i] = r[new2old ? new2old[bs + i] : bs + i];
+  uint32_t used = 0;
+  packed_tri<NSLOT>(A, b, y, bars, ring, slot_bytes, KA, soff, sR, sE, used);
+  packed_tri<NSLOT>(Bv, b, y, bars, ring, slot_bytes, KB, soff, sR, sE, used);
+  __syncwarp();
+  for (int i = lane; i < nb; i += 32) out[new2old ? new2old[bs + i] : bs + i] = y[i];
+}
+
+__global__ void pack_count_kernel(int64_t nlev, const int* __restrict__ grp,
+                                  const int* __restrict__ rows, const int64_t* __restrict__ ip,
+                                  int has_inv, int64_t* __restrict__ size, int* __restrict__ lne,
+                                  int* __restrict__ max_chunk) {
+  const int64_t L = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (L > nlev) return;
+  if (L == nlev) {
+    size[L] = 0;
+    return;
+  }
+  int64_t E = 0;
+  for (int k = grp[L]; k < grp[L + 1]; ++k) E += ip[rows[k] + 1] - ip[rows[k]];
+  const int64_t R = grp[L + 1] - grp[L];
+  const int64_t bytes = (8 * E + (has_inv ? 8 * R : 0) + 2 * E + 6 * R + 15) / 16 * 16;
+  lne[L] = int(E);
+  size[L] = bytes;
+  atomicMax(max_chunk, int(bytes));
+}
+
+__global__ void pack_fill_kernel(int64_t nlev, int nblocks, const int* __restrict__ bptr,
+                                 const int* __restrict__ blk_grp, const int* __restrict__ grp,
+                                 const int* __restrict__ rows, const int64_t* __restrict__ ip,
+                                 const int* __restrict__ ix, const double* __restrict__ v,
+                                 const double* __restrict__ invdiag,
+                                 const int64_t* __restrict__ loff, const int* __restrict__ lne,
+                                 unsigned char* __restrict__ pk) {
+  const int64_t L = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (L >= nlev) return;
+  int lo = 0, hi = nblocks - 1;  // block of level L
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (blk_grp[mid] <= L) lo = mid; else hi = mid - 1;
+  }
+  const int bs = bptr[lo];
+  const int E = lne[L], R = grp[L + 1] - grp[L];
+  unsigned char* ch = pk + loff[L];
+  double* vals = reinterpret_cast<double*>(ch);
+  double* inv = vals + E;
+  unsigned short* cols = reinterpret_cast<unsigned short*>(inv + (invdiag ? R : 0));
+  unsigned short* lrows = cols + E;
+  unsigned short* rst = lrows + R;
+  unsigned short* cnt = rst + R;
+  int e = 0;
+  for (int t = 0; t < R; ++t) {
+    const int row = rows[grp[L] + t];
+    const int64_t a = ip[row], z = ip[row + 1];
+    rst[t] = (unsigned short)e;
+    for (int64_t k = a; k < z; ++k, ++e) {
+      vals[e] = v[k];
+      cols[e] = (unsigned short)(ix[k] - bs);
+    }
+    if (invdiag) inv[t] = invdiag[row];
+    lrows[t] = (unsigned short)(row - bs);
+    cnt[t] = (unsigned short)(z - a);
+  }
+}
+
+// largest span of K consecutive level chunks of one block
+__global__ void pack_group_kernel(int64_t nlev, int nblocks, const int* __restrict__ blk_grp,
+                                  const int64_t* __restrict__ loff, int K,
+                                  int* __restrict__ max_span) {
+  const int64_t L = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (L >= nlev) return;
+  int lo = 0, hi = nblocks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (blk_grp[mid] <= L) lo = mid; else hi = mid - 1;
+  }
+  const int64_t g0 = blk_grp[lo], g1 = blk_grp[lo + 1];
+  if ((L - g0) % K) return;
+  const int64_t z = (L + K < g1) ? L + K : g1;
+  atomicMax(max_span, int(loff[z] - loff[L]));
+}
+
+}  // namespace
+
+constexpr int kPackSpanBudget = 8 * 1024;  // bytes per staged span (two in flight)
+
+static int build_packed_part(fb_blockilu* B, TriPart& P, bool has_inv) {
+  const int64_t nlev = P.grp.n - 1;
+  if (nlev <= 0) return FB_OK;
+  DevBuf<int64_t> size;
+  DevBuf<int> mx;
+  FB_TRY_CUDA(size.alloc(nlev + 1));
+  FB_TRY_CUDA(P.lne.alloc(nlev));
+  FB_TRY_CUDA(mx.alloc(1));
+  FB_TRY_CUDA(cudaMemset(mx.ptr, 0, sizeof(int)));
+  pack_count_kernel<<<ceil_div(nlev + 1, 256), 256>>>(nlev, P.grp.ptr, P.rows.ptr, P.ip.ptr,
+                                                      has_inv ? 1 : 0, size.ptr, P.lne.ptr,
+                                                      mx.ptr);
+  FB_CHECK_LAUNCH();
+  size_t tb = 0;
+  FB_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, size.ptr, size.ptr, nlev + 1));
+  DevBuf<unsigned char> tmp;
+  FB_TRY_CUDA(tmp.alloc(int64_t(tb)));
+  FB_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, tb, size.ptr, size.ptr, nlev + 1));
+  int64_t total = 0;
+  FB_TRY_CUDA(cudaMemcpy(&total, size.ptr + nlev, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  FB_TRY_CUDA(cudaMemcpy(&P.max_chunk, mx.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+  FB_TRY_CUDA(P.pk.alloc(total));
+  pack_fill_kernel<<<ceil_div(nlev, 128), 128>>>(nlev, B->nblocks, B->block_ptr.ptr,
+                                                 P.blk_grp.ptr, P.grp.ptr, P.rows.ptr, P.ip.ptr,
+                                                 P.ix.ptr, P.v.ptr,
+                                                 has_inv ? P.invdiag.ptr : nullptr, size.ptr,
+                                                 P.lne.ptr, P.pk.ptr);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(cudaDeviceSynchronize());
+  P.loff.ptr = size.ptr;  // keep the offsets
+  P.loff.n = size.n;
+  size.ptr = nullptr;
+  size.n = 0;
+  // stage as many levels per copy as keep two spans within the budget
+  for (int K : {8, 4, 2, 1}) {
+    FB_TRY_CUDA(cudaMemset(mx.ptr, 0, sizeof(int)));
+    pack_group_kernel<<<ceil_div(nlev, 256), 256>>>(nlev, B->nblocks, P.blk_grp.ptr, P.loff.ptr,
+                                                    K, mx.ptr);
+    FB_CHECK_LAUNCH();
+    int span = 0;
+    FB_TRY_CUDA(cudaMemcpy(&span, mx.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+    P.lev_group = K;
+    P.max_group = span;
+    if (span <= kPackSpanBudget) break;
+  }
+  return FB_OK;
+}
+
+// Pack all four parts and drop their CSR arrays (the packed chunks replace
+// them); blocks must be large (one block per warp) and fit 16-bit indices.
+static int build_packed(fb_blockilu* B) {
+  if (!g_bilu_packed || B->max_block <= 160 || B->max_block > 65535) return FB_OK;
+  TriPart* parts[4] = {&B->L, &B->U, &B->Ut, &B->Lt};
+  const bool inv[4] = {false, true, true, false};
+  for (int i = 0; i < 4; ++i) {
+    parts[i]->nnz = parts[i]->ix.n;
+    const int rc = build_packed_part(B, *parts[i], inv[i]);
+    if (rc != FB_OK) return rc;
+  }
+  for (TriPart* P : parts) {
+    P->ix.reset();
+    P->v.reset();
+  }
+  return FB_OK;
+}
+
+template <int NSLOT>
+static int launch_packed(const fb_blockilu* B, const TriPart& a, bool ua, const TriPart& b,
+                         bool ub, const double* r, double* out, cudaStream_t st) {
+  const int sb = (std::max(a.max_group, b.max_group) + 15) / 16 * 16;
+  const size_t smem = packed_smem(NSLOT, sb, B->max_block, B->max_grp);
+  static size_t configured = 0;
+  if (smem > configured) {
+    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_packed_kernel<NSLOT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = smem;
+  }
+  const PackView pa{a.pk.ptr, a.loff.ptr, a.lne.ptr, a.grp.ptr, a.blk_grp.ptr, ua ? 0 : 1};
+  const PackView pb{b.pk.ptr, b.loff.ptr, b.lne.ptr, b.grp.ptr, b.blk_grp.ptr, ub ? 0 : 1};
+  block_ilu_packed_kernel<NSLOT><<<B->nblocks, 32, smem, st>>>(
+      B->block_ptr.ptr, B->new2old.ptr, pa, pb, r, out, sb, a.lev_group, b.lev_group,
+      B->max_block, B->max_grp);
+  FB_CHECK_LAUNCH();
   return FB_OK;
 }
 
@@ -993,7 +1324,11 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
   FB_REQUIRE(block_ilu_smem(B->max_block) * (32 / block_ilu_lanes(B->max_block)) <= 200 * 1024 &&
                  B->max_block <= 65535,
              "block too large for shared memory");
-  if (g_bilu_pipe == 2) {
+  {
+    const int rc_p = build_packed(B.get());
+    if (rc_p != FB_OK) return rc_p;
+  }
+  if (g_bilu_pipe == 2 && !B->L.pk.ptr) {
     const int rc_ell = build_ell(B.get());
     if (rc_ell != FB_OK) return rc_ell;
   }
@@ -1009,8 +1344,8 @@ int fb_blockilu_info(const fb_blockilu* B, int64_t* n, int64_t* nnz_lower, int64
                      int* ell_width) {
   FB_REQUIRE(B != nullptr, "block ILU is NULL");
   if (n) *n = B->n;
-  if (nnz_lower) *nnz_lower = B->L.ix.n;   // strict lower triangle (unit diagonal)
-  if (nnz_upper) *nnz_upper = B->U.ix.n;   // strict upper triangle (+ inverse diagonal)
+  if (nnz_lower) *nnz_lower = B->L.nnz ? B->L.nnz : B->L.ix.n;  // strict lower (unit diagonal)
+  if (nnz_upper) *nnz_upper = B->U.nnz ? B->U.nnz : B->U.ix.n;  // strict upper (+ inverse diagonal)
   if (ell_width) *ell_width = B->ell_w;
   return FB_OK;
 }
@@ -1030,6 +1365,12 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
   const TriView a = transpose ? view(B->Ut, false) : view(B->L, true);
   const TriView b = transpose ? view(B->Lt, true) : view(B->U, false);
   cudaStream_t st = as_stream(stream);
+  if (B->L.pk.ptr) {  // level-packed TMA-ring sweep
+    const TriPart& pa = transpose ? B->Ut : B->L;
+    const TriPart& pb = transpose ? B->Lt : B->U;
+    const bool ua = !transpose, ub = transpose;  // unit diagonal: L and L^T
+    return launch_packed<2>(B, pa, ua, pb, ub, r, out, st);
+  }
   const int lanes = g_bilu_lanes ? g_bilu_lanes : block_ilu_lanes(B->max_block);
   if (B->ell_w) {
     const int l2 = lanes == 2 ? 2 : 32;
@@ -1253,7 +1594,11 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
   rc = device_levels(n, nblocks, bptr64.ptr, B->Lt, false, st);
   if (rc != FB_OK) return rc;
   FB_TRY_CUDA(cudaDeviceSynchronize());
-  if (g_bilu_pipe == 2) {
+  {
+    const int rc_p = build_packed(B.get());
+    if (rc_p != FB_OK) return rc_p;
+  }
+  if (g_bilu_pipe == 2 && !B->L.pk.ptr) {
     const int rc_ell = build_ell(B.get());
     if (rc_ell != FB_OK) return rc_ell;
   }
@@ -1263,6 +1608,11 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
     if (rc_g != FB_OK) return rc_g;
   }
   *out = B.release();  // new2old stays empty: the level is block-major already
+  return FB_OK;
+}
+
+extern "C" int fb_set_blockilu_packed(int on) {
+  g_bilu_packed = on ? 1 : 0;
   return FB_OK;
 }
 

@@ -173,6 +173,7 @@ class Operator:
 class _DeviceOperator(Operator):
     """Holds an fb_operator handle; shared apply plumbing."""
 
+    graph_safe = True  # apply_into = device launches only (capturable in a CUDA graph)
     handle = None
     in_size = 0
     out_size = 0
@@ -438,6 +439,10 @@ class ConstrainedOperator(Operator):
         self.shape = op.shape
         self._dofs_dev = None
         self._work = None
+
+    @property
+    def graph_safe(self):
+        return bool(getattr(self.op, "graph_safe", False)) and hasattr(self.op, "apply_into")
 
     def _dofs(self):
         if self._dofs_dev is None:

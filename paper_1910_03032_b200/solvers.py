@@ -20,6 +20,7 @@ to the device once.  Any other ``.apply``/callable is treated as a host
 """
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -171,6 +172,8 @@ def deflate_mean(v, weights=None):
 
 
 class DiagonalPreconditioner(_DeviceMixin):
+    graph_safe = True
+
     def __init__(self, diag):
         self.inv = 1.0 / np.asarray(diag, dtype=np.float64)
         self._inv = None
@@ -198,11 +201,150 @@ def collocated_mass_diagonal(space, constrained=None):
 
 # -- Krylov --------------------------------------------------------------------------
 
+# device-resident PCG (CUDA graph with a conditional WHILE node, fb_graph.cu)
+# for single-GPU device operators up to this size; FB_CG_GRAPH=0 disables it
+GRAPH_MAX_N = 20_000_000
+TRUE_RESIDUAL_PERIOD = 50  # solvers.py:145-150
+
+
+class _CGGraph:
+    """One captured PCG iteration for a fixed (A, precond, n): the body of a
+    device-side while loop.  Vectors, scalars and dot partials are owned
+    here, so the graph's pointers stay valid for every solve."""
+
+    def __init__(self, A, precond, n, cap):
+        self.A, self.precond, self.n, self.cap = A, precond, n, cap
+        self.apply_A = _device_apply(A)
+        self.M = _device_apply(precond) if precond is not None else None
+        self.x, self.r, self.z, self.p, self.Ap, self.tmp, self.b = (dev.empty(n) for _ in range(7))
+        self.s = dev.zeros(8)  # rz, pAp, alpha, rz_new, beta
+        self.cfgd = dev.zeros(2)  # norm0, rel_tol
+        self.state = torch.zeros(4, dtype=torch.int32, device=dev.device())
+        self.hist = dev.zeros(cap + 2)
+        npart = int(_lib.lib.fb_dot_partials(n))
+        self.part = [dev.empty(npart), dev.empty(npart)]
+        self.stream = torch.cuda.Stream()
+        self.graph = None
+
+    def __del__(self):
+        g = getattr(self, "graph", None)
+        if g and _lib is not None and _lib.lib is not None:
+            _lib.lib.fb_while_graph_destroy(g)
+
+    def _dot(self, x, y, k, slot, st):
+        _lib.check(_lib.lib.fb_dot(self.n, x.data_ptr(), y.data_ptr(), self.part[k].data_ptr(),
+                                   self.s[slot:slot + 1].data_ptr(), st))
+
+    def _iteration(self, st, true_res, handle, in_graph):
+        n = self.n
+        self.apply_A(self.p, self.Ap)
+        self._dot(self.p, self.Ap, 0, 1, st)
+        s = self.s
+        _lib.check(_lib.lib.fb_cg_update(n, s[0:1].data_ptr(), s[1:2].data_ptr(),
+                                         s[2:3].data_ptr(), self.p.data_ptr(), self.Ap.data_ptr(),
+                                         self.x.data_ptr(), self.r.data_ptr(),
+                                         0 if true_res else 1, st))
+        if true_res:
+            self.apply_A(self.x, self.tmp)
+            vec.copy(self.b, self.r, st)
+            vec.axpby(-1.0, self.tmp, 1.0, self.r, st)
+        if self.M is not None:
+            self.M(self.r, self.z)
+        else:
+            vec.copy(self.r, self.z, st)
+        self._dot(self.r, self.z, 1, 3, st)
+        _lib.check(_lib.lib.fb_cg_check(handle, in_graph, s.data_ptr(), self.state.data_ptr(),
+                                        self.hist.data_ptr(), self.cfgd.data_ptr(),
+                                        TRUE_RESIDUAL_PERIOD, st))
+        _lib.check(_lib.lib.fb_xpby_dev(n, self.z.data_ptr(), s[4:5].data_ptr(),
+                                        self.p.data_ptr(), st))
+
+    def _capture(self, st):
+        import ctypes as C
+        g = C.c_void_p()
+        _lib.check(_lib.lib.fb_while_graph_create(C.byref(g)))
+        self.graph = g
+        handle = _lib.lib.fb_while_graph_handle(g)
+        _lib.check(_lib.lib.fb_while_graph_begin(g, st))
+        try:
+            self._iteration(st, False, handle, 1)
+        finally:
+            _lib.check(_lib.lib.fb_while_graph_end(g, st))
+
+    def solve(self, bd, cfg, t0):
+        cur = torch.cuda.current_stream()
+        self.stream.wait_stream(cur)
+        with torch.cuda.stream(self.stream):
+            st = self.stream.cuda_stream
+            vec.copy(bd, self.b, st)
+            vec.copy(self.b, self.r, st)  # A(0) == 0 exactly
+            self.x.zero_()
+            if self.M is not None:
+                self.M(self.r, self.z)
+            else:
+                vec.copy(self.r, self.z, st)
+            self._dot(self.r, self.z, 1, 0, st)
+            rz = float(self.s[0].item())
+            norm0 = math.sqrt(abs(rz))
+            history = [1.0]
+            if norm0 == 0.0 or norm0 <= cfg.abs_tol:
+                cur.wait_stream(self.stream)
+                return self.x.clone(), SolveReport(True, 0, 0.0, time.perf_counter() - t0,
+                                                   cfg.label, history)
+            vec.copy(self.z, self.p, st)
+            self.cfgd.copy_(torch.tensor([norm0, cfg.rel_tol], dtype=torch.float64))
+            self.state.copy_(torch.tensor([0, 0, cfg.max_iters, 0], dtype=torch.int32))
+            if self.graph is None:
+                self.apply_A(self.p, self.Ap)  # lazy workspaces are allocated before capture
+                self._capture(st)
+            it, stop = 0, 0
+            while True:
+                if (it + 1) % TRUE_RESIDUAL_PERIOD == 0:
+                    self._iteration(st, True, 0, 0)
+                else:
+                    _lib.check(_lib.lib.fb_while_graph_launch(self.graph, st))
+                it, stop = (int(v) for v in self.state[:2].tolist())
+                if stop or it >= cfg.max_iters:
+                    break
+            hist = self.hist[:it + 1].tolist()
+            x = self.x.clone()
+        cur.wait_stream(self.stream)
+        history = [1.0] + hist[1:it + 1] if stop != 2 else [1.0] + hist[1:it]
+        relres = history[-1]
+        converged = stop == 1 or cfg.rel_tol == 0.0
+        return x, SolveReport(converged, it, relres, time.perf_counter() - t0, cfg.label, history)
+
+
+def _cg_graph_for(A, precond, n, cap):
+    cache = A.__dict__.setdefault("_fb_cg_graphs", {})
+    key = (id(precond), n)
+    g = cache.get(key)
+    if g is None or g.precond is not precond or g.cap < cap:
+        g = _CGGraph(A, precond, n, max(cap, 512))
+        cache[key] = g
+    return g
+
+
+def _graph_eligible(A, precond, x0, project, inner, n):
+    return (inner is None and project is None and x0 is None and n <= GRAPH_MAX_N
+            and bool(getattr(A, "graph_safe", False)) and hasattr(A, "apply_into")
+            and (precond is None or bool(getattr(precond, "graph_safe", False)))
+            and os.environ.get("FB_CG_GRAPH", "1") != "0")
+
+
 def cg(A, b, precond=None, config=None, x0=None, project=None, inner=None):
     """Preconditioned CG with the reference recurrence (solvers.py:108-169).
     inner(x, y, out): the inner product into a 1-element device tensor
     (default: the deterministic libfbb200 dot; the sharded solver passes an
-    owned-slice dot + all-reduce)."""
+    owned-slice dot + all-reduce).  Single-GPU device operators run the
+    whole loop on the device (_CGGraph): same kernels, same arithmetic,
+    no per-iteration host synchronisation."""
+    cfg0 = config or SolverConfig()
+    bd0, host0 = dev.DeviceIn.get(b)
+    if _graph_eligible(A, precond, x0, project, inner, bd0.shape[0]):
+        t0 = time.perf_counter()
+        x, rep = _cg_graph_for(A, precond, bd0.shape[0], cfg0.max_iters).solve(bd0, cfg0, t0)
+        return (dev.to_host(x) if host0 else x), rep
     dot_into = inner if inner is not None else vec.dot_into
     apply_A = _device_apply(A)
     M = _device_apply(precond) if precond is not None else None
@@ -846,6 +988,13 @@ class LORPreconditioner(_DeviceMixin):
         A.residual_into(r, x, t, st)
         sm.backward_into(t, t2, st)
         vec.axpby(1.0, t2, 1.0, x, st)
+
+    @property
+    def graph_safe(self):
+        """The V-cycle is device launches only on preallocated level vectors
+        (block smoother, dense coarse inverse, no mean projection)."""
+        return (self.smoother_kind == "block" and isinstance(self._bottom, DenseInverseSolver)
+                and not self.pure_neumann)
 
     def clone_workspace(self):
         """A view of this preconditioner (same matrices, smoothers and coarse
