@@ -382,18 +382,22 @@ def lor_pcg_scale(cases=((4, 116), (7, 66)), c=C_HELM):
     return out
 
 
-def lor_pcg_sharded(rank, world, cases=((4, 116, 16), (7, 66, 8)), c=C_HELM):
-    """cfg3 on N GPUs (weak scaling): scale-mode LOR-PCG sharded over z-slabs
-    (dist_box.py), `layers` element layers per rank on a (n, n, layers*N) box
-    (p = 4: ~13.8M DoFs per GPU, 110M at 8 GPUs; p = 7: ~12M per GPU).
-    Time-to-solve from CUDA events between barriers, max over ranks."""
+def lor_pcg_sharded(rank, world, cases=((4, 116, 16, "weak"), (7, 66, 8, "weak"),
+                                        (4, 116, 116, "strong"), (7, 68, 68, "strong")),
+                    c=C_HELM):
+    """cfg3 on N GPUs: scale-mode LOR-PCG sharded over z-slabs (dist_box.py).
+    weak: `layers` element layers per rank on a (n, n, layers*N) box (p = 4:
+    ~13.8M DoFs per GPU, 110M at 8 GPUs; p = 7: ~12M per GPU); strong: the
+    fixed (n, n, nz) box split over the N ranks (116^3 p = 4: 100.5M DoFs, the
+    single-GPU lor_pcg_cfg3 problem; 68^3 p = 7: 108.5M DoFs).  Time-to-solve
+    from CUDA events between barriers, max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_1910_03032_b200 import dist_box as D, solvers
     comm = D.TorchComm()
     out = {}
-    for p, n, layers in cases:
-        counts = (n, n, layers * world)
+    for p, n, layers, mode in cases:
+        counts = (n, n, layers * world) if mode == "weak" else (n, n, layers)
         t0 = time.perf_counter()
         pr = D.helmholtz_slab_problem(comm, counts, p, c=c, perturb=0.05, seed=1)
         setup = time.perf_counter() - t0
@@ -410,13 +414,16 @@ def lor_pcg_sharded(rank, world, cases=((4, 116, 16), (7, 66, 8)), c=C_HELM):
         t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ndofs = int(np.prod([a * p + 1 for a in counts]))
-        out[f"p{p}_{n}x{n}x{counts[2]}"] = {
+        out[f"{mode}_p{p}_{n}x{n}x{counts[2]}"] = {
             "dofs": ndofs, "dofs_per_gpu": ndofs // world, "iterations": rep.iterations,
             "converged": rep.converged, "solve_ms": round(float(t.item()), 2),
-            "setup_s": round(setup, 2), "n_gpus": world, "scaling": "weak",
+            "setup_s": round(setup, 2), "n_gpus": world, "scaling": mode,
             "note": "z-slab sharding: slab operator + NCCL halo sums, owned-row LOR levels, "
                     "slab block ILU, agglomerated Q1 V-cycle, all-reduced dots"}
         del pr, x
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
     return out
 
 
@@ -803,6 +810,7 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the driver's log shows the NCCL transport
         dist.init_process_group("nccl")
     if args.impl == "reference":
         run_reference(args, rank, world)
