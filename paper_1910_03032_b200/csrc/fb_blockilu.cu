@@ -1050,7 +1050,7 @@ __device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, 
 #pragma unroll
         for (int u = 0; u < kRowBuf; ++u)
           if (u < n) acc = __dadd_rn(acc, __dmul_rn(av[u], yv[u]));
-        for (int u = kRowBuf; u < n; ++u)  // rows longer than a 27-point triangle
+        for (int u = kRowBuf; u < n; ++u)  // first-touch order: up to 26 lower neighbours
           acc = __dadd_rn(acc, __dmul_rn(vals[start + u], y[cols[start + u]]));
         const double res = __dsub_rn(y[row], acc);
         y[row] = T.has_inv ? __dmul_rn(res, inv[t]) : res;
