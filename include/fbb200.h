@@ -273,13 +273,18 @@ int fb_lor_assemble_box(int p, const int64_t* counts, const double* corners_dev,
                         double c, int constrain_boundary, fb_csr** out);
 /* Slab-local variant (multi-GPU scale mode): constrain_faces is a bitmask of
  * the constrained box faces (1 x-, 2 x+, 4 y-, 8 y+, 16 z-, 32 z+; cut planes
- * between ranks are not constrained); only rows with lattice id < nrows are
+ * between ranks are not constrained) plus periodic axes in bits 6-8 (64 x,
+ * 128 y, 256 z: counts*p lattice points, indices wrap, mesh.py:81-96);
+ * only rows with lattice id < nrows are
  * assembled (the rank's owned DoFs), columns range over ncols local ids
  * (owned + ghost planes).  nrows/ncols < 0: the whole lattice. */
 int fb_lor_assemble_box_rows(int p, const int64_t* counts, const double* corners_dev,
                              const double* nodes, const int* lattice_ids_dev, int kind,
                              double nu, double c, int constrain_faces, int64_t nrows,
                              int64_t ncols, fb_csr** out);
+/* Pin one DoF of a device CSR (row and column zeroed, unit diagonal; the
+ * pattern must hold the diagonal): lor.constrain_matrix(A, [dof]). */
+int fb_csr_pin(fb_csr* A, int64_t dof);
 int fb_csr_info(const fb_csr* A, int64_t* nrows, int64_t* ncols, int64_t* nnz);
 /* copy a device CSR to host arrays (indptr: nrows+1, indices/data: nnz) */
 int fb_csr_download(const fb_csr* A, int64_t* indptr, int64_t* indices, double* data);
@@ -312,6 +317,10 @@ int fb_transfer_create(const fb_restriction* fine, const fb_restriction* hmap,
 void fb_transfer_destroy(fb_transfer* T);
 /* global element coordinates of the transfer's local element (0,0,0)
  * (first-touch ownership on a slab of a larger box) */
+/* Periodic axes (bitmask x 1, y 2, z 4) of a p-transfer and the global
+ * element counts: the last element's local index p along a periodic axis
+ * is owned by the first element (first touch). */
+int fb_transfer_set_periodic(fb_transfer* T, int axes, int64_t gnx, int64_t gny, int64_t gnz);
 int fb_transfer_set_origin(fb_transfer* T, int64_t x0, int64_t y0, int64_t z0);
 /* y[idx[i]] += v[i] for distinct indices (slab halo partial sums) */
 int fb_index_add(int64_t n, const int* idx_dev, const double* v_dev, double* y_dev, void* stream);

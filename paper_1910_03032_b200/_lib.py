@@ -99,12 +99,14 @@ _SIGS = [
                                    C.POINTER(_vp)]),
     ("fb_lor_assemble_box_rows", _int, [_int, _vp, _vp, _vp, _vp, _int, _dbl, _dbl, _int, _i64,
                                         _i64, C.POINTER(_vp)]),
+    ("fb_csr_pin", _int, [_vp, _i64]),
     ("fb_csr_info", _int, [_vp, _pi64, _pi64, _pi64]),
     ("fb_csr_download", _int, [_vp, _vp, _vp, _vp]),
     ("fb_set_blockilu_packed", _int, [_int]),
     ("fb_blockilu_create_csr", _int, [_vp, _i64, _vp, _pi64, C.POINTER(_vp)]),
     ("fb_transfer_create", _int, [_vp, _vp, _vp, _int, _vp, _vp, C.POINTER(_vp)]),
     ("fb_transfer_destroy", None, [_vp]),
+    ("fb_transfer_set_periodic", _int, [_vp, _int, _i64, _i64, _i64]),
     ("fb_transfer_set_origin", _int, [_vp, _i64, _i64, _i64]),
     ("fb_index_add", _int, [_i64, _vp, _vp, _vp, _vp]),
     ("fb_transfer_prolong", _int, [_vp, _vp, _vp, _vp]),

@@ -39,6 +39,8 @@ struct fb_transfer {
   int nf = 0, nc = 0;
   int64_t ne = 0, counts[3] = {0, 0, 0};
   int64_t origin[3] = {0, 0, 0};  // global coordinates of local element (0,0,0)
+  int periodic = 0;                // periodic axes (bitmask) and their global element counts
+  int64_t gcounts[3] = {0, 0, 0};
   fb::DevBuf<double> W;   // (nw, nf, nc) weight tables
   fb::DevBuf<int> widx;   // per axis, per element coordinate: table index
   fb::DevBuf<double> E;   // (ne, nc^3) restriction contributions
@@ -72,6 +74,7 @@ struct BoxParams {
   const double* corners;  // (ne, 8, 3)
   const int* lid;         // lattice -> DoF id, x fastest
   int kind, constrain;   // constrain: bitmask of constrained box faces (x-, x+, y-, y+, z-, z+)
+  int periodic;          // bitmask of periodic axes (x 1, y 2, z 4): N = n p, indices wrap
   int64_t nrows;         // rows with id >= nrows are not assembled (other ranks own them)
   double nu, c;
   double nodes[17];
@@ -150,7 +153,9 @@ __device__ void q1_row(const double X[8][3], int vi, int kind, double nu, double
   }
 }
 
-__device__ __forceinline__ int axis_span(int64_t g, int64_t N) { return 1 + (g > 0) + (g < N - 1); }
+__device__ __forceinline__ int axis_span(int64_t g, int64_t N, bool per) {
+  return per ? 3 : 1 + (g > 0) + (g < N - 1);
+}
 
 __global__ void lor_box_count_kernel(BoxParams P, int* __restrict__ cnt) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -158,7 +163,9 @@ __global__ void lor_box_count_kernel(BoxParams P, int* __restrict__ cnt) {
   if (t >= total) return;
   const int64_t gx = t % P.Nx, gy = (t / P.Nx) % P.Ny, gz = t / (P.Nx * P.Ny);
   const int row = P.lid[t];
-  if (row >= 0 && row < P.nrows) cnt[row] = axis_span(gx, P.Nx) * axis_span(gy, P.Ny) * axis_span(gz, P.Nz);
+  if (row >= 0 && row < P.nrows)
+    cnt[row] = axis_span(gx, P.Nx, P.periodic & 1) * axis_span(gy, P.Ny, P.periodic & 2) *
+               axis_span(gz, P.Nz, P.periodic & 4);
 }
 
 __global__ void __launch_bounds__(128) lor_box_fill_kernel(BoxParams P,
@@ -182,7 +189,11 @@ __global__ void __launch_bounds__(128) lor_box_fill_kernel(BoxParams P,
       bool ok = true;
       for (int a = 0; a < 3; ++a) {
         m[a] = g[a] - ((s >> a) & 1);
-        ok = ok && m[a] >= 0 && m[a] <= N[a] - 2;
+        if ((P.periodic >> a) & 1) {
+          if (m[a] < 0) m[a] += N[a];  // the sub-cell of the last element (wrap)
+        } else {
+          ok = ok && m[a] >= 0 && m[a] <= N[a] - 2;
+        }
       }
       if (!ok) continue;
       int64_t e[3];
@@ -208,7 +219,10 @@ __global__ void __launch_bounds__(128) lor_box_fill_kernel(BoxParams P,
   for (int dz = -1; dz <= 1; ++dz)
     for (int dy = -1; dy <= 1; ++dy)
       for (int dx = -1; dx <= 1; ++dx) {
-        const int64_t hx = g[0] + dx, hy = g[1] + dy, hz = g[2] + dz;
+        int64_t hx = g[0] + dx, hy = g[1] + dy, hz = g[2] + dz;
+        if (P.periodic & 1) hx = (hx + N[0]) % N[0];
+        if (P.periodic & 2) hy = (hy + N[1]) % N[1];
+        if (P.periodic & 4) hz = (hz + N[2]) % N[2];
         if (hx < 0 || hy < 0 || hz < 0 || hx >= N[0] || hy >= N[1] || hz >= N[2]) continue;
         const int col = P.lid[(hz * N[1] + hy) * N[0] + hx];
         double val = acc[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)];
@@ -241,6 +255,8 @@ struct TransferView {
   int64_t nx, ny, nz;
   int64_t ox, oy, oz;
   int nf, nc;
+  int periodic;
+  int64_t gn[3];
 };
 
 // fine element e: per-axis coordinates and weight tables
@@ -259,8 +275,16 @@ __device__ __forceinline__ void transfer_elem(const TransferView& T, int64_t e, 
 
 // first-touch ownership on a structured box: local lattice index 0 along an
 // axis belongs to the lower neighbour unless the element is the first one
-__device__ __forceinline__ bool owned_local(const int64_t ec[3], int l0, int l1, int l2) {
-  return (l0 > 0 || ec[0] == 0) && (l1 > 0 || ec[1] == 0) && (l2 > 0 || ec[2] == 0);
+// (periodic axis: the last element's local index nf-1 is the first
+// element's local 0 and belongs to it)
+__device__ __forceinline__ bool owned_axis(const TransferView& T, int a, int64_t ec, int l) {
+  if (l == 0 && ec != 0) return false;
+  if (((T.periodic >> a) & 1) && ec == T.gn[a] - 1 && l == T.nf - 1) return false;
+  return true;
+}
+__device__ __forceinline__ bool owned_local(const TransferView& T, const int64_t ec[3], int l0,
+                                            int l1, int l2) {
+  return owned_axis(T, 0, ec[0], l0) && owned_axis(T, 1, ec[1], l1) && owned_axis(T, 2, ec[2], l2);
 }
 
 // One warp per fine element, kTE elements per CTA.
@@ -291,7 +315,7 @@ __global__ void __launch_bounds__(32 * kTE) transfer_prolong_kernel(TransferView
   __syncwarp();
   for (int l = lane; l < nf3; l += 32) {
     const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
-    if (!owned_local(ec, l0, l1, l2)) continue;
+    if (!owned_local(T, ec, l0, l1, l2)) continue;
     double acc = 0.0;
 #pragma unroll
     for (int c = 0; c < nc; ++c) {
@@ -327,7 +351,7 @@ __global__ void __launch_bounds__(32 * kTE) transfer_restrict_kernel(TransferVie
   const int nc3 = nc * nc * nc, nf3 = nf * nf * nf;
   for (int l = lane; l < nf3; l += 32) {
     const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
-    rf[l] = owned_local(ec, l0, l1, l2) ? __ldg(xf + __ldg(T.fmap + e * nf3 + l)) : 0.0;
+    rf[l] = owned_local(T, ec, l0, l1, l2) ? __ldg(xf + __ldg(T.fmap + e * nf3 + l)) : 0.0;
   }
   for (int j = lane; j < nf * nc; j += 32)
     for (int a = 0; a < 3; ++a) w[a][j] = __ldg(Wa[a] + j);
@@ -372,9 +396,10 @@ int fb_lor_assemble_box_rows(int p, const int64_t* counts, const double* corners
   P.nx = counts[0];
   P.ny = counts[1];
   P.nz = counts[2];
-  P.Nx = P.nx * p + 1;
-  P.Ny = P.ny * p + 1;
-  P.Nz = P.nz * p + 1;
+  P.periodic = (constrain_faces >> 6) & 7;  // bits 6-8: periodic x, y, z
+  P.Nx = P.nx * p + ((P.periodic & 1) ? 0 : 1);
+  P.Ny = P.ny * p + ((P.periodic & 2) ? 0 : 1);
+  P.Nz = P.nz * p + ((P.periodic & 4) ? 0 : 1);
   P.corners = corners_dev;
   P.lid = lattice_ids_dev;
   P.kind = kind;
@@ -475,6 +500,35 @@ int fb_transfer_create(const fb_restriction* fine, const fb_restriction* hmap,
 
 void fb_transfer_destroy(fb_transfer* T) { delete T; }
 
+// constrain_matrix (lor.py:84-99) for one DoF on a device CSR: row and
+// column `dof` zeroed, unit diagonal (the pure-Neumann pin, solvers.py:361-362)
+__global__ void csr_pin_kernel(int64_t n, const int64_t* __restrict__ ip,
+                               const int* __restrict__ ix, double* __restrict__ v, int64_t dof) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int64_t k = ip[r]; k < ip[r + 1]; ++k)
+    if (r == dof || ix[k] == dof) v[k] = (r == dof && ix[k] == dof) ? 1.0 : 0.0;
+}
+
+int fb_csr_pin(fb_csr* A, int64_t dof) {
+  FB_REQUIRE(A != nullptr && dof >= 0 && dof < A->nrows, "bad pin");
+  if (A->nrows == 0) return FB_OK;
+  csr_pin_kernel<<<ceil_div(A->nrows, 256), 256>>>(A->nrows, A->indptr.ptr, A->indices.ptr,
+                                                   A->data.ptr, dof);
+  FB_CHECK_LAUNCH();
+  FB_TRY_CUDA(cudaDeviceSynchronize());
+  return FB_OK;
+}
+
+int fb_transfer_set_periodic(fb_transfer* T, int axes, int64_t gnx, int64_t gny, int64_t gnz) {
+  FB_REQUIRE(T != nullptr && axes >= 0 && axes <= 7, "bad periodic transfer setup");
+  T->periodic = axes;
+  T->gcounts[0] = gnx;
+  T->gcounts[1] = gny;
+  T->gcounts[2] = gnz;
+  return FB_OK;
+}
+
 int fb_transfer_set_origin(fb_transfer* T, int64_t x0, int64_t y0, int64_t z0) {
   FB_REQUIRE(T != nullptr && x0 >= 0 && y0 >= 0 && z0 >= 0, "bad transfer origin");
   T->origin[0] = x0;
@@ -500,7 +554,8 @@ int fb_index_add(int64_t n, const int* idx, const double* v, double* y, void* st
 static TransferView transfer_view(const fb_transfer* T) {
   return TransferView{restriction_map(T->fine), restriction_map(T->hmap), T->W.ptr, T->widx.ptr,
                       T->counts[0], T->counts[1], T->counts[2], T->origin[0], T->origin[1],
-                      T->origin[2], T->nf, T->nc};
+                      T->origin[2], T->nf, T->nc, T->periodic,
+                      {T->gcounts[0], T->gcounts[1], T->gcounts[2]}};
 }
 
 }  // extern "C"

@@ -54,14 +54,19 @@ DEFAULT_COARSE_CYCLES = 2
 # block-major first-touch numbering of a structured box
 # ---------------------------------------------------------------------------
 
-def _axis_tables(n_el, p, block):
-    """Per-axis closed-form pieces of the numbering for lattice index g."""
-    N = n_el * p + 1
+def _axis_tables(n_el, p, block, periodic=False):
+    """Per-axis closed-form pieces of the numbering for lattice index g.
+    Periodic axes have n_el p lattice points (the last element's local index
+    p is the first element's local 0, mesh.py:81-96): the first touch of
+    every point is unchanged, the last element owns one point less."""
+    N = n_el * p + (0 if periodic else 1)
     g = np.arange(N, dtype=np.int64)
     o = np.maximum(0, (g - 1) // p)             # first-touch owner element
     l = g - o * p                                # local lattice index in the owner
     s = (o > 0).astype(np.int64)                 # first owned local index
     cnt = p + (np.arange(n_el) == 0).astype(np.int64)  # owned lattice points per element
+    if periodic:
+        cnt[-1] -= 1
     blk = np.arange(n_el) // block
     nb = int(blk[-1]) + 1
     TW = np.bincount(blk, weights=cnt, minlength=nb).astype(np.int64)
@@ -70,12 +75,14 @@ def _axis_tables(n_el, p, block):
     return {"N": N, "nb": nb, "TW": TW, "B": blk[o], "C": cnt[o], "SP": SP[o], "R": l - s}
 
 
-def box_lattice_ids(counts, p, block, device=None, gz_range=None):
+def box_lattice_ids(counts, p, block, device=None, gz_range=None, periodic=(False,) * 3):
     """(Nz, Ny, Nx) int64 tensor: DoF id of every lattice point, plus the
     (nblocks+1) block row offsets (numpy).  gz_range = (g0, g1) restricts the
-    result to the lattice planes g0 <= gz < g1 (ids stay global)."""
+    result to the lattice planes g0 <= gz < g1 (ids stay global).  Periodic
+    axes have counts[a] p lattice points (no duplicated wrap plane)."""
     device = device if device is not None else torch.device("cpu")
-    tx, ty, tz = (_axis_tables(counts[a], p, block) for a in range(3))
+    periodic = tuple(bool(v) for v in periodic) if periodic else (False,) * 3
+    tx, ty, tz = (_axis_tables(counts[a], p, block, periodic[a]) for a in range(3))
     bsize = (tz["TW"][:, None, None] * ty["TW"][None, :, None] * tx["TW"][None, None, :])
     flat = bsize.ravel()
     block_ptr = np.concatenate([[0], np.cumsum(flat)]).astype(np.int64)
@@ -100,10 +107,15 @@ def box_lattice_ids(counts, p, block, device=None, gz_range=None):
     return ids, block_ptr
 
 
-def lattice_element_dofs(ids, p):
+def lattice_element_dofs(ids, p, periodic=(False,) * 3):
     """(ne, (p+1)^3) element map from the lattice ids (elements x fastest,
-    local index i0 + n i1 + n^2 i2)."""
+    local index i0 + n i1 + n^2 i2).  A periodic axis wraps: its first
+    lattice plane is appended before the elements are cut out."""
     n = p + 1
+    for a, per in enumerate(periodic or ()):
+        if per:
+            dim = 2 - a  # ids are (z, y, x)
+            ids = torch.cat([ids, ids.narrow(dim, 0, 1)], dim=dim)
     e = ids.unfold(0, n, p).unfold(1, n, p).unfold(2, n, p)
     return e.reshape(-1, n ** 3)
 
@@ -119,8 +131,7 @@ class BoxSpace:
         counts = tuple(int(c) for c in mesh.counts)
         if mesh.dim != 3 or len(counts) != 3:
             raise ValueError("BoxSpace needs a structured 3D box mesh")
-        if any(mesh.periodic):
-            raise ValueError("periodic boxes are not supported in scale mode")
+        self.periodic = tuple(bool(v) for v in (mesh.periodic or (False,) * 3))
         self.mesh = mesh
         self.counts = counts
         self.p = p
@@ -129,7 +140,8 @@ class BoxSpace:
         self.vdim = 1
         self.basis = make_basis(p)
         self.device = device if device is not None else torch.device("cpu")
-        ids, self.block_ptr = box_lattice_ids(counts, p, block, self.device)
+        ids, self.block_ptr = box_lattice_ids(counts, p, block, self.device,
+                                              periodic=self.periodic)
         self.ndofs_scalar = int(ids.numel())
         if self.ndofs_scalar >= 2 ** 31:
             raise ValueError("box too large for int32 DoF ids")
@@ -151,7 +163,7 @@ class BoxSpace:
     @property
     def element_dofs(self):
         if self._ed is None:
-            ed = lattice_element_dofs(self.lattice_ids, self.p).to(torch.int64)
+            ed = lattice_element_dofs(self.lattice_ids, self.p, self.periodic).to(torch.int64)
             self._ed = ed.cpu().numpy()
         return self._ed
 
@@ -159,7 +171,11 @@ class BoxSpace:
         if attributes is not None:
             raise ValueError("scale mode constrains the whole boundary")
         L = self.lattice_ids
-        faces = [L[0], L[-1], L[:, 0], L[:, -1], L[:, :, 0], L[:, :, -1]]
+        px, py, pz = self.periodic
+        faces = ([] if pz else [L[0], L[-1]]) + ([] if py else [L[:, 0], L[:, -1]]) + \
+                ([] if px else [L[:, :, 0], L[:, :, -1]])
+        if not faces:
+            return np.zeros(0, dtype=np.int64)
         b = torch.cat([f.reshape(-1) for f in faces]).to(torch.int64)
         return torch.unique(b).cpu().numpy()
 
@@ -212,19 +228,31 @@ def h_transfer_tables(n):
 class DeviceLevelMatrix(vec.DeviceCSR):
     """LOR matrix of one level, assembled on the device."""
 
-    def __init__(self, space, kind, nu=1.0, c=0.0, constrain=True):
+    def __init__(self, space, kind, nu=1.0, c=0.0, constrain=True, pin=None):
+        """constrain: Dirichlet rows / columns on the non-periodic box faces
+        (lor.py:84-99); pin: one DoF pinned (the pure-Neumann levels,
+        solvers.py:361-362)."""
         dev.device()
         corners = torch.from_numpy(np.ascontiguousarray(space.mesh.corners, dtype=np.float64))
         corners = corners.to(dev.device())
         counts = np.asarray(space.counts, dtype=np.int64)
         nodes = np.ascontiguousarray(space.basis.nodes, dtype=np.float64)
         lid = space.lattice_ids.to(dev.device())
+        per = getattr(space, "periodic", (False,) * 3)
+        faces = 0
+        if constrain:
+            for a in range(3):
+                if not per[a]:
+                    faces |= 3 << (2 * a)
+        mask = faces | sum((1 << (6 + a)) for a in range(3) if per[a])
         h = C.c_void_p()
-        _lib.check(_lib.lib.fb_lor_assemble_box(space.p, _lib.ptr(counts), corners.data_ptr(),
-                                                _lib.ptr(nodes), lid.data_ptr(), _lib.KIND[kind],
-                                                float(nu), float(c), int(bool(constrain)),
-                                                C.byref(h)))
+        _lib.check(_lib.lib.fb_lor_assemble_box_rows(space.p, _lib.ptr(counts), corners.data_ptr(),
+                                                     _lib.ptr(nodes), lid.data_ptr(),
+                                                     _lib.KIND[kind], float(nu), float(c), mask,
+                                                     -1, -1, C.byref(h)))
         self.handle = h
+        if pin is not None:
+            _lib.check(_lib.lib.fb_csr_pin(h, int(pin)))
         n = space.ndofs_scalar
         self.shape = (n, n)
 
@@ -307,6 +335,10 @@ class BoxTransfer:
                                                _lib.ptr(counts), W.shape[0], _lib.ptr(W),
                                                _lib.ptr(widx), C.byref(h)))
         self.handle = h
+        per = getattr(fine, "periodic", (False,) * 3)
+        if any(per):
+            _lib.check(_lib.lib.fb_transfer_set_periodic(
+                h, sum(1 << a for a in range(3) if per[a]), *(int(c) for c in fine.counts)))
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -349,12 +381,19 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
     cube edge of the smoother blocks on p >= 2 / Q1 levels."""
 
     def __init__(self, space, kind, nu=1.0, c=0.0, dirichlet_attrs="all", block=2,
-                 q1_block=4, max_coarse=20000, coarse_cycles=None):
-        if dirichlet_attrs != "all":
+                 q1_block=4, max_coarse=20000, coarse_cycles=None, pure_neumann=False):
+        """dirichlet_attrs="all": Dirichlet rows on every non-periodic box
+        face; None with pure_neumann=True: the periodic / Neumann Poisson
+        levels pin DoF 0 and the cycle deflates the mean before and after
+        (solvers.py:361-362, 384-390)."""
+        if pure_neumann:
+            if dirichlet_attrs is not None:
+                raise ValueError("pure-Neumann cycle expects no constrained dofs")
+        elif dirichlet_attrs != "all":
             raise ValueError("scale mode supports Dirichlet conditions on the whole boundary")
         t0 = time.perf_counter()
-        self.pure_neumann = False
-        self._proj = None
+        self.pure_neumann = bool(pure_neumann)
+        self._proj = solvers.MeanProjector() if pure_neumann else None
         self.smoother_kind = "block"
         ddev = dev.device()
         spaces = [space]
@@ -362,7 +401,9 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
             spaces.append(BoxSpace(space.mesh, deg, block=block if deg > 1 else q1_block,
                                    device=ddev))
         self.q1_index = len(spaces) - 1  # the ladder's Q1 level on the original mesh
-        while spaces[-1].ndofs_scalar > max_coarse and min(spaces[-1].counts) >= 2:
+        periodic = any(getattr(space, "periodic", ()))
+        while (not periodic and spaces[-1].ndofs_scalar > max_coarse
+               and min(spaces[-1].counts) >= 2):
             spaces.append(BoxSpace(coarsen_box(spaces[-1].mesh), 1, block=q1_block, device=ddev))
         self.spaces = spaces
         # near-exact Q1 solve (SURVEY 8(e')): when the Q1 level is coarsened
@@ -373,7 +414,8 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
         if coarse_cycles is None:
             coarse_cycles = DEFAULT_COARSE_CYCLES
         self.coarse_cycles = int(coarse_cycles) if len(spaces) - 1 > self.q1_index else 1
-        self._A = [DeviceLevelMatrix(s, kind, nu=nu, c=c) for s in spaces]
+        self._A = [DeviceLevelMatrix(s, kind, nu=nu, c=c, constrain=not pure_neumann,
+                                     pin=0 if pure_neumann else None) for s in spaces]
         self.levels = list(zip(spaces, self._A))
         self.smoothers = [DeviceBlockILU0(A, s.block_ptr) for s, A in self.levels[:-1]]
         self.transfers = [BoxTransfer(spaces[i], spaces[i + 1]) for i in range(len(spaces) - 1)]

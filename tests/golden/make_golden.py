@@ -248,6 +248,47 @@ def make_cfg3shape():
     return {"cfg3shape": manifest}
 
 
+# periodic boxes (cfg5 shape), LOR-PCG: (name, counts, p, kind, c, pure_neumann, rel_tol)
+PERIODIC_CASES = [
+    ("per_pn_p5_6", (6, 6, 6), 5, "stiffness", 0.0, True, 1e-10),
+    ("per_pn_p3_8", (8, 8, 8), 3, "stiffness", 0.0, True, 1e-10),
+    ("per_helm_p4_6", (6, 6, 6), 4, "helmholtz", 10.0, False, 1e-8),
+]
+
+
+def make_periodic():
+    """Fully periodic [-pi, pi]^3 boxes (the cfg5 Taylor-Green domain):
+    pure-Neumann Poisson with MeanProjector (solvers.py:361-362, 384-390) and
+    a Helmholtz solve, reference LORPreconditioner + cg; counts and a solution
+    fingerprint for the scale-mode (BoxSpace) periodic path."""
+    mesh, fespace, mfop, solvers, lor, _ = ref_modules()
+    out, manifest = {}, []
+    for (name, counts, p, kind, c, pn, tol) in PERIODIC_CASES:
+        m = mesh.cartesian_mesh(counts, lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                                periodic=(True,) * 3)
+        sp_ = fespace.FESpace(m, p, n_q=p + 2)
+        geom = mesh.compute_geometric_factors(m, sp_.basis.quad)
+        op = mfop.setup(kind, space=sp_, geom=geom, nu=1.0, c=c)
+        b = np.random.default_rng(5).standard_normal(sp_.ndofs)
+        cfg = solvers.SolverConfig(rel_tol=tol, max_iters=300)
+        if pn:
+            pre = solvers.LORPreconditioner(sp_, kind, pure_neumann=True)
+            b = solvers.deflate_mean(b)
+            x, rep = solvers.cg(op, b, precond=pre, project=solvers.MeanProjector(), config=cfg)
+        else:
+            pre = solvers.LORPreconditioner(sp_, kind, nu=1.0, c=c)
+            x, rep = solvers.cg(op, b, precond=pre, config=cfg)
+        idx = np.random.default_rng(1).choice(sp_.ndofs, min(4096, sp_.ndofs), replace=False)
+        out[f"{name}/idx"] = idx
+        out[f"{name}/x_sample"] = x[idx]
+        manifest.append(dict(name=name, counts=list(counts), p=p, kind=kind, c=c,
+                             pure_neumann=pn, rel_tol=tol, ndofs=int(sp_.ndofs),
+                             iterations=rep.iterations))
+        print(manifest[-1], flush=True)
+    np.savez_compressed(os.path.join(HERE, "periodic.npz"), **out)
+    return {"periodic": manifest}
+
+
 # (name, d, counts, p, alpha_dt)
 STOKES_CASES = [
     ("cav2d_p2", 2, (8, 8), 2, None),
@@ -430,7 +471,7 @@ def make_boundary():
 
 GROUPS = {"apply": make_apply, "numbering": make_numbering, "solvers": make_solvers, "stokes": make_stokes,
           "extras": make_extras, "boundary": make_boundary,
-          "cfg3shape": make_cfg3shape}
+          "cfg3shape": make_cfg3shape, "periodic": make_periodic}
 
 
 def main(argv):

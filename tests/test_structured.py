@@ -278,3 +278,127 @@ def test_box_lor_pcg_cfg3_shape_vs_reference(name):
     assert abs(rep.iterations - c["iterations"]) <= 1, (rep.iterations, c["iterations"])
     xs = x.cpu().numpy()[perm][gold[f"{name}/idx"]]
     assert rel_err(xs, gold[f"{name}/x_sample"]) < 1e-5
+
+
+# ---- periodic boxes (periodic wrap for cfg5) -----------
+PER_BOXES = [((4, 3, 5), (True, False, True), 2, 2), ((3, 3, 3), (True, True, True), 3, 2),
+             ((6, 4, 4), (True, True, True), 4, 2), ((4, 6, 3), (False, True, True), 1, 4),
+             ((5, 4, 3), (True, True, True), 5, 2)]
+
+
+def _perm_periodic(counts, per, p, block, lows=None, highs=None):
+    from paper_1910_03032_b200 import geometry, spaces, structured as S
+    m = geometry.cartesian_mesh(counts, lows=lows, highs=highs, periodic=per)
+    ref = spaces.FESpace(m, p)
+    ids, bptr = S.box_lattice_ids(counts, p, block, periodic=per)
+    ed = S.lattice_element_dofs(ids, p, per).numpy()
+    perm = np.full(ref.ndofs_scalar, -1, dtype=np.int64)
+    perm[ref.element_dofs.ravel()] = ed.ravel()
+    return m, ref, ed, perm, bptr
+
+
+@pytest.mark.parametrize("counts,per,p,block", PER_BOXES)
+def test_periodic_box_numbering_is_block_major_first_touch(counts, per, p, block):
+    """Periodic axes wrap (mesh.py:81-96): the closed-form numbering is a
+    renumbering of the reference's whose block order is the parity path's."""
+    from paper_1910_03032_b200 import lor, solvers
+    m, ref, ed, perm, bptr = _perm_periodic(counts, per, p, block)
+    n = ref.ndofs_scalar
+    assert np.array_equal(np.sort(perm), np.arange(n))
+    assert np.array_equal(perm[ref.element_dofs], ed)
+    order = lor.first_touch_ordering(ref)
+    blk = solvers.element_block_ids(m, block)[ref.dof_owner_elem]
+    new2old = order[np.argsort(blk[order], kind="stable")]
+    assert np.array_equal(perm[new2old], np.arange(n))
+    bnew = blk[new2old]
+    starts = np.flatnonzero(np.r_[True, bnew[1:] != bnew[:-1]])
+    assert np.array_equal(np.r_[starts, n], bptr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,pin", [(1, False), (2, True), (4, False), (5, True)])
+def test_periodic_device_lor_matrix_matches_host_assembly(p, pin):
+    import torch
+    from paper_1910_03032_b200 import lor, structured as S
+    counts, per = (3, 4, 3), (True, True, True)
+    m, ref, ed, perm, bptr = _perm_periodic(counts, per, p, 2)
+    space = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
+    A = S.DeviceLevelMatrix(space, "stiffness", nu=1.0, c=0.0, constrain=False,
+                            pin=0 if pin else None).to_scipy()
+    Ah = lor.lor_matrix(ref, "stiffness", nu=1.0, c=0.0)
+    if pin:
+        Ah = lor.constrain_matrix(Ah, np.array([0]))
+    P = np.argsort(perm)
+    Ar = Ah[P][:, P].tocsr()
+    Ar.sort_indices()
+    assert perm[0] == 0  # the pinned DoF is the same lattice point in both numberings
+    assert A.nnz == Ar.nnz
+    assert np.array_equal(A.indptr, Ar.indptr) and np.array_equal(A.indices, Ar.indices)
+    assert np.max(np.abs(A.data - Ar.data)) <= 1e-13 * np.max(np.abs(Ar.data))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 5])
+def test_periodic_p_transfer_matches_nodal_interpolation(p):
+    import torch
+    from paper_1910_03032_b200 import device as dev, lor, spaces, structured as S
+    counts, per = (3, 3, 4), (True, True, True)
+    m, ref, ed, perm, bptr = _perm_periodic(counts, per, p, 2)
+    pc = max(1, (p + 1) // 2)
+    refc = spaces.FESpace(m, pc)
+    cblock = 2 if pc > 1 else 4
+    idsc, _ = S.box_lattice_ids(counts, pc, cblock, periodic=per)
+    permc = np.full(refc.ndofs_scalar, -1, dtype=np.int64)
+    permc[refc.element_dofs.ravel()] = S.lattice_element_dofs(idsc, pc, per).numpy().ravel()
+    Pm = lor.nodal_interpolation(ref, refc)
+    fine = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
+    coarse = S.BoxSpace(m, pc, block=cblock, device=torch.device("cuda"))
+    T = S.BoxTransfer(fine, coarse)
+    rng = np.random.default_rng(1)
+    xc = rng.standard_normal(refc.ndofs_scalar)
+    xf = rng.standard_normal(ref.ndofs_scalar)
+    out_f = torch.empty(ref.ndofs_scalar, dtype=torch.float64, device="cuda")
+    out_c = torch.empty(refc.ndofs_scalar, dtype=torch.float64, device="cuda")
+    xc_n = np.empty_like(xc); xc_n[permc] = xc
+    xf_n = np.empty_like(xf); xf_n[perm] = xf
+    T.prolong_into(dev.to_device(xc_n), out_f)
+    T.restrict_into(dev.to_device(xf_n), out_c)
+    assert rel_err(out_f.cpu().numpy()[perm], Pm @ xc) < 1e-13
+    assert rel_err(out_c.cpu().numpy()[permc], Pm.T @ xf) < 1e-13
+
+
+PERIODIC = {c["name"]: c for c in manifest().get("periodic", [])}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(PERIODIC))
+def test_periodic_box_lor_pcg_vs_reference(name):
+    """Scale mode on the cfg5 domain (periodic [-pi, pi]^3): pure-Neumann
+    Poisson with the mean projection, and Helmholtz, against the reference's
+    counts (tests/golden/periodic.npz): +-1 iteration, solution sample."""
+    import torch
+    from paper_1910_03032_b200 import geometry, mfop, solvers, structured as S
+    c = PERIODIC[name]
+    gold = load("periodic")
+    counts, p, per = tuple(c["counts"]), c["p"], (True, True, True)
+    m, ref, ed, perm, bptr = _perm_periodic(counts, per, p, 2, lows=(-np.pi,) * 3,
+                                            highs=(np.pi,) * 3)
+    space = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
+    geom = geometry.DeviceGeometry(m, space.basis.quad)
+    op = mfop.setup(c["kind"], space=space, geom=geom, nu=1.0, c=c["c"])
+    b = np.random.default_rng(5).standard_normal(ref.ndofs)
+    cfg = solvers.SolverConfig(rel_tol=c["rel_tol"], max_iters=300)
+    if c["pure_neumann"]:
+        b = b - b.mean()
+        pre = S.BoxLORPreconditioner(space, c["kind"], dirichlet_attrs=None, pure_neumann=True)
+        proj = solvers.MeanProjector()
+    else:
+        pre = S.BoxLORPreconditioner(space, c["kind"], nu=1.0, c=c["c"])
+        proj = None
+    bn = np.empty_like(b)
+    bn[perm] = b
+    x, rep = solvers.cg(op, torch.from_numpy(bn).cuda(), precond=pre, config=cfg, project=proj)
+    assert rep.converged
+    assert abs(rep.iterations - c["iterations"]) <= 1, (rep.iterations, c["iterations"])
+    xs = x.cpu().numpy()[perm][gold[f"{name}/idx"]]
+    assert rel_err(xs, gold[f"{name}/x_sample"]) < 1e-5
