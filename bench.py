@@ -58,8 +58,8 @@ def algorithmic_flops(ne, p):
 def _traffic():
     """Measured DRAM bytes (read + write) of one sweep step -- every fused
     kernel and E->L sum launch -- from the committed ncu launch list
-    (profiles/r1_traffic.json); None if the profile is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+    (profiles/r2_traffic.json); None if the profile is absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_traffic.json")
     try:
         with open(path) as f:
             return int(json.load(f)["sweep_dram_bytes"])
@@ -500,9 +500,13 @@ def callers(stokes_cases=((2, 2), (2, 4), (2, 6), (3, 2)), tgv=(5, 16, 4)):
         its.append([r.mass_iters, r.pressure_iters, r.helmholtz_iters])
     torch.cuda.synchronize()
     ms = 1e3 * (time.perf_counter() - t0) / steps
+    st.profile = True  # one more step with CUDA events between its phases
+    phases = st.step().phase_ms
+    st.profile = False
     out[f"tgv3d_projection_p{p}_{n}^3"] = {
         "velocity_dofs": int(vs.ndofs), "pressure_dofs": int(ps.ndofs), "ms_per_step": round(ms, 2),
         "steps": steps, "iterations_mass_pressure_helmholtz": its, "setup_s": round(setup, 2),
+        "phase_ms": phases,
         "kinetic_energy": st.kinetic_energy(),
         "scheme": "BDF3/EXT3, dt 0.02, nu 1/1600; timed after the 3 start-up steps (setup_s)"}
     return out

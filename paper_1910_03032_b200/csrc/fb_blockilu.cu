@@ -1171,6 +1171,12 @@ __global__ void pack_group_kernel(int64_t nlev, int nblocks, const int* __restri
 
 constexpr int kPackSpanBudget = 8 * 1024;  // bytes per staged span (two in flight)
 
+static int pack_span_budget() {  // FB_BILU_SPAN=<bytes>: A/B runs (tools/bilu_ab.py)
+  const char* env = getenv("FB_BILU_SPAN");
+  const int v = env ? atoi(env) : 0;
+  return v > 0 ? v : kPackSpanBudget;
+}
+
 static int build_packed_part(fb_blockilu* B, TriPart& P, bool has_inv) {
   const int64_t nlev = P.grp.n - 1;
   if (nlev <= 0) return FB_OK;
@@ -1214,7 +1220,7 @@ static int build_packed_part(fb_blockilu* B, TriPart& P, bool has_inv) {
     FB_TRY_CUDA(cudaMemcpy(&span, mx.ptr, sizeof(int), cudaMemcpyDeviceToHost));
     P.lev_group = K;
     P.max_group = span;
-    if (span <= kPackSpanBudget) break;
+    if (span <= pack_span_budget()) break;
   }
   return FB_OK;
 }
@@ -1223,6 +1229,9 @@ static int build_packed_part(fb_blockilu* B, TriPart& P, bool has_inv) {
 // them); blocks must be large (one block per warp) and fit 16-bit indices.
 static int build_packed(fb_blockilu* B) {
   if (!g_bilu_packed || B->max_block <= 160 || B->max_block > 65535) return FB_OK;
+  // grids of a few waves (one warp per block) stay on the CSR sweeps, whose
+  // two-level lookahead suits them better (TGV-size levels)
+  if (small_grid(B) || B->nblocks < 16 * 148) return FB_OK;
   TriPart* parts[4] = {&B->L, &B->U, &B->Ut, &B->Lt};
   const bool inv[4] = {false, true, true, false};
   for (int i = 0; i < 4; ++i) {

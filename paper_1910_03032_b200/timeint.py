@@ -67,6 +67,7 @@ class StepReport:
     mass_iters: int = 0
     pressure_iters: int = 0
     helmholtz_iters: int = 0
+    phase_ms: dict = None  # device time per phase when the stepper's `profile` is set
 
 
 def _combo(terms, n):
@@ -198,6 +199,15 @@ class ProjectionStepper:
         dt, t_new = self.dt, self.t + self.dt
         b0 = s.b[0]
         rep = StepReport(t=t_new)
+        marks = []
+
+        def mark(name):  # CUDA events between phases (profile mode only)
+            if getattr(self, "profile", False):
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                marks.append((name, e))
+
+        mark("start")
         nv = self.vspace.ndofs
         terms = [(-s.b[j] / dt, self.u_hist[j - 1]) for j in range(1, k_eff + 1)]
         terms += [(s.a[j - 1], self.n_hist[j - 1]) for j in range(1, k_eff + 1)]
@@ -216,8 +226,10 @@ class ProjectionStepper:
                 fl = boundary.flux_matrix(self.pspace)(g_new)  # device SpMV
                 vec.axpby(-(b0 / dt), fl, 1.0, rhs_p)
         rhs_p = deflate_mean(rhs_p)
+        mark("rhs")
         p, prep = cg(self.Lp, rhs_p, precond=self.pressure_pre, x0=self.p, project=self.mean,
                      config=self.config)
+        mark("pressure_solve")
         if not prep.converged:
             raise RuntimeError(f"pressure solve failed: {prep}")
         rep.pressure_iters = prep.iterations
@@ -233,7 +245,9 @@ class ProjectionStepper:
             vec.axpby(-1.0, op.apply(u_lift), 1.0, b_u)
         if self.has_boundary:
             b_u.index_fill_(0, self._bdofs_dev, 0.0)
+        mark("velocity_rhs")
         u, hrep = cg(A, b_u, precond=pre, config=self.config)
+        mark("helmholtz_solve")
         if not hrep.converged:
             raise RuntimeError(f"velocity solve failed: {hrep}")
         rep.helmholtz_iters = hrep.iterations
@@ -242,6 +256,11 @@ class ProjectionStepper:
 
         n_new, it_n = self._nodal_convection(u)
         rep.mass_iters = it_n
+        mark("convection_mass_solve")
+        if marks:
+            torch.cuda.synchronize()
+            rep.phase_ms = {n1: round(e0.elapsed_time(e1), 3)
+                            for (_, e0), (n1, e1) in zip(marks[:-1], marks[1:])}
         self.u_hist.insert(0, u)
         self.n_hist.insert(0, n_new)
         self.r_hist.insert(0, self._rotational_bc(u))
