@@ -1169,7 +1169,7 @@ __global__ void pack_group_kernel(int64_t nlev, int nblocks, const int* __restri
 
 }  // namespace
 
-constexpr int kPackSpanBudget = 8 * 1024;  // bytes per staged span (two in flight)
+constexpr int kPackSpanBudget = 4 * 1024;  // bytes per staged span (two in flight; measured 2-16 KB)
 
 static int pack_span_budget() {  // FB_BILU_SPAN=<bytes>: A/B runs (tools/bilu_ab.py)
   const char* env = getenv("FB_BILU_SPAN");
