@@ -709,6 +709,18 @@ def run_ours(args, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # the drop-in call a reference user makes: op.apply(numpy array) per degree
+    # (pageable host memory, synchronous H2D / apply / D2H; no pipelining)
+    xh = [h.numpy() for h in hx]
+    for pr, xv in zip(probs, xh):
+        pr["op"].apply(xv)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for pr, xv in zip(probs, xh):
+        pr["op"].apply(xv)
+    torch.cuda.synchronize()
+    numpy_ms = 1e3 * (time.perf_counter() - t0)
+
     sharded = None
     meta = [{"N": pr["N"], "ne": pr["ne"], "p": pr["p"], "fast": pr["op"].fast_path}
             for pr in probs]
@@ -759,7 +771,11 @@ def run_ours(args, rank, world):
                 "h2d_bytes_per_step": int(8 * dofs_step), "d2h_bytes_per_step": int(8 * dofs_step),
                 "note": "HelmholtzOperator.apply_into per degree, pinned-host x/y copies inside "
                         "the timed region, H2D/apply/D2H pipelined over the sweep on 3 streams",
-                "readback_matches_device": ok},
+                "readback_matches_device": ok,
+                "numpy_api": {"value": round(world * dofs_step / (numpy_ms * 1e-3) / 1e9, 4),
+                              "unit": "GDoF/s",
+                              "note": "HelmholtzOperator.apply(numpy) per degree: pageable, "
+                                      "synchronous copies, host wall clock, one sweep"}},
         "gpu_launches": int(launches),
         "clocks": clk,
         "warmup_steps_run": nw,

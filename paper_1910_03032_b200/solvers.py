@@ -1044,6 +1044,12 @@ class BlockDiagonalPreconditioner(_DeviceMixin):
                 self._done = [torch.cuda.Event() for _ in range(vdim)]
                 self._fork = torch.cuda.Event()
 
+    @property
+    def graph_safe(self):
+        """Capturable: the concurrent components fork from and join back into
+        the current stream with events (the stream-capture pattern)."""
+        return bool(getattr(self.inner, "graph_safe", False))
+
     def apply_into(self, r, out, stream=None):
         ns = self.ns
         if self._par is not None and stream is None:

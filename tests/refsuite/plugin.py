@@ -23,11 +23,12 @@ os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/fb_ref_numba_cache")
 sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref", "site"))
 
 import flowbench  # noqa: E402
+import flowbench.lor as _rlor  # noqa: E402
 import flowbench.mfop as _rmfop  # noqa: E402
 import flowbench.solvers as _rsol  # noqa: E402
 import flowbench.stokes as _rst  # noqa: E402
 
-from paper_1910_03032_b200 import _lib, mfop, solvers, stokes  # noqa: E402
+from paper_1910_03032_b200 import _lib, lor, mfop, solvers, stokes  # noqa: E402
 
 assert os.path.abspath(flowbench.__file__).startswith(os.path.join(ROOT, "oracle", "_ref"))
 
@@ -42,6 +43,10 @@ SUBSTITUTE = {
                       "InnerCG", "_first_touch_ordering"]),
     _rst: (stokes, ["BlockSaddleOperator", "SteadySchurInverse", "UnsteadySchurInverse",
                     "BlockTriangularPreconditioner", "StokesSystem"]),
+    # LOR matrices / transfers the V-cycle applies (lor.py:61-131); the
+    # refined-mesh builder, Matrix Market export and spectral report stay
+    _rlor: (lor, ["lor_matrix", "constrain_matrix", "nodal_interpolation",
+                  "coarse_q1_interpolation"]),
 }
 for _ref_mod, (_ours, _names) in SUBSTITUTE.items():
     for _n in _names:

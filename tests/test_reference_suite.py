@@ -22,7 +22,8 @@ NOT_APPLICABLE = {
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("module", ["test_mfop.py", "test_solvers.py", "test_stokes.py"])
+@pytest.mark.parametrize("module", ["test_mfop.py", "test_solvers.py", "test_stokes.py",
+                                    "test_lor.py"])
 def test_reference_module_against_package(module):
     path = os.path.join(REF_TESTS, module)
     if not os.path.exists(path):
