@@ -127,7 +127,7 @@ class BoxSpace:
     (`mesh`, `p`, `dim`, `vdim`, `basis`, `element_dofs`, `ndofs_scalar`,
     `boundary_dof_set`)."""
 
-    def __init__(self, mesh, p, block=2, device=None):
+    def __init__(self, mesh, p, block=2, device=None, vdim=1):
         counts = tuple(int(c) for c in mesh.counts)
         if mesh.dim != 3 or len(counts) != 3:
             raise ValueError("BoxSpace needs a structured 3D box mesh")
@@ -137,8 +137,9 @@ class BoxSpace:
         self.p = p
         self.block = block
         self.dim = 3
-        self.vdim = 1
+        self.vdim = int(vdim)
         self.basis = make_basis(p)
+        self._owner = self._coords = None
         self.device = device if device is not None else torch.device("cpu")
         ids, self.block_ptr = box_lattice_ids(counts, p, block, self.device,
                                               periodic=self.periodic)
@@ -150,11 +151,48 @@ class BoxSpace:
 
     @property
     def ndofs(self):
-        return self.ndofs_scalar
+        return self.vdim * self.ndofs_scalar
 
     @property
     def nloc(self):
         return (self.p + 1) ** 3
+
+    # -- FESpace helpers the callers use (fespace.py:247-340) ------------------
+    def _owners(self):
+        if self._owner is None:
+            flat = self.element_dofs.ravel()
+            first = np.full(self.ndofs_scalar, flat.size, dtype=np.int64)
+            np.minimum.at(first, flat, np.arange(flat.size))
+            self._owner = (first // self.nloc, first % self.nloc)
+        return self._owner
+
+    @property
+    def dof_owner_elem(self):
+        return self._owners()[0]
+
+    @property
+    def dof_owner_local(self):
+        return self._owners()[1]
+
+    @property
+    def node_coords(self):
+        """Physical position of every DoF (its first-touch owner element's node)."""
+        if self._coords is None:
+            from .spaces import element_node_coords
+            e, l = self._owners()
+            self._coords = element_node_coords(self)[e, l]
+        return self._coords
+
+    def expand_dofs(self, scalar_dofs, components=None):
+        comps = range(self.vdim) if components is None else components
+        ns = self.ndofs_scalar
+        return np.concatenate([np.asarray(scalar_dofs) + c * ns for c in comps])
+
+    def project(self, f):
+        vals = np.asarray(f(self.node_coords), dtype=np.float64)
+        if self.vdim == 1:
+            return vals.reshape(-1).copy()
+        return vals.T.reshape(-1).copy()
 
     @property
     def nblocks(self):

@@ -107,20 +107,36 @@ class ProjectionStepper:
         self.D = mfop.DivergenceOperator(vspace, pspace, geom)
         self.Lp = mfop.StiffnessOperator(pspace, geom)
         self.mass_pre = DiagonalPreconditioner(collocated_mass_diagonal(vspace))
-        self.pressure_pre = LORPreconditioner(pspace, "stiffness", pure_neumann=True,
-                                              smoother=smoother)
+        self.pressure_pre = self._pressure_cycle()
         self.mean = MeanProjector()
         self.pressure_weights = collocated_mass_diagonal(pspace)
         self.bdofs = (vspace.expand_dofs(vspace.boundary_dof_set())
                       if self.has_boundary else np.zeros(0, dtype=np.int64))
         self._bdofs_dev = torch.from_numpy(self.bdofs).to(dev.device()) if self.has_boundary else None
         self._helm = {}
-        self._scalar_v = FESpace(mesh, vspace.p)
+        self._scalar_v = self._scalar_velocity_space()
         self.t = None
         self.u = None
         self.p = None
         self.u_hist, self.n_hist, self.r_hist = [], [], []
-        self._volume = float(np.sum(geom.detj @ geom.w))
+        self._volume = self._domain_volume()
+
+    # -- preconditioner / space factories (overridden by the scale-mode stepper) --
+
+    def _pressure_cycle(self):
+        return LORPreconditioner(self.pspace, "stiffness", pure_neumann=True,
+                                 smoother=self.smoother)
+
+    def _helmholtz_cycle(self, c):
+        return LORPreconditioner(self._scalar_v, "helmholtz", nu=self.nu, c=c,
+                                 dirichlet_attrs=("all" if self.has_boundary else None),
+                                 smoother=self.smoother)
+
+    def _scalar_velocity_space(self):
+        return FESpace(self.vspace.mesh, self.vspace.p)
+
+    def _domain_volume(self):
+        return float(np.sum(self.geom.detj @ self.geom.w))
 
     # -- state ----------------------------------------------------------------
 
@@ -176,9 +192,7 @@ class ProjectionStepper:
             c = b0 / self.dt
             op = mfop.HelmholtzOperator(self.vspace, self.geom, c=c, nu=self.nu)
             A = mfop.ConstrainedOperator(op, self.bdofs)
-            cyc = LORPreconditioner(self._scalar_v, "helmholtz", nu=self.nu, c=c,
-                                    dirichlet_attrs=("all" if self.has_boundary else None),
-                                    smoother=self.smoother)
+            cyc = self._helmholtz_cycle(c)
             pre = BlockDiagonalPreconditioner(cyc, self.vspace.vdim, self.vspace.ndofs_scalar)
             self._helm[key] = (op, A, pre)
         return self._helm[key]
@@ -284,3 +298,43 @@ class ProjectionStepper:
         """(u, p) as host numpy arrays -- the reference stepper's `u` / `p`
         attributes are numpy; here they stay device tensors between steps."""
         return dev.to_host(self.u), dev.to_host(self.p)
+
+
+class BoxProjectionStepper(ProjectionStepper):
+    """The projection stepper in scale mode (cfg5 at size on one GPU): a
+    periodic (or bounded, Dirichlet) structured box with the block-major
+    `structured.BoxSpace` numbering, factors built on the device and the
+    pressure / Helmholtz LOR hierarchies assembled and factored on the device
+    (`structured.BoxLORPreconditioner`: block-ILU smoother, pure-Neumann pin
+    + mean projection for the pressure).  Same step as ProjectionStepper
+    (timeint.py:338-388); the velocity is SoA over the box numbering."""
+
+    def __init__(self, mesh, p, k, dt, nu, forcing=None, config=None, block=2):
+        from . import geometry, structured
+        ddev = dev.device()
+        if any(not a for a in mesh.periodic):
+            raise ValueError("BoxProjectionStepper supports fully periodic boxes")
+        self._block = block
+        vspace = structured.BoxSpace(mesh, p, block=block, device=ddev, vdim=3)
+        pspace = structured.BoxSpace(mesh, p, block=block, device=ddev)
+        geom = geometry.DeviceGeometry(mesh, vspace.basis.quad)
+        super().__init__(vspace, pspace, geom, k, dt, nu, forcing=forcing, config=config)
+
+    def _pressure_cycle(self):
+        from . import structured
+        return structured.BoxLORPreconditioner(self.pspace, "stiffness", dirichlet_attrs=None,
+                                               pure_neumann=True, block=self._block)
+
+    def _helmholtz_cycle(self, c):
+        from . import structured
+        return structured.BoxLORPreconditioner(self._scalar_v, "helmholtz", nu=self.nu, c=c,
+                                               block=self._block)
+
+    def _scalar_velocity_space(self):
+        return self.pspace  # same degree, same box numbering
+
+    def _domain_volume(self):
+        from .geometry import compute_geometric_factors
+        from .quadrature import GAUSS_LEGENDRE, quadrature_rule
+        g = compute_geometric_factors(self.vspace.mesh, quadrature_rule(GAUSS_LEGENDRE, 2))
+        return float(np.sum(g.detj @ g.w))
