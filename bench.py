@@ -509,7 +509,53 @@ def callers(stokes_cases=((2, 2), (2, 4), (2, 6), (3, 2)), tgv=(5, 16, 4)):
         "phase_ms": phases,
         "kinetic_energy": st.kinetic_energy(),
         "scheme": "BDF3/EXT3, dt 0.02, nu 1/1600; timed after the 3 start-up steps (setup_s)"}
+    del st
+    out.update(box_tgv(p=p, n=32, steps=2))
     return out
+
+
+def box_tgv(p=5, n=32, steps=2):
+    """cfg5 at size on one GPU: the periodic Taylor-Green projection in scale
+    mode (timeint.BoxProjectionStepper: BoxSpace numbering, device-built
+    pure-Neumann / Helmholtz block-ILU hierarchies), n^3 elements."""
+    import gc
+    import torch
+    from paper_1910_03032_b200 import geometry, timeint
+    gc.collect()
+    torch.cuda.empty_cache()
+    m = geometry.cartesian_mesh((n, n, n), lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                                periodic=(True,) * 3)
+    t0 = time.perf_counter()
+    st = timeint.BoxProjectionStepper(m, p, k=3, dt=0.02, nu=1.0 / 1600.0)
+
+    def tgv_u(x):
+        X, Y, Z = x[:, 0], x[:, 1], x[:, 2]
+        return np.stack([np.sin(X) * np.cos(Y) * np.cos(Z), -np.cos(X) * np.sin(Y) * np.cos(Z),
+                         np.zeros_like(X)], axis=1)
+
+    st.initialize(st.vspace.project(tgv_u))
+    for _ in range(3):
+        st.step()
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    its = []
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = st.step()
+        its.append([r.mass_iters, r.pressure_iters, r.helmholtz_iters])
+    torch.cuda.synchronize()
+    ms = 1e3 * (time.perf_counter() - t0) / steps
+    st.profile = True
+    phases = st.step().phase_ms
+    res = {f"tgv3d_projection_scale_mode_p{p}_{n}^3": {
+        "velocity_dofs": int(st.vspace.ndofs), "pressure_dofs": int(st.pspace.ndofs),
+        "ms_per_step": round(ms, 2), "steps": steps, "iterations_mass_pressure_helmholtz": its,
+        "setup_s": round(setup, 2), "phase_ms": phases, "kinetic_energy": st.kinetic_energy(),
+        "scheme": "BDF3/EXT3, dt 0.02, nu 1/1600, scale mode (BoxProjectionStepper)"}}
+    del st
+    gc.collect()
+    torch.cuda.empty_cache()
+    return res
 
 
 def mixed_and_vector_ops(reps=10, target=TARGET_DOFS / 3):

@@ -482,9 +482,16 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
             vec.axpby(1.0, self._dk, 1.0, x, st)
 
     def clone_workspace(self):
+        """Concurrent copy for BlockDiagonalPreconditioner: own level vectors
+        and own transfers (a transfer keeps its per-element restriction
+        contributions in a device buffer, so clones must not share it)."""
         c = super().clone_workspace()
         if c is not None:
             c._rk = c._dk = None
+            c.transfers = [BoxTransfer(self.spaces[i], self.spaces[i + 1])
+                           for i in range(len(self.spaces) - 1)]
+            c._P = [_Prolong(T) for T in c.transfers]
+            c._Pt = [_Restrict(T) for T in c.transfers]
         return c
 
     def level_bytes(self):
