@@ -511,7 +511,7 @@ __global__ void csr_pin_kernel(int64_t n, const int64_t* __restrict__ ip,
 }
 
 int fb_csr_pin(fb_csr* A, int64_t dof) {
-  FB_REQUIRE(A != nullptr && dof >= 0 && dof < A->nrows, "bad pin");
+  FB_REQUIRE(A != nullptr && dof >= 0 && dof < A->ncols, "bad pin");  // a ghost column may be pinned
   if (A->nrows == 0) return FB_OK;
   csr_pin_kernel<<<ceil_div(A->nrows, 256), 256>>>(A->nrows, A->indptr.ptr, A->indices.ptr,
                                                    A->data.ptr, dof);

@@ -79,6 +79,20 @@ class TorchComm:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
 
+    def exchange_ring(self, send_down, send_up, recv_down, recv_up):
+        """Periodic neighbours (rank -+ 1 mod world), in two phases (all
+        up-going messages, then all down-going ones) so that a 2-rank ring,
+        where both neighbours are the same peer, pairs messages correctly."""
+        w = self.world
+        up, down = (self.rank + 1) % w, (self.rank - 1) % w
+        P2P = self.dist.P2POp
+        for ops in ([(send_up, self.dist.isend, up), (recv_down, self.dist.irecv, down)],
+                    [(send_down, self.dist.isend, down), (recv_up, self.dist.irecv, up)]):
+            ops = [P2P(fn, t, peer) for t, fn, peer in ops if t is not None]
+            if ops:
+                for req in self.dist.batch_isend_irecv(ops):
+                    req.wait()
+
     def allreduce_sum(self, t):
         self.dist.all_reduce(t)
         return t
@@ -139,6 +153,17 @@ class ThreadComm:
             recv_down.copy_(h.slots[(r - 1, "up")])
         if recv_up is not None:
             recv_up.copy_(h.slots[(r + 1, "down")])
+        self._sync()
+
+    def exchange_ring(self, send_down, send_up, recv_down, recv_up):
+        h, r, w = self.hub, self.rank, self.world
+        h.slots[(r, "rdown")] = send_down
+        h.slots[(r, "rup")] = send_up
+        self._sync()
+        if recv_down is not None:
+            recv_down.copy_(h.slots[((r - 1) % w, "rup")])
+        if recv_up is not None:
+            recv_up.copy_(h.slots[((r + 1) % w, "rdown")])
         self._sync()
 
     def allreduce_sum(self, t):

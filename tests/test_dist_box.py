@@ -123,3 +123,55 @@ def test_sharded_lor_pcg_matches_single_gpu(world, counts, p):
     assert abs(out[0][4].iterations - rep_ref.iterations) <= 1, (out[0][4].iterations,
                                                                  rep_ref.iterations)
     assert rel_err(x, x_ref) < 1e-7
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,counts,p,kind", [(2, (4, 6, 8), 3, "stiffness"),
+                                                  (3, (6, 4, 12), 5, "stiffness"),
+                                                  (2, (6, 6, 8), 4, "helmholtz")])
+def test_periodic_ring_lor_pcg_matches_single_gpu(world, counts, p, kind):
+    """cfg5 building block on N ranks: periodic [-pi, pi]^3 box sharded into
+    z-slabs on a ring (dist_periodic.py).  The sharded operator equals the
+    single-GPU BoxSpace operator; the pure-Neumann Poisson solve (pinned
+    levels, mean projection) or the Helmholtz solve gives the single-GPU
+    scale-mode iteration count and solution."""
+    import torch
+    from paper_1910_03032_b200 import dist_box as D, dist_periodic as DP, geometry, mfop
+    from paper_1910_03032_b200 import solvers, structured as S
+    pn = kind == "stiffness"
+    c = 0.0 if pn else 10.0
+    cfg = solvers.SolverConfig(rel_tol=1e-10 if pn else 1e-8, max_iters=300)
+    mesh = geometry.cartesian_mesh(counts, lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                                   periodic=(True,) * 3)
+    space = S.BoxSpace(mesh, p, block=2, device=torch.device("cuda"))
+    op = mfop.setup(kind, space=space, geom=geometry.DeviceGeometry(mesh, space.basis.quad),
+                    nu=1.0, c=c)
+    if pn:
+        pre = S.BoxLORPreconditioner(space, kind, dirichlet_attrs=None, pure_neumann=True)
+    else:
+        pre = S.BoxLORPreconditioner(space, kind, nu=1.0, c=c)
+
+    def fn(comm):
+        pr = DP.periodic_slab_problem(comm, counts, p, kind=kind, c=c, pure_neumann=pn, mesh=mesh)
+        lv = pr["level"]
+        y = torch.empty_like(pr["b"])
+        pr["A"].apply_into(pr["b"], y)
+        x, rep = DP.dist_cg(pr["A"], pr["b"], pr["M"], comm, lv.n_own, cfg, project=pr["project"])
+        return (lv.off, lv.n_own, y[:lv.n_own].cpu().numpy(), x[:lv.n_own].cpu().numpy(), rep,
+                pr["b_global"].cpu().numpy())
+
+    out = D.run_threads(world, fn)
+    bg = torch.from_numpy(out[0][5]).cuda()
+    y_ref = op.apply(bg).cpu().numpy()
+    x_ref, rep_ref = solvers.cg(op, bg, precond=pre, config=cfg,
+                                project=solvers.MeanProjector() if pn else None)
+    x_ref = x_ref.cpu().numpy()
+    assert [o[0] for o in out] == list(np.cumsum([0] + [o[1] for o in out[:-1]]))
+    y = np.concatenate([o[2] for o in out])
+    x = np.concatenate([o[3] for o in out])
+    assert rel_err(y, y_ref) < 1e-13
+    for o in out:
+        assert o[4].iterations == out[0][4].iterations and o[4].converged
+    assert abs(out[0][4].iterations - rep_ref.iterations) <= 1, (out[0][4].iterations,
+                                                                 rep_ref.iterations)
+    assert rel_err(x, x_ref) < 1e-7
