@@ -380,3 +380,239 @@ def periodic_slab_problem(comm, counts, p, kind="stiffness", c=0.0, nu=1.0, bloc
     proj = DistMean(comm, lv.n_own, N) if pure_neumann else None
     return {"level": lv, "A": A, "M": M, "b": b, "b_global": bg, "project": proj,
             "layers": layers, "mesh": mesh}
+
+
+# ---------------------------------------------------------------------------
+# the projection step on the ring (cfg5 on N GPUs)
+# ---------------------------------------------------------------------------
+
+class VectorView:
+    """vdim-component view of a ring slab level (SoA, component stride
+    n_local): the space-like object the vector operators see."""
+
+    def __init__(self, lv, vdim=3):
+        self.lv, self.vdim = lv, vdim
+        self.mesh, self.p, self.dim, self.basis = lv.mesh, lv.p, 3, lv.basis
+        self.ndofs_scalar = lv.n_local
+
+    @property
+    def ndofs(self):
+        return self.vdim * self.ndofs_scalar
+
+    @property
+    def element_dofs(self):
+        return self.lv.element_dofs
+
+
+class DistFieldOperator:
+    """Slab operator between (vector) fields on the ring: ghost update of
+    every input component, the local fused kernel, cut-plane partial sums of
+    every output component."""
+
+    def __init__(self, apply_local, lv, comm, vin, vout):
+        self.apply_local, self.lv, self.comm, self.vin, self.vout = apply_local, lv, comm, vin, vout
+        n = lv.n_local
+        self.shape = (vout * n, vin * n)
+
+    def apply_into(self, x, y, stream=None):
+        lv, n = self.lv, self.lv.n_local
+        for c in range(self.vin):
+            lv.ghost_update(self.comm, x[c * n:(c + 1) * n])
+        self.apply_local(x, y)
+        for c in range(self.vout):
+            lv.sum_planes(self.comm, y[c * n:(c + 1) * n])
+        return y
+
+    def apply(self, x):
+        y = dev.empty(self.shape[0])
+        return self.apply_into(x, y)
+
+
+class DistProjectionStepper:
+    """ProjectionStepper (timeint.py:218-388) for the periodic Taylor-Green
+    box sharded over z-slabs on a ring, one rank per GPU: slab operators
+    (mass, convection, G, G^T, D, pressure stiffness, vector Helmholtz) with
+    ring halos, distributed CG (owned-slice dots + all-reduce), ring LOR
+    V-cycles (pure-Neumann pressure with the distributed mean projection;
+    one Helmholtz cycle per velocity component) and the collocated mass
+    diagonal assembled with cut-plane sums.  Same step, same preconditioners
+    as timeint.BoxProjectionStepper on one GPU."""
+
+    def __init__(self, comm, mesh, p, k, dt, nu, block=2, q1_block=4, config=None):
+        from .solvers import DiagonalPreconditioner, SolverConfig, collocated_mass_diagonal
+        from .timeint import bdf_coefficients  # noqa: F401 (validated in step)
+        self.comm, self.mesh, self.k, self.dt, self.nu = comm, mesh, int(k), float(dt), float(nu)
+        self.block, self.q1_block = block, q1_block
+        self.config = config or SolverConfig(rel_tol=1e-10, max_iters=400)
+        r, w = comm.rank, comm.world
+        ddev = dev.device()
+        nz = mesh.counts[2]
+        self.layers = slab_layers(nz, w, int(np.lcm(block, q1_block)))
+        degs = [d for d in lor_mod.degree_ladder(p) if d > 1]
+        self.levels = [PeriodicSlabLevel(mesh, d, block, self.layers, r, w, ddev) for d in degs]
+        lv = self.lv = self.levels[0]
+        self.vv = VectorView(lv, 3)
+        n = self.n = lv.n_local
+        geom = geometry.DeviceGeometry(lv.mesh_elems, lv.basis.quad)
+        self.geom = geom
+        M = mfop.MassOperator(self.vv, geom)
+        conv = mfop.ConvectionOperator(self.vv, geom)
+        G = mfop.GradientOperator(self.vv, lv, geom)
+        D = mfop.DivergenceOperator(self.vv, lv, geom)
+        Lp = mfop.StiffnessOperator(lv, geom)
+        self.M = DistFieldOperator(M.apply_into, lv, comm, 3, 3)
+        self.conv = DistFieldOperator(conv.apply_into, lv, comm, 3, 3)
+        self.G = DistFieldOperator(G.apply_into, lv, comm, 1, 3)
+        self.Gt = DistFieldOperator(G.apply_transpose_into, lv, comm, 3, 1)
+        self.D = DistFieldOperator(D.apply_into, lv, comm, 3, 1)
+        self.Lp = DistFieldOperator(Lp.apply_into, lv, comm, 1, 1)
+        self._ops = (M, conv, G, D, Lp)
+        # collocated (GLL) mass diagonal: element sums + cut-plane sums
+        dl = dev.to_device(collocated_mass_diagonal(lv))
+        lv.sum_planes(comm, dl)
+        lv.ghost_update(comm, dl)
+        self.pressure_weights = dl
+        dh = dl.cpu().numpy()
+        self.mass_pre = DiagonalPreconditioner(np.concatenate([dh, dh, dh]))
+        N = int(np.prod([a * p for a in mesh.counts]))
+        self.N = N
+        self.mean = DistMean(comm, lv.n_own, N)
+        self.pressure_pre = DistPeriodicLOR(mesh, p, "stiffness", comm, self.layers,
+                                            block=block, q1_block=q1_block, pure_neumann=True,
+                                            levels=self.levels)
+        self._helm = {}
+        self._wsum = None
+        from .geometry import compute_geometric_factors
+        from .quadrature import GAUSS_LEGENDRE, quadrature_rule
+        gq = compute_geometric_factors(mesh, quadrature_rule(GAUSS_LEGENDRE, 2))
+        self._volume = float(np.sum(gq.detj @ gq.w))
+        self.t = self.u = self.p = None
+        self.u_hist, self.n_hist = [], []
+
+    # -- distributed reductions ------------------------------------------------------
+    def _dot(self, x, y, out, ncomp):
+        n, no = self.n, self.lv.n_own
+        vec.dot_into(x[:no], y[:no], out)
+        if ncomp > 1:
+            tmp = dev.zeros(1)
+            for c in range(1, ncomp):
+                vec.dot_into(x[c * n:c * n + no], y[c * n:c * n + no], tmp)
+                vec.axpby(1.0, tmp, 1.0, out)
+        self.comm.allreduce_sum(out)
+        return out
+
+    def _cg(self, A, b, pre, ncomp, x0=None, project=None):
+        return solvers.cg(A, b, precond=pre, config=self.config, x0=x0, project=project,
+                          inner=lambda x, y, out: self._dot(x, y, out, ncomp))
+
+    def _weighted_mean_free(self, v):
+        """v - (sum w v / sum w): deflate_mean with the collocated weights."""
+        no = self.lv.n_own
+        w = self.pressure_weights
+        if self._wsum is None:
+            s = dev.zeros(1)
+            vec.dot_into(w[:no], torch.ones(no, dtype=torch.float64, device=w.device), s)
+            self.comm.allreduce_sum(s)
+            self._wsum = float(s.item())
+        num = dev.zeros(1)
+        vec.dot_into(w[:no], v[:no], num)
+        self.comm.allreduce_sum(num)
+        out = torch.empty_like(v)
+        vec.shift_ratio(v, num, self._wsum, out)
+        return out
+
+    # -- state --------------------------------------------------------------------------
+    def scatter_global_velocity(self, u_global):
+        """This rank's local velocity (owned slices of the global block-major
+        SoA vector, ghosts filled by the first operator apply)."""
+        lv, n, ng = self.lv, self.n, self.N
+        u = dev.zeros(3 * n)
+        ug = dev.to_device(np.asarray(u_global, dtype=np.float64))
+        for c in range(3):
+            vec.copy(ug[c * ng + lv.off:c * ng + lv.off + lv.n_own], u[c * n:c * n + lv.n_own])
+        return u
+
+    def gather_owned(self, v, ncomp):
+        n, no = self.n, self.lv.n_own
+        parts = [v[c * n:c * n + no] for c in range(ncomp)]
+        return [self.comm.allgather(pt, self._sizes()) for pt in parts]
+
+    def _sizes(self):
+        if not hasattr(self, "_sz"):
+            t = torch.tensor([float(self.lv.n_own)], dtype=torch.float64, device=dev.device())
+            self._sz = [int(v) for v in self.comm.allgather(t, [1] * self.comm.world).tolist()]
+        return self._sz
+
+    def initialize(self, u_global, t0=0.0):
+        self.t = float(t0)
+        self.u = self.scatter_global_velocity(u_global)
+        self.p = dev.zeros(self.n)
+        self.u_hist = [self.u.clone()]
+        self.n_hist = [self._nodal_convection(self.u)[0]]
+        return self
+
+    def _mass_solve(self, rhs):
+        from .solvers import SolverConfig
+        tol = min(1e-12, self.config.rel_tol)
+        x, rep = solvers.cg(self.M, rhs, precond=self.mass_pre,
+                            config=SolverConfig(rel_tol=tol, max_iters=300),
+                            inner=lambda a, b, out: self._dot(a, b, out, 3))
+        if not rep.converged:
+            raise RuntimeError(f"mass solve failed: {rep}")
+        return x, rep.iterations
+
+    def _nodal_convection(self, u):
+        y = self.conv.apply(u)
+        vec.scale(-1.0, y, y)
+        return self._mass_solve(y)
+
+    def _helmholtz(self, b0):
+        key = round(b0, 12)
+        if key not in self._helm:
+            c = b0 / self.dt
+            op = mfop.HelmholtzOperator(self.vv, self.geom, c=c, nu=self.nu)
+            A = DistFieldOperator(op.apply_into, self.lv, self.comm, 3, 3)
+            cyc = DistPeriodicLOR(self.mesh, self.lv.p, "helmholtz", self.comm, self.layers,
+                                  nu=self.nu, c=c, block=self.block, q1_block=self.q1_block,
+                                  levels=self.levels)
+            pre = solvers.BlockDiagonalPreconditioner(cyc, 3, self.n)
+            self._helm[key] = (op, A, pre)
+        return self._helm[key]
+
+    def step(self):
+        from .timeint import StepReport, _combo, bdf_coefficients
+        k_eff = min(self.k, len(self.u_hist))
+        s = bdf_coefficients(k_eff)
+        dt, t_new = self.dt, self.t + self.dt
+        b0 = s.b[0]
+        rep = StepReport(t=t_new)
+        nv = 3 * self.n
+        terms = [(-s.b[j] / dt, self.u_hist[j - 1]) for j in range(1, k_eff + 1)]
+        terms += [(s.a[j - 1], self.n_hist[j - 1]) for j in range(1, k_eff + 1)]
+        F = _combo(terms, nv)
+        rhs_p = self.Gt.apply(F)
+        self.mean.apply_into(rhs_p, rhs_p)
+        p, prep = self._cg(self.Lp, rhs_p, self.pressure_pre, 1, x0=self.p, project=self.mean)
+        if not prep.converged:
+            raise RuntimeError(f"pressure solve failed: {prep}")
+        rep.pressure_iters = prep.iterations
+        op, A, pre = self._helmholtz(b0)
+        b_u = self.M.apply(F)
+        vec.axpby(-1.0, self.G.apply(p), 1.0, b_u)
+        u, hrep = self._cg(A, b_u, pre, 3)
+        if not hrep.converged:
+            raise RuntimeError(f"velocity solve failed: {hrep}")
+        rep.helmholtz_iters = hrep.iterations
+        n_new, it_n = self._nodal_convection(u)
+        rep.mass_iters = it_n
+        self.u_hist.insert(0, u)
+        self.n_hist.insert(0, n_new)
+        del self.u_hist[self.k:], self.n_hist[self.k:]
+        self.u, self.p, self.t = u, self._weighted_mean_free(p), t_new
+        return rep
+
+    def kinetic_energy(self):
+        Mu = self.M.apply(self.u)
+        e = dev.zeros(1)
+        self._dot(self.u, Mu, e, 3)
+        return float(e.item()) / (2.0 * self._volume)

@@ -175,3 +175,48 @@ def test_periodic_ring_lor_pcg_matches_single_gpu(world, counts, p, kind):
     assert abs(out[0][4].iterations - rep_ref.iterations) <= 1, (out[0][4].iterations,
                                                                  rep_ref.iterations)
     assert rel_err(x, x_ref) < 1e-7
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,counts,p", [(2, (4, 4, 8), 3), (3, (4, 6, 12), 2)])
+def test_ring_projection_stepper_matches_single_gpu(world, counts, p):
+    """cfg5 on N ranks: the periodic Taylor-Green projection step sharded
+    over a ring of z-slabs (dist_periodic.DistProjectionStepper) against the
+    single-GPU scale-mode stepper (timeint.BoxProjectionStepper, itself pinned
+    to the reference golden): sub-solve counts +-1, velocity and energy."""
+    from paper_1910_03032_b200 import dist_box as D, dist_periodic as DP, geometry, timeint
+    mesh = geometry.cartesian_mesh(counts, lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                                   periodic=(True,) * 3)
+
+    def tgv(x):
+        X, Y, Z = x[:, 0], x[:, 1], x[:, 2]
+        return np.stack([np.sin(X) * np.cos(Y) * np.cos(Z), -np.cos(X) * np.sin(Y) * np.cos(Z),
+                         np.zeros_like(X)], axis=1)
+
+    one = timeint.BoxProjectionStepper(mesh, p, k=3, dt=0.02, nu=1.0 / 1600.0)
+    u0 = one.vspace.project(tgv)
+    one.initialize(u0)
+    ref_its = []
+    for _ in range(4):
+        r = one.step()
+        ref_its.append([r.mass_iters, r.pressure_iters, r.helmholtz_iters])
+    u_ref = one.u.cpu().numpy()
+    e_ref = one.kinetic_energy()
+
+    def fn(comm):
+        st = DP.DistProjectionStepper(comm, mesh, p, k=3, dt=0.02, nu=1.0 / 1600.0)
+        st.initialize(u0)
+        its = []
+        for _ in range(4):
+            r = st.step()
+            its.append([r.mass_iters, r.pressure_iters, r.helmholtz_iters])
+        parts = st.gather_owned(st.u, 3)
+        return its, np.concatenate([q.cpu().numpy() for q in parts]), st.kinetic_energy()
+
+    out = D.run_threads(world, fn)
+    for its, u, e in out:
+        assert its == out[0][0]
+        for a, b in zip(its, ref_its):
+            assert all(abs(x - y) <= 1 for x, y in zip(a, b)), (its, ref_its)
+        assert rel_err(u, u_ref) < 1e-8
+        assert e == pytest.approx(e_ref, rel=1e-10)
