@@ -558,6 +558,67 @@ def box_tgv(p=5, n=32, steps=2):
     return res
 
 
+def _max_over_ranks(v):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def box_tgv_sharded(comm, p=5, n=32, steps=2, reduce_max=None):
+    """cfg5 on N GPUs: the periodic Taylor-Green projection step sharded over
+    z-slabs on a ring (dist_periodic.DistProjectionStepper), strong scaling of
+    the n^3 box (32^3 p = 5: 12.3M velocity + 4.1M pressure DoFs, the
+    single-GPU box_tgv problem).  Per-step time from CUDA events between
+    barriers; reduce_max(ms) -> max over ranks (NCCL all-reduce in the bench)."""
+    import gc
+    import torch
+    from paper_1910_03032_b200 import dist_periodic as DP, geometry
+    gc.collect()
+    torch.cuda.empty_cache()
+    m = geometry.cartesian_mesh((n, n, n), lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                                periodic=(True,) * 3)
+    t0 = time.perf_counter()
+    st = DP.DistProjectionStepper(comm, m, p, k=3, dt=0.02, nu=1.0 / 1600.0)
+
+    def tgv_u(x):
+        X, Y, Z = x[:, 0], x[:, 1], x[:, 2]
+        return np.stack([np.sin(X) * np.cos(Y) * np.cos(Z), -np.cos(X) * np.sin(Y) * np.cos(Z),
+                         np.zeros_like(X)], axis=1)
+
+    st.initialize_from(tgv_u)
+    for _ in range(3):
+        st.step()
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    its = []
+    comm.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        r = st.step()
+        its.append([r.mass_iters, r.pressure_iters, r.helmholtz_iters])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if reduce_max is not None:
+        ms = reduce_max(ms)
+    energy = st.kinetic_energy()
+    res = {f"tgv3d_projection_ring_p{p}_{n}^3": {
+        "velocity_dofs": 3 * (n * p) ** 3, "pressure_dofs": (n * p) ** 3,
+        "ms_per_step": round(ms, 2), "steps": steps, "iterations_mass_pressure_helmholtz": its,
+        "setup_s": round(setup, 2), "kinetic_energy": energy, "n_gpus": comm.world,
+        "scaling": "strong", "layers_per_rank": [b - a for a, b in st.layers],
+        "scheme": "BDF3/EXT3, dt 0.02, nu 1/1600; z-slabs on a periodic ring "
+                  "(dist_periodic.DistProjectionStepper), ring halos over NCCL"}}
+    del st
+    gc.collect()
+    torch.cuda.empty_cache()
+    return res
+
+
 def mixed_and_vector_ops(reps=10, target=TARGET_DOFS / 3):
     """Device time and HBM-roofline fraction of the Stokes / projection
     blocks: the fused mixed-degree kernel's G, G^T, D and
@@ -779,6 +840,12 @@ def run_ours(args, rank, world):
             sharded = lor_pcg_sharded(rank, world)
         except Exception as exc:  # keep the headline line if the auxiliary solve fails
             sharded = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        if not args.no_callers:
+            try:
+                from paper_1910_03032_b200 import dist_box as D
+                sharded.update(box_tgv_sharded(D.TorchComm(), reduce_max=_max_over_ranks))
+            except Exception as exc:
+                sharded["tgv_error"] = f"{type(exc).__name__}: {exc}"[:300]
     if rank != 0:
         return
     peak, peak_kind = load_peaks()

@@ -97,6 +97,9 @@ class TorchComm:
         self.dist.all_reduce(t)
         return t
 
+    def barrier(self):
+        self.dist.barrier()
+
     def allgather(self, t, sizes):
         """Concatenation of every rank's t[:sizes[rank]] (ranks in order)."""
         m = max(sizes)
@@ -164,6 +167,9 @@ class ThreadComm:
             recv_down.copy_(h.slots[((r - 1) % w, "rup")])
         if recv_up is not None:
             recv_up.copy_(h.slots[((r + 1) % w, "rdown")])
+        self._sync()
+
+    def barrier(self):
         self._sync()
 
     def allreduce_sum(self, t):

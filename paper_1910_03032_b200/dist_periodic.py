@@ -543,9 +543,33 @@ class DistProjectionStepper:
             self._sz = [int(v) for v in self.comm.allgather(t, [1] * self.comm.world).tolist()]
         return self._sz
 
+    def local_node_coords(self):
+        """Physical position of each owned local DoF (first-touch element node,
+        as BoxSpace.node_coords); no global vector is formed."""
+        from .spaces import element_node_coords
+        lv = self.lv
+        xyz = element_node_coords(self.vv).reshape(-1, 3)
+        ids = np.asarray(lv.element_dofs).reshape(-1)
+        out = np.zeros((lv.n_local, 3))
+        out[ids[::-1]] = xyz[::-1]  # earliest touching element written last
+        return out[:lv.n_own]
+
+    def initialize_from(self, f, t0=0.0):
+        """Start from the nodal interpolant of f(x) -> (n, 3), evaluated on
+        this rank's owned DoFs only (the bench's 8-GPU path)."""
+        vals = np.asarray(f(self.local_node_coords()), dtype=np.float64)
+        n, no = self.n, self.lv.n_own
+        u = np.zeros(3 * n)
+        for c in range(3):
+            u[c * n:c * n + no] = vals[:, c]
+        return self._start(dev.to_device(u), t0)
+
     def initialize(self, u_global, t0=0.0):
+        return self._start(self.scatter_global_velocity(u_global), t0)
+
+    def _start(self, u, t0):
         self.t = float(t0)
-        self.u = self.scatter_global_velocity(u_global)
+        self.u = u
         self.p = dev.zeros(self.n)
         self.u_hist = [self.u.clone()]
         self.n_hist = [self._nodal_convection(self.u)[0]]

@@ -64,15 +64,21 @@ def _torchcomm_worker(rank, world, port, q):
         comm.exchange(sd, su, rd, ru)
         s = comm.allreduce_sum(torch.tensor([float(r + 1)], dtype=torch.float64))
         g = comm.allgather(torch.arange(r + 1, dtype=torch.float64), list(range(1, w + 1)))
+        # periodic ring: every rank exchanges with both neighbours (mod world)
+        ring_d, ring_u = torch.empty(3), torch.empty(3)
+        comm.exchange_ring(torch.full((3,), float(10 * r + 1)), torch.full((3,), float(10 * r + 2)),
+                           ring_d, ring_u)
         q.put((r, None if rd is None else rd[0].item(), None if ru is None else ru[0].item(),
-               s.item(), g.tolist()))
+               s.item(), g.tolist(), ring_d[0].item(), ring_u[0].item()))
     finally:
         dist.destroy_process_group()
 
 
-def test_torch_comm_over_gloo_matches_thread_comm():
+@pytest.mark.parametrize("world", [2, 3])
+def test_torch_comm_over_gloo_matches_thread_comm(world):
     """The torch.distributed communicator (NCCL on the GPU box) has the
-    same exchange / all-reduce / all-gather semantics (gloo, 3 processes)."""
+    same exchange / ring exchange / all-reduce / all-gather semantics (gloo,
+    2 and 3 processes; on 2 ranks both ring neighbours are the same peer)."""
     import multiprocessing as mp
     import socket
     s = socket.socket()
@@ -81,16 +87,25 @@ def test_torch_comm_over_gloo_matches_thread_comm():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_torchcomm_worker, args=(r, 3, port, q)) for r in range(3)]
+    procs = [ctx.Process(target=_torchcomm_worker, args=(r, world, port, q))
+             for r in range(world)]
     for pr in procs:
         pr.start()
-    out = sorted(q.get(timeout=240) for _ in range(3))
+    out = sorted(q.get(timeout=240) for _ in range(world))
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    assert out[0][1:3] == (None, 11.0) and out[1][1:3] == (2.0, 21.0) and out[2][1:3] == (12.0, None)
-    assert all(o[3] == 6.0 for o in out)
-    assert all(o[4] == [0.0, 0.0, 1.0, 0.0, 1.0, 2.0] for o in out)
+    if world == 3:
+        assert out[0][1:3] == (None, 11.0) and out[1][1:3] == (2.0, 21.0)
+        assert out[2][1:3] == (12.0, None)
+    else:
+        assert out[0][1:3] == (None, 11.0) and out[1][1:3] == (2.0, None)
+    assert all(o[3] == world * (world + 1) / 2 for o in out)
+    gather = [float(j) for i in range(1, world + 1) for j in range(i)]
+    assert all(o[4] == gather for o in out)
+    for r, o in enumerate(out):
+        assert o[5] == 10 * ((r - 1) % world) + 2  # from the lower neighbour's up-send
+        assert o[6] == 10 * ((r + 1) % world) + 1  # from the upper neighbour's down-send
 
 
 @pytest.mark.gpu
@@ -205,7 +220,10 @@ def test_ring_projection_stepper_matches_single_gpu(world, counts, p):
 
     def fn(comm):
         st = DP.DistProjectionStepper(comm, mesh, p, k=3, dt=0.02, nu=1.0 / 1600.0)
+        st.initialize_from(tgv)
+        u_local = st.u.clone()
         st.initialize(u0)
+        assert rel_err(u_local.cpu().numpy(), st.u.cpu().numpy()) < 1e-14
         its = []
         for _ in range(4):
             r = st.step()
