@@ -286,7 +286,7 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
       if (v == 3) return launch_fast_kind<5, 6, 2, 96, 6, 2>(op, x, y, st);
       if (v == 4) return launch_fast_kind<5, 6, 1, 64, 12, 2>(op, x, y, st);
       if (v == 5) return launch_fast_kind<5, 6, 1, 96, 8, 2>(op, x, y, st);
-      if (v == 6) return launch_fast_kind<5, 6, 2, 96, 6, 3>(op, x, y, st);
+      if (v == 6) return launch_fast_kind<5, 6, 2, 96, 5, 3>(op, x, y, st);
       if (v == 7) return launch_fast_kind<5, 6, 2, 64, 8, 3>(op, x, y, st);
       return launch_fast_kind<5, 6, 2, 96, 8>(op, x, y, st);
     case 5:

@@ -214,9 +214,7 @@ struct SF3Shape {
   static constexpr int OFF_WORK = round_up(OFF_X + NE * XBUF * 8, 16);
   static constexpr int ES = NBUF * BUF + SF3Pitch<Q>::PAD;  // element stride (doubles)
   static constexpr int OFF_FAC = round_up(OFF_WORK + NE * ES * 8, 16);
-  // per local DoF: -1 (element interior) or its element-boundary rank
-  static constexpr int OFF_TBL = round_up(OFF_FAC + (FSTAGE ? NE * FACP * 8 : 0), 16);
-  static constexpr int SMEM = OFF_TBL + round_up(NLOC * 2, 16);
+  static constexpr int SMEM = round_up(OFF_FAC + (FSTAGE ? NE * FACP * 8 : 0), 16);
 };
 
 // rank of lattice position (k,j,i) among the element-boundary positions of
@@ -380,16 +378,35 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
       bulk_prefetch_l2_hint(P.fac + e0 * FACP, int64_t(nel_of(batch)) * FACP * 8, fpol);
     }
   };
+  // Per-thread gather / store slots: the batch's local DoFs idx = tid + m NT
+  // (m < GM) map to the same (element, position) in every batch, so their
+  // offsets are computed once: gpk = gather-buffer offset << 16 | map index,
+  // opk = work-buffer offset << 16 | slot index in the staged transposed map
+  // (0xFFFF: element-interior DoF, stored straight to y).
+  constexpr int GM = (NE * NLOC + NT - 1) / NT;
+  static_assert(NE * Sh::XBUF < 65536 && NE * ES < 65536 && NE * NBP < 65535 &&
+                NE * NLOCP < 65536, "16-bit slot offsets");
+  uint32_t gpk[GM], opk[GM];
+#pragma unroll
+  for (int m = 0; m < GM; ++m) {
+    const int idx = tid + m * NT;
+    const int el = idx / NLOC, l = idx - el * NLOC;
+    const int i = l % N, j = (l / N) % N, k = l / (N * N);
+    const bool inner = i > 0 && i < N - 1 && j > 0 && j < N - 1 && k > 0 && k < N - 1;
+    gpk[m] = (uint32_t(el * Sh::XBUF + XI(k, j, i)) << 16) | uint32_t(el * NLOCP + l);
+    opk[m] = (uint32_t(el * ES + l) << 16) |
+             (inner ? 0xFFFFu : uint32_t(el * NBP + boundary_rank3<N>(k, j, i)));
+  }
   // all threads: cp.async gathers of component `comp` of `batch` into sx
   auto issue_gather = [&](int batch, int comp, int s) {
     const int nel = nel_of(batch);
     const int* smap = stage_map(s);
     const double* xc = P.x + comp * P.x_comp_stride;
-#pragma unroll 4
-    for (int idx = tid; idx < nel * NLOC; idx += NT) {
-      const int el = idx / NLOC, l = idx - el * NLOC;
-      const int i = l % N, j = (l / N) % N, k = l / (N * N);
-      cp_async8(smem_u32(sx + el * Sh::XBUF + XI(k, j, i)), xc + smap[el * NLOCP + l]);
+    const uint32_t sx0 = smem_u32(sx);
+#pragma unroll
+    for (int m = 0; m < GM; ++m) {
+      if (tid + m * NT < nel * NLOC)
+        cp_async8(sx0 + (gpk[m] >> 16) * 8u, xc + smap[gpk[m] & 0xFFFFu]);
     }
     cp_async_commit();
   };
@@ -397,12 +414,6 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
   if (tid == 0) {
     for (int h = 0; h < Sh::NSTAGE + (Sh::FSTAGE ? 1 : 0); ++h) mbar_init(smem_u32(&bars[h]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  int16_t* btbl = reinterpret_cast<int16_t*>(smem_raw + Sh::OFF_TBL);
-  for (int l = tid; l < NLOC; l += NT) {
-    const int i = l % N, j = (l / N) % N, k = l / (N * N);
-    const bool inner = i > 0 && i < N - 1 && j > 0 && j < N - 1 && k > 0 && k < N - 1;
-    btbl[l] = inner ? int16_t(-1) : int16_t(boundary_rank3<N>(k, j, i));
   }
   const bool direct_out = (P.skip >> 12) & 1;  // diagnostics: the line-order stores
   __syncthreads();
@@ -817,13 +828,14 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
         // an element's interior block (contiguous in y) and its runs of
         // transposed-map slots are written with coalesced stores
         __syncthreads();
-#pragma unroll 4
-        for (int L = tid; L < nel * NLOC; L += NT) {
-          const int el = L / NLOC, l = L - el * NLOC;
-          const double v = smem[el * ES + l];
-          const int rk = btbl[l];
-          if (rk < 0) y[smap[el * NLOCP + l]] = 0.0 + v;  // bincount: 0.0 + contribution
-          else S[spos[el * NBP + rk]] = v;
+#pragma unroll
+        for (int m = 0; m < GM; ++m) {
+          if (tid + m * NT < nel * NLOC) {
+            const double v = smem[opk[m] >> 16];
+            const uint32_t sl = opk[m] & 0xFFFFu;
+            if (sl == 0xFFFFu) y[smap[gpk[m] & 0xFFFFu]] = 0.0 + v;  // bincount: 0.0 + contribution
+            else S[spos[sl]] = v;
+          }
         }
       }
     }
