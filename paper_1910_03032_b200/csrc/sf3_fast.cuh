@@ -831,10 +831,13 @@ __global__ void __launch_bounds__(NT, MINB) sf3_fast_kernel(const __grid_constan
 #pragma unroll
         for (int m = 0; m < GM; ++m) {
           if (tid + m * NT < nel * NLOC) {
+            // branch-free: interior DoF -> y[map] (bincount: 0.0 + contribution),
+            // boundary DoF -> its slot S[spos]
             const double v = smem[opk[m] >> 16];
             const uint32_t sl = opk[m] & 0xFFFFu;
-            if (sl == 0xFFFFu) y[smap[gpk[m] & 0xFFFFu]] = 0.0 + v;  // bincount: 0.0 + contribution
-            else S[spos[sl]] = v;
+            const bool inner = sl == 0xFFFFu;
+            const int di = inner ? smap[gpk[m] & 0xFFFFu] : spos[sl];
+            (inner ? y : S)[di] = inner ? 0.0 + v : v;
           }
         }
       }
