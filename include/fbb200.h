@@ -239,6 +239,9 @@ int fb_blockilu_info(const fb_blockilu* B, int64_t* n, int64_t* nnz_lower, int64
                      int* ell_width);
 int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r_dev, double* out_dev,
                       void* stream);
+/* Sweep the factor runs: 0 = CSR level loop, 1 = ELL, 2 = level-packed
+ * TMA ring (fb_set_blockilu_packed). */
+int fb_blockilu_sweep_kind(const fb_blockilu* B);
 /* y = M x for a dense row-major n x n matrix (coarse-level inverse). */
 int fb_dense_mv(int64_t n, const double* M_dev, const double* x_dev, double* y_dev, void* stream);
 /* LOR matrix of a degree-p space on its nodal sub-cell mesh (lor.py:61-99):
@@ -302,7 +305,10 @@ int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks, const int64_t* bloc
  * results in every mode. */
 int fb_set_blockilu_pipeline(int mode, int lanes);
 /* 1 (default): factors created afterwards with blocks of more than 160 rows
- * use the level-packed layout and the TMA-ring sweep; 0: CSR / ELL sweeps. */
+ * (on grids of many blocks) use the level-packed layout and the TMA-ring
+ * sweep, which splits each row over 1-4 lanes (same factor; the row sums are
+ * taken in a different fixed order, so results agree with the CSR / ELL
+ * sweeps to rounding, and are deterministic); 0: CSR / ELL sweeps. */
 int fb_set_blockilu_packed(int on);
 /* Nodal interpolation between two levels of a structured box, matrix-free
  * (lor.py:102-123).  fine: map of the fine level (ne, nf^3); hmap: for each

@@ -994,6 +994,48 @@ __host__ __device__ inline size_t packed_smem(int nslot, int max_chunk, int max_
          size_t(max_grp + 1) * 16;
 }
 
+// One dependency level of a packed chunk: rows t < R, S lanes per row.
+// Lane `sub` of a row accumulates entries sub, sub + S, ... with fma; the S
+// partial sums are combined by xor shuffles in a fixed order, so the result
+// is deterministic (not bitwise the sequential CSR chain).
+template <int S>
+__device__ __forceinline__ void packed_rows(const double* vals, const double* inv,
+                                            const unsigned short* cols,
+                                            const unsigned short* rows,
+                                            const unsigned short* rst,
+                                            const unsigned short* cnt, int R, int has_inv,
+                                            double* y) {
+  constexpr int LG = (S == 4) ? 2 : (S == 2) ? 1 : 0;
+  constexpr int U = (kRowBuf + S - 1) / S;  // unrolled entries per lane
+  const int lane = threadIdx.x;
+  const int sub = lane & (S - 1);
+  for (int t0 = 0; t0 < R; t0 += (32 >> LG)) {
+    const int t = t0 + (lane >> LG);
+    const bool live = t < R;
+    const int start = live ? rst[t] : 0, n = live ? cnt[t] : 0;
+    double av[U], yv[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int u = sub + k * S;
+      const bool ok = u < n;
+      av[k] = ok ? vals[start + u] : 0.0;
+      yv[k] = ok ? y[cols[start + u]] : 0.0;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < U; ++k) acc = fma(av[k], yv[k], acc);
+    for (int u = sub + U * S; u < n; u += S)  // first-touch order: up to 26 lower neighbours
+      acc = fma(vals[start + u], y[cols[start + u]], acc);
+    if constexpr (S >= 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if constexpr (S >= 4) acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (live && sub == 0) {
+      const int row = rows[t];
+      const double res = y[row] - acc;
+      y[row] = has_inv ? res * inv[t] : res;
+    }
+  }
+}
+
 // Levels are staged K at a time (one bulk copy spans K consecutive chunks of
 // the block; NSLOT spans in flight), so the mbarrier wait and the copy issue
 // are paid once per K levels.
@@ -1036,25 +1078,11 @@ __device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, 
       const unsigned short* rows = cols + E;
       const unsigned short* rst = rows + R;  // per row: first entry, entry count
       const unsigned short* cnt = rst + R;
-      for (int t = lane; t < R; t += 32) {
-        const int start = rst[t], n = cnt[t], row = rows[t];
-        // all loads of the row first (independent), then the sequential chain
-        double av[kRowBuf], yv[kRowBuf];
-#pragma unroll
-        for (int u = 0; u < kRowBuf; ++u) {
-          const bool ok = u < n;
-          av[u] = ok ? vals[start + u] : 0.0;
-          yv[u] = y[ok ? cols[start + u] : row];
-        }
-        double acc = 0.0;
-#pragma unroll
-        for (int u = 0; u < kRowBuf; ++u)
-          if (u < n) acc = __dadd_rn(acc, __dmul_rn(av[u], yv[u]));
-        for (int u = kRowBuf; u < n; ++u)  // first-touch order: up to 26 lower neighbours
-          acc = __dadd_rn(acc, __dmul_rn(vals[start + u], y[cols[start + u]]));
-        const double res = __dsub_rn(y[row], acc);
-        y[row] = T.has_inv ? __dmul_rn(res, inv[t]) : res;
-      }
+      // S lanes per row (levels are narrow: ~6 rows at p = 4), each summing
+      // a strided share of the row's entries, combined by a fixed xor tree
+      if (R <= 8) packed_rows<4>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
+      else if (R <= 16) packed_rows<2>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
+      else packed_rows<1>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
       __syncwarp();
     }
     if (lane == 0 && j + NSLOT < NG) {
@@ -1357,6 +1385,11 @@ int fb_blockilu_info(const fb_blockilu* B, int64_t* n, int64_t* nnz_lower, int64
   if (nnz_upper) *nnz_upper = B->U.nnz ? B->U.nnz : B->U.ix.n;  // strict upper (+ inverse diagonal)
   if (ell_width) *ell_width = B->ell_w;
   return FB_OK;
+}
+
+int fb_blockilu_sweep_kind(const fb_blockilu* B) {
+  FB_REQUIRE(B != nullptr, "block ILU is NULL");
+  return B->L.pk.ptr ? 2 : (B->ell_w ? 1 : 0);
 }
 
 void fb_blockilu_destroy(fb_blockilu* B) {

@@ -54,5 +54,6 @@ for packed in (0, 1):
     del prob, A, M, b, sm
     torch.cuda.empty_cache()
 res["fwd_bitwise_equal"] = bool(torch.equal(xs[0][0], xs[1][0]))
-res["x_equal"] = bool(torch.equal(xs[0][1], xs[1][1]))
+res["fwd_rel_diff"] = float((xs[0][0] - xs[1][0]).norm() / xs[0][0].norm())
+res["x_rel_diff"] = float((xs[0][1] - xs[1][1]).norm() / xs[0][1].norm())
 print(json.dumps(res), flush=True)
