@@ -55,6 +55,9 @@ struct TriPart {
 };
 
 }  // namespace
+namespace {
+inline bool small_grid(const fb_blockilu* B);  // grids of a few waves (below)
+}  // namespace
 
 static int g_bilu_pipe = 2;  // 0: CSR sweep, 1: CSR + next-level loads, 2: padded rows for large blocks, else 1
 static int g_bilu_lanes = 0;  // 0 = by block size
@@ -535,9 +538,28 @@ __global__ void ell_fill_kernel(int64_t n, int nblocks, const int* __restrict__ 
 
 
 // lanes per block: small blocks (p <= 2 levels, ~1.5 rows per dependency
-// level) share a warp 16 ways; larger blocks are smem-bound (18 B per row)
-// and run one per warp (measured, tools/box_profile.py)
-inline int block_ilu_lanes(int max_block) { return max_block <= 160 ? 2 : 32; }
+// level) run the quad-row sweep with 8 lanes (4 blocks per warp), 16 on grids
+// of a few waves (latency bound); larger blocks are smem-bound (18 B per row)
+// and run one per warp.  Measured with tools/vcycle_breakdown.py and
+// tools/box_tgv.py: cfg3 p = 4 small-block sweeps 7.05 -> 5.58 ms per V-cycle,
+// TGV 16^3 p = 5 227 -> 168 ms per step against 2 lanes (sequential chain).
+inline int small_block_lanes() {  // FB_BILU_SMALL_LANES=<2|4|8|16>: A/B runs (0: auto)
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("FB_BILU_SMALL_LANES");
+    v = env ? atoi(env) : 0;
+  }
+  return v;
+}
+inline int block_ilu_lanes(const fb_blockilu* B) {
+  if (B->max_block > 160) return 32;
+  const int v = small_block_lanes();
+  return v > 0 ? v : (small_grid(B) ? 16 : 8);
+}
+// shared memory of the widest launch (small blocks: up to 16 per warp)
+inline size_t block_ilu_smem_max(int max_block) {
+  return block_ilu_smem(max_block) * (max_block <= 160 ? 16 : 1);
+}
 
 template <int LPB, int PIPE>
 int launch_block_ilu(const fb_blockilu* B, TriView a, TriView b, const double* r, double* out,
@@ -1205,6 +1227,15 @@ static int pack_span_budget() {  // FB_BILU_SPAN=<bytes>: A/B runs (tools/bilu_a
   return v > 0 ? v : kPackSpanBudget;
 }
 
+static int pack_slots() {  // FB_BILU_NSLOT=<2..4>: spans in flight per block (A/B runs)
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("FB_BILU_NSLOT");
+    v = env ? atoi(env) : 2;
+  }
+  return v;
+}
+
 static int build_packed_part(fb_blockilu* B, TriPart& P, bool has_inv) {
   const int64_t nlev = P.grp.n - 1;
   if (nlev <= 0) return FB_OK;
@@ -1358,7 +1389,7 @@ int fb_blockilu_create(int64_t n, int nblocks, const int64_t* block_ptr,
   if (rc != FB_OK) return rc;
   FB_TRY_CUDA(B->block_ptr.upload(bptr.data(), nblocks + 1));
   FB_TRY_CUDA(B->new2old.upload(n2o.data(), n));
-  FB_REQUIRE(block_ilu_smem(B->max_block) * (32 / block_ilu_lanes(B->max_block)) <= 200 * 1024 &&
+  FB_REQUIRE(block_ilu_smem_max(B->max_block) <= 200 * 1024 &&
                  B->max_block <= 65535,
              "block too large for shared memory");
   {
@@ -1411,9 +1442,13 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
     const TriPart& pa = transpose ? B->Ut : B->L;
     const TriPart& pb = transpose ? B->Lt : B->U;
     const bool ua = !transpose, ub = transpose;  // unit diagonal: L and L^T
-    return launch_packed<2>(B, pa, ua, pb, ub, r, out, st);
+    switch (pack_slots()) {
+      case 3: return launch_packed<3>(B, pa, ua, pb, ub, r, out, st);
+      case 4: return launch_packed<4>(B, pa, ua, pb, ub, r, out, st);
+      default: return launch_packed<2>(B, pa, ua, pb, ub, r, out, st);
+    }
   }
-  const int lanes = g_bilu_lanes ? g_bilu_lanes : block_ilu_lanes(B->max_block);
+  const int lanes = g_bilu_lanes ? g_bilu_lanes : block_ilu_lanes(B);
   if (B->ell_w) {
     const int l2 = lanes == 2 ? 2 : 32;
     switch (B->ell_w) {
@@ -1423,7 +1458,9 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
       default: return launch_ell_w<32>(B, l2, a, b, r, out, st);
     }
   }
-  const bool pipe = g_bilu_pipe >= 1;
+  // small blocks: quad-row sweep (FB_BILU_SMALL_QUAD=0: the sequential-chain sweep, A/B runs)
+  static const bool small_quad = !(getenv("FB_BILU_SMALL_QUAD") && getenv("FB_BILU_SMALL_QUAD")[0] == '0');
+  const bool pipe = g_bilu_pipe >= 1 && !(small_quad && B->max_block <= 160 && lanes >= 4);
   switch (lanes) {
     case 2: return pipe ? launch_block_ilu<2, true>(B, a, b, r, out, st) : launch_block_ilu<2, false>(B, a, b, r, out, st);
     case 4: return pipe ? launch_block_ilu<4, true>(B, a, b, r, out, st) : launch_block_ilu<4, false>(B, a, b, r, out, st);
@@ -1535,7 +1572,7 @@ extern "C" int fb_blockilu_create_csr(const fb_csr* A, int64_t nblocks,
     FB_REQUIRE(block_ptr_host[b + 1] >= block_ptr_host[b], "block_ptr must be non-decreasing");
     B->max_block = std::max<int64_t>(B->max_block, block_ptr_host[b + 1] - block_ptr_host[b]);
   }
-  FB_REQUIRE(block_ilu_smem(B->max_block) * (32 / block_ilu_lanes(B->max_block)) <= 200 * 1024 &&
+  FB_REQUIRE(block_ilu_smem_max(B->max_block) <= 200 * 1024 &&
                  B->max_block <= 65535,
              "block too large for shared memory");
   cudaStream_t st = 0;
