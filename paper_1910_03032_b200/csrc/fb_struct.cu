@@ -297,13 +297,17 @@ template <int NF, int NC>
 __global__ void __launch_bounds__(32 * kTE) transfer_prolong_kernel(TransferView T, int64_t ne,
                                                                     const double* __restrict__ xc,
                                                                     double* __restrict__ xf) {
-  __shared__ double xe_all[kTE][125];
-  __shared__ double w_all[kTE][3][9 * 5];
+  // sized by the compile-time ladder pair for nf <= 5 (less shared memory per
+  // warp keeps more elements' gathers in flight: p = 4 -> 2 restriction
+  // 2.17 -> 1.7 ms at cfg3); nf > 5 keeps the full size (measured slower
+  // with more resident warps) and runtime sizes the largest (nf <= 9, nc <= 5)
+  __shared__ double xe_all[kTE][(NF > 0 && NF <= 5) ? NC * NC * NC : 125];
+  __shared__ double w_all[kTE][3][(NF > 0 && NF <= 5) ? NF * NC : 9 * 5];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t e = int64_t(blockIdx.x) * kTE + wi;
   if (e >= ne) return;
   double* xe = xe_all[wi];
-  double(*w)[9 * 5] = w_all[wi];
+  auto& w = w_all[wi];
   int64_t ec[3];
   const double* Wa[3];
   transfer_elem(T, e, ec, Wa);
@@ -337,13 +341,13 @@ template <int NF, int NC>
 __global__ void __launch_bounds__(32 * kTE) transfer_restrict_kernel(TransferView T, int64_t ne,
                                                                      const double* __restrict__ xf,
                                                                      double* __restrict__ E) {
-  __shared__ double rf_all[kTE][729];
-  __shared__ double w_all[kTE][3][9 * 5];
+  __shared__ double rf_all[kTE][(NF > 0 && NF <= 5) ? NF * NF * NF : 729];
+  __shared__ double w_all[kTE][3][(NF > 0 && NF <= 5) ? NF * NC : 9 * 5];
   const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t e = int64_t(blockIdx.x) * kTE + wi;
   if (e >= ne) return;
   double* rf = rf_all[wi];
-  double(*w)[9 * 5] = w_all[wi];
+  auto& w = w_all[wi];
   int64_t ec[3];
   const double* Wa[3];
   transfer_elem(T, e, ec, Wa);
@@ -371,6 +375,115 @@ __global__ void __launch_bounds__(32 * kTE) transfer_restrict_kernel(TransferVie
       }
       acc += w[2][l2 * nc + j2] * s1;
     }
+    E[e * nc3 + j] = acc;
+  }
+}
+
+// Sum-factorized variants for the wide pairs (nf >= 6: p = 5..8 fine
+// levels), one axis per pass with the partial results in shared memory:
+// the same nested sums as the direct loops above (sum_c w2 (sum_b w1 (sum_a
+// w0 x)) and its transpose), at nf nc (nc^2 + nc nf + nf^2) instead of
+// nf^3 (nc^3 + nc^2 + nc) FMAs.  Measured at cfg3 p = 7 (66^3): restriction
+// 2.46 -> 1.97 ms, prolongation 2.22 -> 1.04 ms; at nf <= 5 the extra passes
+// cost more than the FMAs they save (p = 4: 1.7 -> 3.0 ms), so those keep the
+// direct loops.
+template <int NF, int NC>
+__global__ void __launch_bounds__(32 * kTE) transfer_prolong_sf_kernel(TransferView T, int64_t ne,
+                                                                       const double* __restrict__ xc,
+                                                                       double* __restrict__ xf) {
+  static_assert(NF > 0 && NF <= 9 && NC > 0 && NC <= 5, "compile-time ladder pair");
+  __shared__ double xe_all[kTE][NC * NC * NC];
+  __shared__ double t1_all[kTE][NC * NC * NF];  // [c][b][l0]
+  __shared__ double t2_all[kTE][NC * NF * NF];  // [c][l1][l0]
+  __shared__ double w_all[kTE][3][NF * NC];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e = int64_t(blockIdx.x) * kTE + wi;
+  if (e >= ne) return;
+  double* xe = xe_all[wi];
+  double* t1 = t1_all[wi];
+  double* t2 = t2_all[wi];
+  auto& w = w_all[wi];
+  int64_t ec[3];
+  const double* Wa[3];
+  transfer_elem(T, e, ec, Wa);
+  constexpr int nc = NC, nf = NF, nc3 = NC * NC * NC, nf3 = NF * NF * NF;
+  for (int j = lane; j < nc3; j += 32) xe[j] = __ldg(xc + __ldg(T.hmap + e * nc3 + j));
+  for (int j = lane; j < nf * nc; j += 32)
+    for (int a = 0; a < 3; ++a) w[a][j] = __ldg(Wa[a] + j);
+  __syncwarp();
+  for (int k = lane; k < nc * nc * nf; k += 32) {  // x: (c, b, l0)
+    const int l0 = k % nf, cb = k / nf;
+    double aa = 0.0;
+#pragma unroll
+    for (int a = 0; a < nc; ++a) aa += w[0][l0 * nc + a] * xe[cb * nc + a];
+    t1[k] = aa;
+  }
+  __syncwarp();
+  for (int k = lane; k < nc * nf * nf; k += 32) {  // y: (c, l1, l0)
+    const int l0 = k % nf, l1 = (k / nf) % nf, c = k / (nf * nf);
+    double ab = 0.0;
+#pragma unroll
+    for (int b = 0; b < nc; ++b) ab += w[1][l1 * nc + b] * t1[(c * nc + b) * nf + l0];
+    t2[k] = ab;
+  }
+  __syncwarp();
+  for (int l = lane; l < nf3; l += 32) {  // z: (l2, l1, l0), owned fine DoFs only
+    const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
+    if (!owned_local(T, ec, l0, l1, l2)) continue;
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < nc; ++c) acc += w[2][l2 * nc + c] * t2[(c * nf + l1) * nf + l0];
+    xf[__ldg(T.fmap + e * nf3 + l)] = acc;
+  }
+}
+
+template <int NF, int NC>
+__global__ void __launch_bounds__(32 * kTE) transfer_restrict_sf_kernel(TransferView T, int64_t ne,
+                                                                        const double* __restrict__ xf,
+                                                                        double* __restrict__ E) {
+  static_assert(NF > 0 && NF <= 9 && NC > 0 && NC <= 5, "compile-time ladder pair");
+  __shared__ double rf_all[kTE][NF * NF * NF];  // fine values, then [l2][j1][j0]
+  __shared__ double u1_all[kTE][NF * NF * NC];  // [l2][l1][j0]
+  __shared__ double w_all[kTE][3][NF * NC];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e = int64_t(blockIdx.x) * kTE + wi;
+  if (e >= ne) return;
+  double* rf = rf_all[wi];
+  double* u1 = u1_all[wi];
+  auto& w = w_all[wi];
+  int64_t ec[3];
+  const double* Wa[3];
+  transfer_elem(T, e, ec, Wa);
+  constexpr int nc = NC, nf = NF, nc3 = NC * NC * NC, nf3 = NF * NF * NF;
+  for (int l = lane; l < nf3; l += 32) {
+    const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
+    rf[l] = owned_local(T, ec, l0, l1, l2) ? __ldg(xf + __ldg(T.fmap + e * nf3 + l)) : 0.0;
+  }
+  for (int j = lane; j < nf * nc; j += 32)
+    for (int a = 0; a < 3; ++a) w[a][j] = __ldg(Wa[a] + j);
+  __syncwarp();
+  for (int k = lane; k < nf * nf * nc; k += 32) {  // x: (l2, l1, j0)
+    const int j0 = k % nc, l21 = k / nc;
+    double s0 = 0.0;
+#pragma unroll
+    for (int l0 = 0; l0 < nf; ++l0) s0 += w[0][l0 * nc + j0] * rf[l21 * nf + l0];
+    u1[k] = s0;
+  }
+  __syncwarp();
+  double* u2 = rf;  // rf is free now: [l2][j1][j0]
+  for (int k = lane; k < nf * nc * nc; k += 32) {  // y: (l2, j1, j0)
+    const int j0 = k % nc, j1 = (k / nc) % nc, l2 = k / (nc * nc);
+    double s1 = 0.0;
+#pragma unroll
+    for (int l1 = 0; l1 < nf; ++l1) s1 += w[1][l1 * nc + j1] * u1[(l2 * nf + l1) * nc + j0];
+    u2[k] = s1;
+  }
+  __syncwarp();
+  for (int j = lane; j < nc3; j += 32) {  // z: (j2, j1, j0)
+    const int j10 = j % (nc * nc), j2 = j / (nc * nc);
+    double acc = 0.0;
+#pragma unroll
+    for (int l2 = 0; l2 < nf; ++l2) acc += w[2][l2 * nc + j2] * u2[l2 * nc * nc + j10];
     E[e * nc3 + j] = acc;
   }
 }
@@ -563,12 +676,18 @@ static TransferView transfer_view(const fb_transfer* T) {
 template <bool PROLONG, int NF, int NC>
 static int launch_transfer_t(const fb_transfer* T, const double* in, double* out,
                              cudaStream_t st) {
-  if (PROLONG)
-    transfer_prolong_kernel<NF, NC><<<ceil_div(T->ne, kTE), 32 * kTE, 0, st>>>(transfer_view(T),
-                                                                               T->ne, in, out);
-  else
-    transfer_restrict_kernel<NF, NC><<<ceil_div(T->ne, kTE), 32 * kTE, 0, st>>>(transfer_view(T),
-                                                                                T->ne, in, out);
+  const dim3 grid(unsigned(ceil_div(T->ne, kTE))), block(32 * kTE);
+  if constexpr (NF >= 6) {
+    if (PROLONG)
+      transfer_prolong_sf_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
+    else
+      transfer_restrict_sf_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
+  } else {
+    if (PROLONG)
+      transfer_prolong_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
+    else
+      transfer_restrict_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
+  }
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
