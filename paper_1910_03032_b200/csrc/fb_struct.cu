@@ -488,6 +488,82 @@ __global__ void __launch_bounds__(32 * kTE) transfer_restrict_sf_kernel(Transfer
   }
 }
 
+// Q1 -> Q1 (the h-coarsened levels, nf = nc = 2): one thread per fine
+// element (a warp per element left 24 of 32 lanes idle and one element's
+// gather latency per warp), same nested sums as transfer_*_kernel.
+template <bool PROLONG>
+__global__ void __launch_bounds__(256) transfer_q1_kernel(TransferView T, int64_t ne,
+                                                          const double* __restrict__ in,
+                                                          double* __restrict__ out) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  int64_t ec[3];
+  const double* Wa[3];
+  transfer_elem(T, e, ec, Wa);
+  double w[3][4];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[a][j] = __ldg(Wa[a] + j);
+  const int4* fm = reinterpret_cast<const int4*>(T.fmap + e * 8);
+  const int4 f0 = __ldg(fm), f1 = __ldg(fm + 1);
+  const int fmap[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+  if constexpr (PROLONG) {
+    const int4* hm = reinterpret_cast<const int4*>(T.hmap + e * 8);
+    const int4 h0 = __ldg(hm), h1 = __ldg(hm + 1);
+    const int hmap[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+    double xe[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xe[j] = __ldg(in + hmap[j]);
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      const int l0 = l & 1, l1 = (l >> 1) & 1, l2 = l >> 2;
+      if (!owned_local(T, ec, l0, l1, l2)) continue;
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        double ab = 0.0;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          double aa = 0.0;
+#pragma unroll
+          for (int a = 0; a < 2; ++a) aa += w[0][l0 * 2 + a] * xe[(c * 2 + b) * 2 + a];
+          ab += w[1][l1 * 2 + b] * aa;
+        }
+        acc += w[2][l2 * 2 + c] * ab;
+      }
+      out[fmap[l]] = acc;
+    }
+  } else {
+    double rf[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+      rf[l] = owned_local(T, ec, l & 1, (l >> 1) & 1, l >> 2) ? __ldg(in + fmap[l]) : 0.0;
+    double E[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int j0 = j & 1, j1 = (j >> 1) & 1, j2 = j >> 2;
+      double acc = 0.0;
+#pragma unroll
+      for (int l2 = 0; l2 < 2; ++l2) {
+        double s1 = 0.0;
+#pragma unroll
+        for (int l1 = 0; l1 < 2; ++l1) {
+          double s0 = 0.0;
+#pragma unroll
+          for (int l0 = 0; l0 < 2; ++l0) s0 += w[0][l0 * 2 + j0] * rf[(l2 * 2 + l1) * 2 + l0];
+          s1 += w[1][l1 * 2 + j1] * s0;
+        }
+        acc += w[2][l2 * 2 + j2] * s1;
+      }
+      E[j] = acc;
+    }
+    double2* o = reinterpret_cast<double2*>(out + e * 8);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = make_double2(E[2 * j], E[2 * j + 1]);
+  }
+}
+
 }  // namespace fb
 
 using namespace fb;
@@ -677,7 +753,10 @@ template <bool PROLONG, int NF, int NC>
 static int launch_transfer_t(const fb_transfer* T, const double* in, double* out,
                              cudaStream_t st) {
   const dim3 grid(unsigned(ceil_div(T->ne, kTE))), block(32 * kTE);
-  if constexpr (NF >= 6) {
+  if constexpr (NF == 2 && NC == 2) {
+    transfer_q1_kernel<PROLONG><<<unsigned(ceil_div(T->ne, 256)), 256, 0, st>>>(transfer_view(T),
+                                                                               T->ne, in, out);
+  } else if constexpr (NF >= 6) {
     if (PROLONG)
       transfer_prolong_sf_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
     else
