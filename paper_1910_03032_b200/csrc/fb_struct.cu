@@ -379,14 +379,16 @@ __global__ void __launch_bounds__(32 * kTE) transfer_restrict_kernel(TransferVie
   }
 }
 
-// Sum-factorized variants for the wide pairs (nf >= 6: p = 5..8 fine
-// levels), one axis per pass with the partial results in shared memory:
-// the same nested sums as the direct loops above (sum_c w2 (sum_b w1 (sum_a
-// w0 x)) and its transpose), at nf nc (nc^2 + nc nf + nf^2) instead of
-// nf^3 (nc^3 + nc^2 + nc) FMAs.  Measured at cfg3 p = 7 (66^3): restriction
-// 2.46 -> 1.97 ms, prolongation 2.22 -> 1.04 ms; at nf <= 5 the extra passes
-// cost more than the FMAs they save (p = 4: 1.7 -> 3.0 ms), so those keep the
-// direct loops.
+// Sum-factorized variants for the wide pairs (nf >= 4: p = 3..8 fine
+// levels), one axis per pass with the partial results in shared memory
+// sized exactly for the pair: the same nested sums as the direct loops
+// above (sum_c w2 (sum_b w1 (sum_a w0 x)) and its transpose), at
+// nf nc (nc^2 + nc nf + nf^2) instead of nf^3 (nc^3 + nc^2 + nc) FMAs.
+// Measured per cfg3 V-cycle: p = 7 (66^3) restriction 2.46 -> 1.52 ms,
+// prolongation 2.22 -> 0.84 ms; p = 4 (116^3) 1.71 -> 1.25 and 1.41 -> 1.15 ms.
+// nf = 2, 3 run one thread per element (transfer_q1_kernel,
+// transfer_thread_kernel); the warp-per-element direct loops remain for
+// runtime sizes.
 template <int NF, int NC>
 __global__ void __launch_bounds__(32 * kTE) transfer_prolong_sf_kernel(TransferView T, int64_t ne,
                                                                        const double* __restrict__ xc,
@@ -561,6 +563,74 @@ __global__ void __launch_bounds__(256) transfer_q1_kernel(TransferView T, int64_
     double2* o = reinterpret_cast<double2*>(out + e * 8);
 #pragma unroll
     for (int j = 0; j < 4; ++j) o[j] = make_double2(E[2 * j], E[2 * j + 1]);
+  }
+}
+
+// Narrow pairs with nf = 3 (p = 2 -> 1): one thread per fine element as for
+// Q1, same nested sums.
+template <bool PROLONG, int NF, int NC>
+__global__ void __launch_bounds__(256) transfer_thread_kernel(TransferView T, int64_t ne,
+                                                              const double* __restrict__ in,
+                                                              double* __restrict__ out) {
+  constexpr int nf3 = NF * NF * NF, nc3 = NC * NC * NC;
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  int64_t ec[3];
+  const double* Wa[3];
+  transfer_elem(T, e, ec, Wa);
+  double w[3][NF * NC];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < NF * NC; ++j) w[a][j] = __ldg(Wa[a] + j);
+  if constexpr (PROLONG) {
+    double xe[nc3];
+#pragma unroll
+    for (int j = 0; j < nc3; ++j) xe[j] = __ldg(in + __ldg(T.hmap + e * nc3 + j));
+#pragma unroll
+    for (int l = 0; l < nf3; ++l) {
+      const int l0 = l % NF, l1 = (l / NF) % NF, l2 = l / (NF * NF);
+      if (!owned_local(T, ec, l0, l1, l2)) continue;
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double ab = 0.0;
+#pragma unroll
+        for (int b = 0; b < NC; ++b) {
+          double aa = 0.0;
+#pragma unroll
+          for (int a = 0; a < NC; ++a) aa += w[0][l0 * NC + a] * xe[(c * NC + b) * NC + a];
+          ab += w[1][l1 * NC + b] * aa;
+        }
+        acc += w[2][l2 * NC + c] * ab;
+      }
+      out[__ldg(T.fmap + e * nf3 + l)] = acc;
+    }
+  } else {
+    double rf[nf3];
+#pragma unroll
+    for (int l = 0; l < nf3; ++l) {
+      const int l0 = l % NF, l1 = (l / NF) % NF, l2 = l / (NF * NF);
+      rf[l] = owned_local(T, ec, l0, l1, l2) ? __ldg(in + __ldg(T.fmap + e * nf3 + l)) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < nc3; ++j) {
+      const int j0 = j % NC, j1 = (j / NC) % NC, j2 = j / (NC * NC);
+      double acc = 0.0;
+#pragma unroll
+      for (int l2 = 0; l2 < NF; ++l2) {
+        double s1 = 0.0;
+#pragma unroll
+        for (int l1 = 0; l1 < NF; ++l1) {
+          double s0 = 0.0;
+#pragma unroll
+          for (int l0 = 0; l0 < NF; ++l0) s0 += w[0][l0 * NC + j0] * rf[(l2 * NF + l1) * NF + l0];
+          s1 += w[1][l1 * NC + j1] * s0;
+        }
+        acc += w[2][l2 * NC + j2] * s1;
+      }
+      out[e * nc3 + j] = acc;
+    }
   }
 }
 
@@ -756,7 +826,10 @@ static int launch_transfer_t(const fb_transfer* T, const double* in, double* out
   if constexpr (NF == 2 && NC == 2) {
     transfer_q1_kernel<PROLONG><<<unsigned(ceil_div(T->ne, 256)), 256, 0, st>>>(transfer_view(T),
                                                                                T->ne, in, out);
-  } else if constexpr (NF >= 6) {
+  } else if constexpr (NF == 3) {
+    transfer_thread_kernel<PROLONG, NF, NC><<<unsigned(ceil_div(T->ne, 256)), 256, 0, st>>>(
+        transfer_view(T), T->ne, in, out);
+  } else if constexpr (NF >= 4) {
     if (PROLONG)
       transfer_prolong_sf_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
     else
