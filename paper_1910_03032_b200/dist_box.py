@@ -429,13 +429,46 @@ class DistTransfer(S.BoxTransfer):
         _lib.check(_lib.lib.fb_transfer_set_origin(h, 0, 0, fine.e0))
 
 
+class DistHTransfer(S.BoxTransfer):
+    """h-transfer from a rank's Q1 slab to the whole (agglomerated) coarsened
+    Q1 box: the slab's fine elements with their parents' global coarse DoFs.
+    Restriction gives this slab's partial coarse vector (summed over ranks by
+    the caller); prolongation writes the slab's owned fine DoFs."""
+
+    def __init__(self, fine, coarse):
+        self.fine_r = mfop.restriction(fine)
+        nx, ny, nz = fine.counts
+        W, ix, px = S.h_transfer_tables(nx)
+        _, iy, py = S.h_transfer_tables(ny)
+        _, iz, pz = S.h_transfer_tables(nz)
+        iz, pz = iz[fine.e0:fine.e1], pz[fine.e0:fine.e1]
+        widx = np.concatenate([ix, iy, iz])
+        mx, my, _ = coarse.counts
+        pe = (px[None, None, :] + mx * (py[None, :, None] + my * pz[:, None, None])).ravel()
+        self._hspace = S._Map(3, 1, coarse.element_dofs[pe], coarse.ndofs_scalar)
+        self.hmap_r = mfop.Restriction(self._hspace)
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        counts = np.asarray([nx, ny, fine.e1 - fine.e0], dtype=np.int64)
+        h = C.c_void_p()
+        _lib.check(_lib.lib.fb_transfer_create(self.fine_r.handle, self.hmap_r.handle,
+                                               _lib.ptr(counts), W.shape[0], _lib.ptr(W),
+                                               _lib.ptr(widx), C.byref(h)))
+        self.handle = h
+        _lib.check(_lib.lib.fb_transfer_set_origin(h, 0, 0, fine.e0))
+
+
 class DistLORPreconditioner:
     """Sharded scale-mode V(1,1) cycle (same recursion as
     solvers.LORPreconditioner._cycle, solvers.py:375-392), levels p >= 2 on
-    the slabs, the Q1 problem agglomerated and solved redundantly."""
+    the slabs.  Q1 level: when the single-GPU hierarchy coarsens it
+    geometrically (more than max_coarse rows), the Q1 level itself is sharded
+    too -- its `coarse_cycles` stationary cycles run on the slabs, and only
+    the h-coarsened levels (1/8 of the Q1 rows and below) are agglomerated
+    (one all-reduce of the restricted residual per cycle) and solved
+    redundantly; otherwise the whole Q1 problem is agglomerated."""
 
     def __init__(self, mesh, p, kind, comm, layers, nu=1.0, c=0.0, block=2, q1_block=4,
-                 max_coarse=20000, levels=None):
+                 max_coarse=20000, levels=None, distribute_q1=True, coarse_cycles=None):
         self.comm = comm
         r, w = comm.rank, comm.world
         ddev = dev.device()
@@ -446,10 +479,28 @@ class DistLORPreconditioner:
         self.smoothers = [S.DeviceBlockILU0(A, lv.block_ptr) for A, lv in zip(self._A, self.levels)]
         chain = self.levels + [self.q1]
         self.transfers = [DistTransfer(chain[i], chain[i + 1]) for i in range(len(self.levels))]
-        # agglomerated Q1 problem: the whole Q1 V-cycle on every rank
-        q1space = S.BoxSpace(mesh, 1, block=q1_block, device=ddev)
-        self.coarse = S.BoxLORPreconditioner(q1space, kind, nu=nu, c=c, q1_block=q1_block,
-                                             max_coarse=max_coarse)
+        q1_rows = int(np.prod([a + 1 for a in mesh.counts]))
+        self.q1_sharded = bool(distribute_q1 and q1_rows > max_coarse
+                               and min(mesh.counts) >= 2)
+        if self.q1_sharded:
+            # sharded Q1 level; h-coarsened hierarchy agglomerated (one V-cycle each)
+            self.coarse_cycles = int(coarse_cycles if coarse_cycles is not None
+                                     else S.DEFAULT_COARSE_CYCLES)
+            self._Aq = DistLevelMatrix(self.q1, kind, nu, c, True)
+            self.smq = S.DeviceBlockILU0(self._Aq, self.q1.block_ptr)
+            hspace = S.BoxSpace(S.coarsen_box(mesh), 1, block=q1_block, device=ddev)
+            self.hT = DistHTransfer(self.q1, hspace)
+            self.coarse = S.BoxLORPreconditioner(hspace, kind, nu=nu, c=c, q1_block=q1_block,
+                                                 max_coarse=max_coarse, coarse_cycles=1)
+            nh = hspace.ndofs_scalar
+            self._rh, self._xh = dev.zeros(nh), dev.zeros(nh)
+            nq = self.q1.n_local
+            self._rk, self._dk = dev.zeros(nq), dev.zeros(nq)
+        else:
+            # agglomerated Q1 problem: the whole Q1 V-cycle on every rank
+            q1space = S.BoxSpace(mesh, 1, block=q1_block, device=ddev)
+            self.coarse = S.BoxLORPreconditioner(q1space, kind, nu=nu, c=c, q1_block=q1_block,
+                                                 max_coarse=max_coarse)
         sizes = torch.tensor([self.q1.n_own], dtype=torch.float64, device=ddev)
         allsz = comm.allgather(sizes, [1] * w)
         self.q1_sizes = [int(v) for v in allsz.tolist()]
@@ -460,10 +511,42 @@ class DistLORPreconditioner:
         self._t2 = [dev.zeros(lv.n_local) for lv in chain]
         self._q1_ghost_ids = None
 
+    def _q1_vcycle(self, r, x):
+        """One V-cycle from the sharded Q1 level: slab block-ILU smoothing and
+        residuals, restriction to the agglomerated h-coarse box (partial
+        vectors summed over ranks), its V-cycle on every rank, prolongation
+        back to the owned fine DoFs (structured.BoxLORPreconditioner._cycle
+        at the Q1 level, solvers.py:375-392)."""
+        q1, A, sm = self.q1, self._Aq, self.smq
+        n = q1.n_own
+        t, t2 = self._t[-1], self._t2[-1]
+        sm.forward_into(r, x)
+        q1.ghost_update(self.comm, x)
+        A.residual_into(r, x, t)
+        self.hT.restrict_into(t, self._rh)
+        self.comm.allreduce_sum(self._rh)
+        self.coarse.apply_into(self._rh, self._xh)
+        self.hT.prolong_into(self._xh, t)
+        vec.axpby(1.0, t[:n], 1.0, x[:n])
+        q1.ghost_update(self.comm, x)
+        A.residual_into(r, x, t)
+        sm.backward_into(t, t2)
+        vec.axpby(1.0, t2[:n], 1.0, x[:n])
+
     def _coarse_solve(self, rq, xq):
         """rq: Q1 slab vector with owned residual; xq <- owned correction +
         bottom ghost plane (what the prolongation reads)."""
         q1 = self.q1
+        if self.q1_sharded:
+            # coarse_cycles stationary cycles: x = V r; x += V (r - A x)
+            self._q1_vcycle(rq, xq)
+            for _ in range(self.coarse_cycles - 1):
+                q1.ghost_update(self.comm, xq)
+                self._Aq.residual_into(rq, xq, self._rk)
+                self._q1_vcycle(self._rk, self._dk)
+                vec.axpby(1.0, self._dk[:q1.n_own], 1.0, xq[:q1.n_own])
+            q1.ghost_update(self.comm, xq, top1=False)
+            return
         rg = self.comm.allgather(rq[:q1.n_own], self.q1_sizes)
         xg = torch.empty_like(rg)
         self.coarse.apply_into(rg, xg)
@@ -518,7 +601,8 @@ def dist_cg(A, b, M, comm, n_own, config=None):
 
 
 def helmholtz_slab_problem(comm, counts, p, c=10.0, nu=1.0, perturb=0.05, seed=1, block=2,
-                           q1_block=4, max_coarse=20000, rhs_seed=0, mesh=None):
+                           q1_block=4, max_coarse=20000, rhs_seed=0, mesh=None,
+                           distribute_q1=True):
     """One rank's share of the cfg3 problem: slab operator (constrained),
     sharded LOR V-cycle, owned part of the global random right-hand side."""
     r, w = comm.rank, comm.world
@@ -534,7 +618,8 @@ def helmholtz_slab_problem(comm, counts, p, c=10.0, nu=1.0, perturb=0.05, seed=1
     bdr = lv.boundary_local()
     A = mfop.ConstrainedOperator(DistOperator(op_local, lv, comm), bdr)
     M = DistLORPreconditioner(mesh, p, "helmholtz", comm, layers, nu=nu, c=c, block=block,
-                              q1_block=q1_block, max_coarse=max_coarse, levels=levels)
+                              q1_block=q1_block, max_coarse=max_coarse, levels=levels,
+                              distribute_q1=distribute_q1)
     # global right-hand side, generated identically everywhere; owned slice kept
     N = int(np.prod([counts[a] * p + 1 for a in range(3)]))
     g = torch.Generator(device=ddev)

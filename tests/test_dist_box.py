@@ -109,8 +109,12 @@ def test_torch_comm_over_gloo_matches_thread_comm(world):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,counts,p", [(2, (3, 4, 8), 4), (3, (4, 3, 12), 2), (2, (2, 3, 8), 7)])
-def test_sharded_lor_pcg_matches_single_gpu(world, counts, p):
+@pytest.mark.parametrize("world,counts,p,dq1", [(2, (3, 4, 8), 4, True), (3, (4, 3, 12), 2, True),
+                                               (2, (2, 3, 8), 7, True), (2, (3, 4, 8), 4, False),
+                                               (3, (4, 4, 12), 3, True)])
+def test_sharded_lor_pcg_matches_single_gpu(world, counts, p, dq1):
+    """cfg3 on N ranks: the Q1 level is sharded too (dq1: its stationary
+    cycles on the slabs, the h-coarse box agglomerated) or agglomerated whole."""
     import torch
     from paper_1910_03032_b200 import dist_box as D, solvers, structured as S
     cfg = solvers.SolverConfig(rel_tol=1e-8, max_iters=300)
@@ -121,7 +125,9 @@ def test_sharded_lor_pcg_matches_single_gpu(world, counts, p):
     y_ref = ref["A"].apply(ref["b"]).cpu().numpy()
 
     def fn(comm):
-        pr = D.helmholtz_slab_problem(comm, counts, p, c=10.0, max_coarse=100, mesh=mesh)
+        pr = D.helmholtz_slab_problem(comm, counts, p, c=10.0, max_coarse=100, mesh=mesh,
+                                      distribute_q1=dq1)
+        assert pr["M"].q1_sharded == dq1
         lv = pr["level"]
         y = torch.empty_like(pr["b"])
         pr["A"].apply_into(pr["b"], y)
