@@ -1,4 +1,8 @@
-"""Element kernel: full vs arithmetic only (no factor / x / y traffic, skip bit 15) vs memory only (all passes skipped)."""
+"""Element kernel: full vs arithmetic only vs memory only (all passes skipped).
+The arithmetic-only leg needs the diagnostic build: `git apply
+tools/micro/nomem.patch` (skip bit 15 drops the factor / x / y traffic; it
+changes code generation, so never keep it in the product build), rebuild,
+run, `git apply -R`.  Without the patch the arith_only column equals full."""
 import json
 import sys
 
