@@ -969,9 +969,9 @@ static int build_ell(fb_blockilu* B) {
 // 89-131 levels per block.  Here each level of each block is ONE contiguous
 // chunk (TriPart::pk), and one lane streams chunks NSLOT levels ahead into a
 // shared-memory ring with cp.async.bulk (TMA) + an mbarrier per slot, so the
-// lanes computing level g read everything from shared memory.  Every row's
-// sum is the same sequential, separately rounded multiply-add chain as
-// row_finish (bitwise the CSR sweep).
+// lanes computing level g read everything from shared memory.  Each row is
+// split over 1-4 lanes (packed_rows): deterministic, equal to the CSR sweep
+// to rounding (not bitwise its sequential chain).
 namespace {
 
 struct PackView {
