@@ -190,7 +190,8 @@ def cpu_time(problems, reps=1):
 def run_reference(args, rank, world):
     """Reference arm: the UNMODIFIED reference (oracle/_ref, built from
     /root/reference by oracle/build_ref.py) timed through its own public API
-    in a single-threaded subprocess (oracle/ref_bench.py): stock
+    in a subprocess allowed every host thread (oracle/ref_bench.py; the
+    reference's numba kernels are serial, so it uses one): stock
     HelmholtzOperator.apply, FLOWBENCH_BACKEND=numba, on a bounded sample of
     the workload.  Never imports the product package."""
     if rank != 0:
@@ -198,7 +199,8 @@ def run_reference(args, rank, world):
     from oracle import ref_bench
     if ref_bench.available():
         res = ref_bench.run_subprocess(["apply", "--target", str(CPU_SAMPLE_DOFS),
-                                        "--steps", str(args.steps), "--warmup", str(args.warmup)])
+                                        "--steps", str(args.steps), "--warmup", str(args.warmup)],
+                                       threads=os.cpu_count() or 1)
         value, el, cores, kind, desc = (res["value"], res["seconds"], res["cores"], res["kind"],
                                         res["sample"])
         extra = {"per_p": res["per_p"], "host_cpus": res["host_cpus"], "setup_s": res["setup_s"]}

@@ -16,7 +16,8 @@ path:
 
 The backend is `FLOWBENCH_BACKEND=numba` (the reference default; its kernels
 are serial `@njit`) and the process is pinned to one thread for
-numba / OpenMP / OpenBLAS, so `cores` = 1.  This module never imports the
+numba / OpenMP / OpenBLAS, so `cores` = 1, except for the `--impl reference`
+arm, which allows all host threads (`--threads`).  This module never imports the
 product package; run it as a subprocess:
 
     python -m oracle.ref_bench apply --target 120000 --steps 3 --warmup 1
@@ -76,7 +77,7 @@ def apply_problems(target, degrees, c=10.0, nu=1.0):
     return probs
 
 
-def apply_sweep(target=120_000, degrees=range(1, 9), steps=3, warmup=1):
+def apply_sweep(target=120_000, degrees=range(1, 9), steps=3, warmup=1, threads=1):
     """One step = one reference Helmholtz apply per degree.  Returns the
     sweep GDoF/s (total DoFs / total seconds) and per-degree figures."""
     t0 = time.perf_counter()
@@ -95,15 +96,16 @@ def apply_sweep(target=120_000, degrees=range(1, 9), steps=3, warmup=1):
     tot_s = sum(per.values())
     return {
         "value": tot_dofs / tot_s / 1e9, "unit": "GDoF/s", "seconds": tot_s, "steps": steps,
-        "warmup": warmup, "setup_s": round(setup, 2), "cores": 1, "kind": "reference",
+        "warmup": warmup, "setup_s": round(setup, 2), "cores": threads, "kind": "reference",
         "per_p": {str(pr["p"]): {"dofs": pr["dofs"], "cells": pr["n"],
                                  "ms_per_apply": round(1e3 * per[pr["p"]] / steps, 3),
                                  "mdofs": round(pr["dofs"] * steps / per[pr["p"]] / 1e6, 4)}
                   for pr in probs},
         "sample": (f"reference flowbench 0.1.0 (oracle/_ref) HelmholtzOperator(c=10, nu=1).apply, "
                    f"p=1..8, ~{target / 1e3:.0f}k DoFs per degree (n^3 perturbed cube), "
-                   f"FLOWBENCH_BACKEND=numba, 1 thread; {steps} timed sweep(s) after {warmup} "
-                   f"warm-up"),
+                   f"FLOWBENCH_BACKEND=numba, {threads} host thread(s) allowed to numba / OpenMP / "
+                   f"BLAS (the reference's @njit kernels are serial); {steps} timed sweep(s) "
+                   f"after {warmup} warm-up"),
     }
 
 
@@ -139,11 +141,20 @@ def lor_pcg(names=("cfg1", "p4_16", "p7_8")):
     return out
 
 
-def run_subprocess(args, timeout=1800):
-    """Run this module in a fresh single-threaded interpreter; parsed JSON."""
+def thread_env(threads):
+    env = dict(REF_ENV)
+    for k in ("NUMBA_NUM_THREADS", "OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        env[k] = str(threads)
+    return env
+
+
+def run_subprocess(args, timeout=1800, threads=1):
+    """Run this module in a fresh interpreter with `threads` host threads
+    allowed (1: single-threaded); parsed JSON."""
     import subprocess
     env = dict(os.environ)
-    env.update(REF_ENV)
+    env.update(thread_env(threads))
+    args = list(args) + ["--threads", str(threads)]
     env["PYTHONPATH"] = ROOT
     r = subprocess.run([sys.executable, "-m", "oracle.ref_bench"] + list(args), cwd=ROOT, env=env,
                        stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, timeout=timeout)
@@ -157,7 +168,10 @@ def available():
 
 
 def main():
-    for k, v in REF_ENV.items():  # before numpy / numba load their thread pools
+    th = 1
+    if "--threads" in sys.argv:
+        th = int(sys.argv[sys.argv.index("--threads") + 1])
+    for k, v in thread_env(th).items():  # before numpy / numba load their thread pools
         os.environ[k] = v
     ap = argparse.ArgumentParser()
     ap.add_argument("what", choices=["apply", "pcg"])
@@ -165,9 +179,10 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--cases", default="cfg1,p4_16,p7_8")
+    ap.add_argument("--threads", type=int, default=1)
     a = ap.parse_args()
     if a.what == "apply":
-        res = apply_sweep(a.target, steps=a.steps, warmup=a.warmup)
+        res = apply_sweep(a.target, steps=a.steps, warmup=a.warmup, threads=a.threads)
     else:
         res = lor_pcg(a.cases.split(","))
     res["host_cpus"] = os.cpu_count()
