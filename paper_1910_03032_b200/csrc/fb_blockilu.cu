@@ -981,6 +981,7 @@ struct PackView {
   const int* grp;
   const int* blk_grp;
   int has_inv;
+  int s4, s2;  // rows per level up to which 4 / 2 lanes share a row
 };
 
 __device__ __forceinline__ uint32_t psmem_u32(const void* p) {
@@ -1102,8 +1103,8 @@ __device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, 
       const unsigned short* cnt = rst + R;
       // S lanes per row (levels are narrow: ~6 rows at p = 4), each summing
       // a strided share of the row's entries, combined by a fixed xor tree
-      if (R <= 8) packed_rows<4>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
-      else if (R <= 16) packed_rows<2>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
+      if (R <= T.s4) packed_rows<4>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
+      else if (R <= T.s2) packed_rows<2>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
       else packed_rows<1>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
       __syncwarp();
     }
@@ -1316,8 +1317,12 @@ static int launch_packed(const fb_blockilu* B, const TriPart& a, bool ua, const 
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = smem;
   }
-  const PackView pa{a.pk.ptr, a.loff.ptr, a.lne.ptr, a.grp.ptr, a.blk_grp.ptr, ua ? 0 : 1};
-  const PackView pb{b.pk.ptr, b.loff.ptr, b.lne.ptr, b.grp.ptr, b.blk_grp.ptr, ub ? 0 : 1};
+  // FB_BILU_S4 / FB_BILU_S2: level widths up to which rows are split over 4 / 2
+  // lanes (A/B runs; defaults measured with tools/vcycle_breakdown.py)
+  static const int s4 = getenv("FB_BILU_S4") ? atoi(getenv("FB_BILU_S4")) : 8;
+  static const int s2 = getenv("FB_BILU_S2") ? atoi(getenv("FB_BILU_S2")) : 16;
+  const PackView pa{a.pk.ptr, a.loff.ptr, a.lne.ptr, a.grp.ptr, a.blk_grp.ptr, ua ? 0 : 1, s4, s2};
+  const PackView pb{b.pk.ptr, b.loff.ptr, b.lne.ptr, b.grp.ptr, b.blk_grp.ptr, ub ? 0 : 1, s4, s2};
   block_ilu_packed_kernel<NSLOT><<<B->nblocks, 32, smem, st>>>(
       B->block_ptr.ptr, B->new2old.ptr, pa, pb, r, out, sb, a.lev_group, b.lev_group,
       B->max_block, B->max_grp);
