@@ -1021,7 +1021,7 @@ __host__ __device__ inline size_t packed_smem(int nslot, int max_chunk, int max_
 // Lane `sub` of a row accumulates entries sub, sub + S, ... with fma; the S
 // partial sums are combined by xor shuffles in a fixed order, so the result
 // is deterministic (not bitwise the sequential CSR chain).
-template <int S>
+template <int S, int NW>
 __device__ __forceinline__ void packed_rows(const double* vals, const double* inv,
                                             const unsigned short* cols,
                                             const unsigned short* rows,
@@ -1032,7 +1032,7 @@ __device__ __forceinline__ void packed_rows(const double* vals, const double* in
   constexpr int U = (kRowBuf + S - 1) / S;  // unrolled entries per lane
   const int lane = threadIdx.x;
   const int sub = lane & (S - 1);
-  for (int t0 = 0; t0 < R; t0 += (32 >> LG)) {
+  for (int t0 = 0; t0 < R; t0 += ((32 * NW) >> LG)) {
     const int t = t0 + (lane >> LG);
     const bool live = t < R;
     const int start = live ? rst[t] : 0, n = live ? cnt[t] : 0;
@@ -1062,20 +1062,27 @@ __device__ __forceinline__ void packed_rows(const double* vals, const double* in
 // Levels are staged K at a time (one bulk copy spans K consecutive chunks of
 // the block; NSLOT spans in flight), so the mbarrier wait and the copy issue
 // are paid once per K levels.
-template <int NSLOT>
+// one warp (NW = 1) or NW warps per block (wide levels of large blocks)
+template <int NW>
+__device__ __forceinline__ void pk_sync() {
+  if constexpr (NW == 1) __syncwarp();
+  else __syncthreads();
+}
+
+template <int NSLOT, int NW>
 __device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, uint64_t* bars,
                                            unsigned char* ring, int slot_bytes, int K,
                                            int64_t* soff, int* sR, int* sE, uint32_t& used) {
   const int lane = threadIdx.x;
   const int g0 = T.blk_grp[b], G = T.blk_grp[b + 1] - g0;
   const int NG = (G + K - 1) / K;
-  __syncwarp();
-  for (int i = lane; i <= G; i += 32) soff[i] = T.loff[g0 + i];
-  for (int i = lane; i < G; i += 32) {
+  pk_sync<NW>();
+  for (int i = lane; i <= G; i += 32 * NW) soff[i] = T.loff[g0 + i];
+  for (int i = lane; i < G; i += 32 * NW) {
     sR[i] = T.grp[g0 + i + 1] - T.grp[g0 + i];
     sE[i] = T.lne[g0 + i];
   }
-  __syncwarp();
+  pk_sync<NW>();
   auto issue = [&](int j) {
     const uint32_t slot = (used + uint32_t(j)) % NSLOT;
     const int a = j * K, z = min(a + K, G);
@@ -1103,10 +1110,10 @@ __device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, 
       const unsigned short* cnt = rst + R;
       // S lanes per row (levels are narrow: ~6 rows at p = 4), each summing
       // a strided share of the row's entries, combined by a fixed xor tree
-      if (R <= T.s4) packed_rows<4>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
-      else if (R <= T.s2) packed_rows<2>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
-      else packed_rows<1>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
-      __syncwarp();
+      if (R <= T.s4 * NW) packed_rows<4, NW>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
+      else if (R <= T.s2 * NW) packed_rows<2, NW>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
+      else packed_rows<1, NW>(vals, inv, cols, rows, rst, cnt, R, T.has_inv, y);
+      pk_sync<NW>();
     }
     if (lane == 0 && j + NSLOT < NG) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1116,8 +1123,8 @@ __device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, 
   used += uint32_t(NG);
 }
 
-template <int NSLOT>
-__global__ void __launch_bounds__(32) block_ilu_packed_kernel(
+template <int NSLOT, int NW>
+__global__ void __launch_bounds__(32 * NW) block_ilu_packed_kernel(
     const int* __restrict__ block_ptr, const int* __restrict__ new2old, PackView A, PackView Bv,
     const double* __restrict__ r, double* __restrict__ out, int slot_bytes, int KA, int KB,
     int max_block, int max_grp) {
@@ -1136,12 +1143,12 @@ __global__ void __launch_bounds__(32) block_ilu_packed_kernel(
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(psmem_u32(&bars[i])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = lane; i < nb; i += 32) y[i] = r[new2old ? new2old[bs + i] : bs + i];
+  for (int i = lane; i < nb; i += 32 * NW) y[i] = r[new2old ? new2old[bs + i] : bs + i];
   uint32_t used = 0;
-  packed_tri<NSLOT>(A, b, y, bars, ring, slot_bytes, KA, soff, sR, sE, used);
-  packed_tri<NSLOT>(Bv, b, y, bars, ring, slot_bytes, KB, soff, sR, sE, used);
-  __syncwarp();
-  for (int i = lane; i < nb; i += 32) out[new2old ? new2old[bs + i] : bs + i] = y[i];
+  packed_tri<NSLOT, NW>(A, b, y, bars, ring, slot_bytes, KA, soff, sR, sE, used);
+  packed_tri<NSLOT, NW>(Bv, b, y, bars, ring, slot_bytes, KB, soff, sR, sE, used);
+  pk_sync<NW>();
+  for (int i = lane; i < nb; i += 32 * NW) out[new2old ? new2old[bs + i] : bs + i] = y[i];
 }
 
 __global__ void pack_count_kernel(int64_t nlev, const int* __restrict__ grp,
@@ -1306,14 +1313,14 @@ static int build_packed(fb_blockilu* B) {
   return FB_OK;
 }
 
-template <int NSLOT>
-static int launch_packed(const fb_blockilu* B, const TriPart& a, bool ua, const TriPart& b,
-                         bool ub, const double* r, double* out, cudaStream_t st) {
+template <int NSLOT, int NW>
+static int launch_packed_w(const fb_blockilu* B, const TriPart& a, bool ua, const TriPart& b,
+                           bool ub, const double* r, double* out, cudaStream_t st) {
   const int sb = (std::max(a.max_group, b.max_group) + 15) / 16 * 16;
   const size_t smem = packed_smem(NSLOT, sb, B->max_block, B->max_grp);
   static size_t configured = 0;
   if (smem > configured) {
-    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_packed_kernel<NSLOT>,
+    FB_TRY_CUDA(cudaFuncSetAttribute(block_ilu_packed_kernel<NSLOT, NW>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = smem;
   }
@@ -1323,11 +1330,21 @@ static int launch_packed(const fb_blockilu* B, const TriPart& a, bool ua, const 
   static const int s2 = getenv("FB_BILU_S2") ? atoi(getenv("FB_BILU_S2")) : 16;
   const PackView pa{a.pk.ptr, a.loff.ptr, a.lne.ptr, a.grp.ptr, a.blk_grp.ptr, ua ? 0 : 1, s4, s2};
   const PackView pb{b.pk.ptr, b.loff.ptr, b.lne.ptr, b.grp.ptr, b.blk_grp.ptr, ub ? 0 : 1, s4, s2};
-  block_ilu_packed_kernel<NSLOT><<<B->nblocks, 32, smem, st>>>(
+  block_ilu_packed_kernel<NSLOT, NW><<<B->nblocks, 32 * NW, smem, st>>>(
       B->block_ptr.ptr, B->new2old.ptr, pa, pb, r, out, sb, a.lev_group, b.lev_group,
       B->max_block, B->max_grp);
   FB_CHECK_LAUNCH();
   return FB_OK;
+}
+
+// warps per block: FB_BILU_NW=<1|2> (A/B runs), else by block size
+template <int NSLOT>
+static int launch_packed(const fb_blockilu* B, const TriPart& a, bool ua, const TriPart& b,
+                         bool ub, const double* r, double* out, cudaStream_t st) {
+  static const int nw_env = getenv("FB_BILU_NW") ? atoi(getenv("FB_BILU_NW")) : 0;
+  const int nw = nw_env > 0 ? nw_env : (B->max_block > 1024 ? 2 : 1);
+  if (nw == 2) return launch_packed_w<NSLOT, 2>(B, a, ua, b, ub, r, out, st);
+  return launch_packed_w<NSLOT, 1>(B, a, ua, b, ub, r, out, st);
 }
 
 extern "C" {

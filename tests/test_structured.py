@@ -405,10 +405,11 @@ def test_periodic_box_lor_pcg_vs_reference(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("p,counts", [(3, (28, 28, 26)), (4, (28, 28, 26))])
+@pytest.mark.parametrize("p,counts", [(3, (28, 28, 26)), (4, (28, 28, 26)), (7, (28, 28, 26))])
 def test_packed_block_ilu_sweep_matches_csr_sweep(p, counts):
-    """The level-packed TMA-ring sweep (rows split over lanes, the path of
-    every cfg3-size fine level) against the CSR level sweep of the same
+    """The level-packed TMA-ring sweep (rows split over lanes; two warps per
+    block at p = 7; the path of every cfg3-size fine level) against the CSR
+    level sweep of the same
     factor: forward / backward solves agree to rounding and are deterministic."""
     import torch
     from paper_1910_03032_b200 import _lib, geometry, structured as S
