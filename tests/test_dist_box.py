@@ -244,3 +244,37 @@ def test_ring_projection_stepper_matches_single_gpu(world, counts, p):
             assert all(abs(x - y) <= 1 for x, y in zip(a, b)), (its, ref_its)
         assert rel_err(u, u_ref) < 1e-8
         assert e == pytest.approx(e_ref, rel=1e-10)
+
+
+@pytest.mark.parametrize("world,counts,p", [(2, (4, 4, 8), 3), (3, (4, 6, 12), 2), (3, (3, 4, 12), 4)])
+def test_periodic_ring_layout_host(world, counts, p):
+    """Host logic of the periodic ring (no GPU): owned slices partition the
+    global box numbering in rank order; every rank's element map, pulled back
+    to global ids through [owned | lower ghost | upper ghost], is the global
+    BoxSpace element map of its elements; each ghost plane is exactly what
+    the neighbour around the ring sends."""
+    import torch
+    from paper_1910_03032_b200 import dist_box as D, dist_periodic as DP, geometry, structured as S
+    cpu = torch.device("cpu")
+    m = geometry.cartesian_mesh(counts, lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                                periodic=(True,) * 3)
+    g = S.BoxSpace(m, p, block=2, device=cpu)
+    ged = np.asarray(g.element_dofs)
+    layers = D.slab_layers(counts[2], world, 4)
+    lvs = [DP.PeriodicSlabLevel(m, p, 2, layers, r, world, cpu) for r in range(world)]
+    assert [lv.off for lv in lvs] == list(np.cumsum([0] + [lv.n_own for lv in lvs[:-1]]))
+    assert lvs[-1].off + lvs[-1].n_own == g.ndofs
+    ne_layer = counts[0] * counts[1]
+    for r, lv in enumerate(lvs):
+        l2g = np.concatenate([np.arange(lv.off, lv.off + lv.n_own),
+                              lv.ghost_gids["lower"].numpy(), lv.ghost_gids["upper"].numpy()])
+        assert l2g.shape[0] == lv.n_local
+        led = np.asarray(lv.element_dofs)
+        e0, e1 = layers[r]
+        assert np.array_equal(l2g[led], ged[e0 * ne_layer:e1 * ne_layer])
+        down, up = lvs[(r - 1) % world], lvs[(r + 1) % world]
+        # lower ghost <- the lower neighbour's up-send; upper ghost <- the upper's down-send
+        assert np.array_equal(lv.ghost_gids["lower"].numpy(),
+                              down.off + down.send_up_ids.numpy().astype(np.int64))
+        assert np.array_equal(lv.ghost_gids["upper"].numpy(),
+                              up.off + up.send_down_ids.numpy().astype(np.int64))
