@@ -278,3 +278,42 @@ def test_periodic_ring_layout_host(world, counts, p):
                               down.off + down.send_up_ids.numpy().astype(np.int64))
         assert np.array_equal(lv.ghost_gids["upper"].numpy(),
                               up.off + up.send_down_ids.numpy().astype(np.int64))
+
+
+@pytest.mark.parametrize("world,counts,p", [(2, (3, 4, 8), 4), (3, (4, 3, 12), 2), (3, (2, 3, 12), 3)])
+def test_slab_layout_host(world, counts, p):
+    """Host logic of the cfg3 slabs (no GPU): owned slices partition the
+    block-major numbering; each rank's element map, pulled back to global ids
+    through [owned | bottom ghost | top+1 ghost], is the global map of its
+    elements; the exchanged planes are the neighbours' owned planes."""
+    import torch
+    from paper_1910_03032_b200 import dist_box as D, structured as S
+    cpu = torch.device("cpu")
+    m = S.box_mesh(counts, perturb=0.0)
+    g = S.BoxSpace(m, p, block=2, device=cpu)
+    ged = np.asarray(g.element_dofs)
+    layers = D.slab_layers(counts[2], world, 4)
+    lvs = [D.SlabLevel(m, p, 2, layers, r, world, cpu) for r in range(world)]
+    assert [lv.off for lv in lvs] == list(np.cumsum([0] + [lv.n_own for lv in lvs[:-1]]))
+    ne_layer = counts[0] * counts[1]
+
+    def plane_ids(gz):
+        ids, _ = S.box_lattice_ids(counts, p, 2, cpu, gz_range=(gz, gz + 1))
+        return ids.reshape(-1).numpy()
+
+    for r, lv in enumerate(lvs):
+        parts = [np.arange(lv.off, lv.off + lv.n_own)]
+        if lv.down:
+            parts.append(plane_ids(lv.e0 * p))
+        if lv.up:
+            parts.append(plane_ids(lv.e1 * p + 1))
+        l2g = np.concatenate(parts)
+        assert l2g.shape[0] == lv.n_local
+        e0, e1 = layers[r]
+        assert np.array_equal(l2g[np.asarray(lv.element_dofs)], ged[e0 * ne_layer:e1 * ne_layer])
+        if lv.down:  # bottom ghost <- rank-1's owned top plane
+            dn = lvs[r - 1]
+            assert np.array_equal(plane_ids(lv.e0 * p), dn.off + dn.top_plane.numpy())
+        if lv.up:  # top+1 ghost <- rank+1's owned bottom+1 plane
+            upl = lvs[r + 1]
+            assert np.array_equal(plane_ids(lv.e1 * p + 1), upl.off + upl.bot_plus1.numpy())
