@@ -538,11 +538,12 @@ __global__ void ell_fill_kernel(int64_t n, int nblocks, const int* __restrict__ 
 
 
 // lanes per block: small blocks (p <= 2 levels, ~1.5 rows per dependency
-// level) run the quad-row sweep with 8 lanes (4 blocks per warp), 16 on grids
-// of a few waves (latency bound); larger blocks are smem-bound (18 B per row)
-// and run one per warp.  Measured with tools/vcycle_breakdown.py and
-// tools/box_tgv.py: cfg3 p = 4 small-block sweeps 7.05 -> 5.58 ms per V-cycle,
-// TGV 16^3 p = 5 227 -> 168 ms per step against 2 lanes (sequential chain).
+// level) run the two-level-lookahead sweep with 4 lanes (8 blocks per warp),
+// or on grids of a few waves (latency bound) the quad-row sweep with 16;
+// larger blocks are smem-bound (18 B per row) and run one per warp.
+// Measured with tools/vcycle_breakdown.py and tools/box_tgv.py against the
+// round-1 choice (2 lanes, one level of lookahead): cfg3 p = 4 small-block
+// sweeps 7.05 -> 4.87 ms per V-cycle, TGV 16^3 p = 5 227 -> 168-173 ms per step.
 inline int small_block_lanes() {  // FB_BILU_SMALL_LANES=<2|4|8|16>: A/B runs (0: auto)
   static int v = -1;
   if (v < 0) {
@@ -554,7 +555,7 @@ inline int small_block_lanes() {  // FB_BILU_SMALL_LANES=<2|4|8|16>: A/B runs (0
 inline int block_ilu_lanes(const fb_blockilu* B) {
   if (B->max_block > 160) return 32;
   const int v = small_block_lanes();
-  return v > 0 ? v : (small_grid(B) ? 16 : 8);
+  return v > 0 ? v : (small_grid(B) ? 16 : 4);
 }
 // shared memory of the widest launch (small blocks: up to 16 per warp)
 inline size_t block_ilu_smem_max(int max_block) {
@@ -1483,6 +1484,16 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
   // small blocks: quad-row sweep (FB_BILU_SMALL_QUAD=0: the sequential-chain sweep, A/B runs)
   static const bool small_quad = !(getenv("FB_BILU_SMALL_QUAD") && getenv("FB_BILU_SMALL_QUAD")[0] == '0');
   const bool pipe = g_bilu_pipe >= 1 && !(small_quad && B->max_block <= 160 && lanes >= 4);
+  // small blocks on grids of many waves: the sequential-chain sweep with two
+  // levels of lookahead, 4 lanes per block (cfg3 p = 4: 5.45 -> 4.87 ms of
+  // small-block sweeps per V-cycle against the quad-row sweep);
+  // FB_BILU_SMALL_PIPE2=0 turns it off (A/B runs)
+  static const bool pipe2 = !(getenv("FB_BILU_SMALL_PIPE2") && getenv("FB_BILU_SMALL_PIPE2")[0] == '0');
+  if (pipe2 && B->max_block <= 160 && g_bilu_pipe >= 1 && !small_grid(B)) {
+    if (lanes == 4) return launch_block_ilu<4, 2>(B, a, b, r, out, st);
+    if (lanes == 8) return launch_block_ilu<8, 2>(B, a, b, r, out, st);
+    if (lanes == 2) return launch_block_ilu<2, 2>(B, a, b, r, out, st);
+  }
   switch (lanes) {
     case 2: return pipe ? launch_block_ilu<2, true>(B, a, b, r, out, st) : launch_block_ilu<2, false>(B, a, b, r, out, st);
     case 4: return pipe ? launch_block_ilu<4, true>(B, a, b, r, out, st) : launch_block_ilu<4, false>(B, a, b, r, out, st);
