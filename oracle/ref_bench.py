@@ -16,8 +16,9 @@ path:
 
 The backend is `FLOWBENCH_BACKEND=numba` (the reference default; its kernels
 are serial `@njit`) and the process is pinned to one thread for
-numba / OpenMP / OpenBLAS, so `cores` = 1, except for the `--impl reference`
-arm, which allows all host threads (`--threads`).  This module never imports the
+numba / OpenMP / OpenBLAS, except for the `--impl reference` arm, which allows
+all host threads (`--threads`); the reference's kernels are serial, so `cores`
+= 1 either way.  This module never imports the
 product package; run it as a subprocess:
 
     python -m oracle.ref_bench apply --target 120000 --steps 3 --warmup 1
@@ -96,7 +97,8 @@ def apply_sweep(target=120_000, degrees=range(1, 9), steps=3, warmup=1, threads=
     tot_s = sum(per.values())
     return {
         "value": tot_dofs / tot_s / 1e9, "unit": "GDoF/s", "seconds": tot_s, "steps": steps,
-        "warmup": warmup, "setup_s": round(setup, 2), "cores": threads, "kind": "reference",
+        "warmup": warmup, "setup_s": round(setup, 2), "cores": 1, "threads_allowed": threads,
+        "kind": "reference",
         "per_p": {str(pr["p"]): {"dofs": pr["dofs"], "cells": pr["n"],
                                  "ms_per_apply": round(1e3 * per[pr["p"]] / steps, 3),
                                  "mdofs": round(pr["dofs"] * steps / per[pr["p"]] / 1e6, 4)}
@@ -104,8 +106,8 @@ def apply_sweep(target=120_000, degrees=range(1, 9), steps=3, warmup=1, threads=
         "sample": (f"reference flowbench 0.1.0 (oracle/_ref) HelmholtzOperator(c=10, nu=1).apply, "
                    f"p=1..8, ~{target / 1e3:.0f}k DoFs per degree (n^3 perturbed cube), "
                    f"FLOWBENCH_BACKEND=numba, {threads} host thread(s) allowed to numba / OpenMP / "
-                   f"BLAS (the reference's @njit kernels are serial); {steps} timed sweep(s) "
-                   f"after {warmup} warm-up"),
+                   f"BLAS; the reference's @njit kernels are serial, so it uses one core "
+                   f"(cores = 1); {steps} timed sweep(s) after {warmup} warm-up"),
     }
 
 
