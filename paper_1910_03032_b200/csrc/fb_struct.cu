@@ -409,6 +409,14 @@ __global__ void __launch_bounds__(32 * kTE) transfer_prolong_sf_kernel(TransferV
   const double* Wa[3];
   transfer_elem(T, e, ec, Wa);
   constexpr int nc = NC, nf = NF, nc3 = NC * NC * NC, nf3 = NF * NF * NF;
+  constexpr int NG = (nf3 + 31) / 32;
+  int fm[NG];  // output map, loaded before the passes (off the store path)
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const int l = lane + 32 * i;
+    fm[i] = l < nf3 ? __ldg(T.fmap + e * nf3 + l) : 0;
+  }
+#pragma unroll
   for (int j = lane; j < nc3; j += 32) xe[j] = __ldg(xc + __ldg(T.hmap + e * nc3 + j));
   for (int j = lane; j < nf * nc; j += 32)
     for (int a = 0; a < 3; ++a) w[a][j] = __ldg(Wa[a] + j);
@@ -429,13 +437,16 @@ __global__ void __launch_bounds__(32 * kTE) transfer_prolong_sf_kernel(TransferV
     t2[k] = ab;
   }
   __syncwarp();
-  for (int l = lane; l < nf3; l += 32) {  // z: (l2, l1, l0), owned fine DoFs only
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {  // z: (l2, l1, l0), owned fine DoFs only
+    const int l = lane + 32 * i;
+    if (l >= nf3) continue;
     const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
     if (!owned_local(T, ec, l0, l1, l2)) continue;
     double acc = 0.0;
 #pragma unroll
     for (int c = 0; c < nc; ++c) acc += w[2][l2 * nc + c] * t2[(c * nf + l1) * nf + l0];
-    xf[__ldg(T.fmap + e * nf3 + l)] = acc;
+    xf[fm[i]] = acc;
   }
 }
 
@@ -457,9 +468,20 @@ __global__ void __launch_bounds__(32 * kTE) transfer_restrict_sf_kernel(Transfer
   const double* Wa[3];
   transfer_elem(T, e, ec, Wa);
   constexpr int nc = NC, nf = NF, nc3 = NC * NC * NC, nf3 = NF * NF * NF;
-  for (int l = lane; l < nf3; l += 32) {
-    const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
-    rf[l] = owned_local(T, ec, l0, l1, l2) ? __ldg(xf + __ldg(T.fmap + e * nf3 + l)) : 0.0;
+  constexpr int NG = (nf3 + 31) / 32;  // map loads first, then the gathers (two latencies)
+  int fm[NG];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const int l = lane + 32 * i;
+    fm[i] = l < nf3 ? __ldg(T.fmap + e * nf3 + l) : 0;
+  }
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const int l = lane + 32 * i;
+    if (l < nf3) {
+      const int l0 = l % nf, l1 = (l / nf) % nf, l2 = l / (nf * nf);
+      rf[l] = owned_local(T, ec, l0, l1, l2) ? __ldg(xf + fm[i]) : 0.0;
+    }
   }
   for (int j = lane; j < nf * nc; j += 32)
     for (int a = 0; a < 3; ++a) w[a][j] = __ldg(Wa[a] + j);
