@@ -317,3 +317,27 @@ def test_slab_layout_host(world, counts, p):
         if lv.up:  # top+1 ghost <- rank+1's owned bottom+1 plane
             upl = lvs[r + 1]
             assert np.array_equal(plane_ids(lv.e1 * p + 1), upl.off + upl.bot_plus1.numpy())
+
+
+@pytest.mark.gpu
+def test_sharded_cfg3_default_hierarchy_matches_single_gpu():
+    """cfg3 shape at 2.1M DoFs with the default hierarchy (Q1 level above
+    max_coarse: sharded Q1, agglomerated h-coarse levels) on 1, 2 and 4
+    ranks: equal iteration counts, solutions equal to rounding."""
+    from paper_1910_03032_b200 import dist_box as D, solvers, structured as S
+    counts, p = (32, 32, 32), 4
+    cfg = solvers.SolverConfig(rel_tol=1e-8, max_iters=300)
+    mesh = S.box_mesh(counts, perturb=0.05, seed=1)
+    ref = S.helmholtz_box_problem(counts, p, c=10.0)
+    x_ref, rep_ref = solvers.cg(ref["A"], ref["b"], precond=ref["M"], config=cfg)
+    x_ref = x_ref.cpu().numpy()
+    for world in (2, 4):
+        def fn(comm):
+            pr = D.helmholtz_slab_problem(comm, counts, p, c=10.0, mesh=mesh)
+            lv = pr["level"]
+            x, rep = D.dist_cg(pr["A"], pr["b"], pr["M"], comm, lv.n_own, cfg)
+            return x[:lv.n_own].cpu().numpy(), rep.iterations, pr["M"].q1_sharded
+        out = D.run_threads(world, fn)
+        assert all(o[2] for o in out)
+        assert all(o[1] == rep_ref.iterations for o in out), ([o[1] for o in out], rep_ref.iterations)
+        assert rel_err(np.concatenate([o[0] for o in out]), x_ref) < 1e-12
