@@ -12,7 +12,7 @@ scipy.sparse and moved to the device by the solvers (``sparse.DeviceCSR``).
 import numpy as np
 import scipy.sparse as sp
 
-from .geometry import compute_geometric_factors, tensor_points, tensor_weights, q1_shape
+from .geometry import compute_geometric_factors
 from .quadrature import GAUSS_LEGENDRE, build_eval_matrices, quadrature_rule
 from .spaces import element_node_coords
 
