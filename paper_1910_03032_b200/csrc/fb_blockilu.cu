@@ -1037,6 +1037,16 @@ __device__ __forceinline__ void packed_rows(const double* vals, const double* in
     const int t = t0 + (lane >> LG);
     const bool live = t < R;
     const int start = live ? rst[t] : 0, n = live ? cnt[t] : 0;
+    // S <= 2 (wide levels): the row's own value and scale do not depend on
+    // this level's sums -- load them up front, off the critical path (p = 7
+    // sweep -5 %); with 4 lanes per row the redundant loads cost more (p = 4 +3 %)
+    int row = 0;
+    double yr = 0.0, iv = 1.0;
+    if constexpr (S <= 2) {
+      row = live ? rows[t] : 0;
+      yr = live ? y[row] : 0.0;
+      iv = (live && has_inv) ? inv[t] : 1.0;
+    }
     double av[U], yv[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -1053,9 +1063,13 @@ __device__ __forceinline__ void packed_rows(const double* vals, const double* in
     if constexpr (S >= 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     if constexpr (S >= 4) acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     if (live && sub == 0) {
-      const int row = rows[t];
-      const double res = y[row] - acc;
-      y[row] = has_inv ? res * inv[t] : res;
+      if constexpr (S > 2) {
+        row = rows[t];
+        yr = y[row];
+        iv = has_inv ? inv[t] : 1.0;
+      }
+      const double res = yr - acc;
+      y[row] = has_inv ? res * iv : res;
     }
   }
 }
