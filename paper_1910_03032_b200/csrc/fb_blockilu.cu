@@ -1015,7 +1015,7 @@ __device__ __forceinline__ void pk_copy(uint32_t dst, const void* src, uint32_t 
 __host__ __device__ inline size_t packed_smem(int nslot, int max_chunk, int max_block,
                                               int max_grp) {
   return 128 + size_t(nslot) * size_t(max_chunk) + size_t(max_block) * 8 +
-         size_t(max_grp + 1) * 16;
+         size_t(max_grp + 1) * 12;
 }
 
 // One dependency level of a packed chunk: rows t < R, S lanes per row.
@@ -1087,12 +1087,14 @@ __device__ __forceinline__ void pk_sync() {
 template <int NSLOT, int NW>
 __device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, uint64_t* bars,
                                            unsigned char* ring, int slot_bytes, int K,
-                                           int64_t* soff, int* sR, int* sE, uint32_t& used) {
+                                           int* soff, int* sR, int* sE, uint32_t& used) {
   const int lane = threadIdx.x;
   const int g0 = T.blk_grp[b], G = T.blk_grp[b + 1] - g0;
   const int NG = (G + K - 1) / K;
   pk_sync<NW>();
-  for (int i = lane; i <= G; i += 32 * NW) soff[i] = T.loff[g0 + i];
+  // level chunk offsets relative to the block's first chunk (32-bit), base kept 64-bit
+  const int64_t lbase = T.loff[g0];
+  for (int i = lane; i <= G; i += 32 * NW) soff[i] = int(T.loff[g0 + i] - lbase);
   for (int i = lane; i < G; i += 32 * NW) {
     sR[i] = T.grp[g0 + i + 1] - T.grp[g0 + i];
     sE[i] = T.lne[g0 + i];
@@ -1101,7 +1103,7 @@ __device__ __forceinline__ void packed_tri(const PackView& T, int b, double* y, 
   auto issue = [&](int j) {
     const uint32_t slot = (used + uint32_t(j)) % NSLOT;
     const int a = j * K, z = min(a + K, G);
-    pk_copy(psmem_u32(ring + size_t(slot) * slot_bytes), T.pk + soff[a],
+    pk_copy(psmem_u32(ring + size_t(slot) * slot_bytes), T.pk + lbase + soff[a],
             uint32_t(soff[z] - soff[a]), psmem_u32(&bars[slot]));
   };
   if (lane == 0) {
@@ -1147,7 +1149,7 @@ __global__ void __launch_bounds__(32 * NW) block_ilu_packed_kernel(
   uint64_t* bars = reinterpret_cast<uint64_t*>(psm);
   unsigned char* ring = psm + 128;
   double* y = reinterpret_cast<double*>(ring + size_t(NSLOT) * slot_bytes);
-  int64_t* soff = reinterpret_cast<int64_t*>(y + max_block);
+  int* soff = reinterpret_cast<int*>(y + max_block);
   int* sR = reinterpret_cast<int*>(soff + max_grp + 1);
   int* sE = sR + max_grp + 1;
   const int lane = threadIdx.x;
