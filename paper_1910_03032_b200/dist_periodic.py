@@ -293,7 +293,9 @@ class DistPeriodicLOR:
         q1 = self.q1
         rg = self.comm.allgather(rq[:q1.n_own], self.q1_sizes)
         xg = torch.empty_like(rg)
-        self.coarse.apply_into(rg, xg)
+        # the Q1 level of the single-GPU cycle (its cycle, not its apply: the
+        # mean projection happens once, around the whole V-cycle)
+        self.coarse._cycle(0, rg, xg, dev.stream_handle())
         o = int(self.q1_offsets[self.comm.rank])
         vec.copy(xg[o:o + q1.n_own], xq[:q1.n_own])
         if self._q1_ghost is None:
