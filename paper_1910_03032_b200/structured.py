@@ -234,10 +234,41 @@ def _coarse_vertex_index(n):
     return np.minimum(2 * np.arange(m + 1), n), m
 
 
+def can_coarsen_box(mesh):
+    """Geometric coarsening applies: at least 2 cells per direction, and
+    periodic directions keep >= 3 coarse cells with an even fine count."""
+    per = tuple(getattr(mesh, "periodic", ()) or (False,) * 3)
+    counts = tuple(mesh.counts)
+    if min(counts) < 2:
+        return False
+    return all(not per[a] or (counts[a] % 2 == 0 and counts[a] // 2 >= 3) for a in range(3))
+
+
 def coarsen_box(mesh):
     """Box of ceil(n/2) cells per direction whose vertices are every second
-    vertex of `mesh` (the last cell spans one fine cell when n is odd)."""
+    vertex of `mesh` (the last cell spans one fine cell when n is odd).
+    Periodic boxes (even counts along periodic axes): coarse cell (I, J, K)
+    has the corners of the fine cells (2I + bx, 2J + by, 2K + bz) at its
+    corners (bx, by, bz), so the wrap cells keep their physical corners."""
     counts = tuple(mesh.counts)
+    per = tuple(getattr(mesh, "periodic", ()) or (False,) * 3)
+    if any(per):
+        if not can_coarsen_box(mesh):
+            raise ValueError("periodic coarsening needs even counts and >= 6 cells per axis")
+        mx, my, mz = (c // 2 for c in counts)
+        cm = geometry.cartesian_mesh((mx, my, mz), periodic=per)
+        Fc = mesh.corners.reshape(counts[2], counts[1], counts[0], 8, 3)
+        I, J, K = (np.arange(m) for m in (mx, my, mz))
+        corners = np.empty((mz, my, mx, 8, 3))
+        for c in range(8):
+            bx, by, bz = c & 1, (c >> 1) & 1, (c >> 2) & 1
+            corners[:, :, :, c] = Fc[(2 * K + bz)[:, None, None], (2 * J + by)[None, :, None],
+                                     (2 * I + bx)[None, None, :], c]
+        corners = corners.reshape(-1, 8, 3)
+        vertices = np.zeros((cm.num_vertices, 3))
+        vertices[cm.elements.ravel()] = corners.reshape(-1, 3)  # identified vertices: one copy
+        return geometry.Mesh(3, vertices, cm.elements, corners, cm.boundary_faces, per,
+                             (mx, my, mz))
     V = mesh.vertices.reshape(counts[2] + 1, counts[1] + 1, counts[0] + 1, 3)
     (fx, mx), (fy, my), (fz, mz) = (_coarse_vertex_index(n) for n in counts)
     Vc = V[fz][:, fy][:, :, fx].reshape(-1, 3)
@@ -439,9 +470,7 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
             spaces.append(BoxSpace(space.mesh, deg, block=block if deg > 1 else q1_block,
                                    device=ddev))
         self.q1_index = len(spaces) - 1  # the ladder's Q1 level on the original mesh
-        periodic = any(getattr(space, "periodic", ()))
-        while (not periodic and spaces[-1].ndofs_scalar > max_coarse
-               and min(spaces[-1].counts) >= 2):
+        while spaces[-1].ndofs_scalar > max_coarse and can_coarsen_box(spaces[-1].mesh):
             spaces.append(BoxSpace(coarsen_box(spaces[-1].mesh), 1, block=q1_block, device=ddev))
         self.spaces = spaces
         # near-exact Q1 solve (SURVEY 8(e')): when the Q1 level is coarsened

@@ -432,3 +432,24 @@ def test_packed_block_ilu_sweep_matches_csr_sweep(p, counts):
         again = getattr(sms[1], f)(r, torch.empty_like(r))
         assert torch.equal(got, again), f
         assert rel_err(got.cpu().numpy(), want.cpu().numpy()) < 1e-13, f
+
+
+def test_periodic_coarsen_box():
+    """Geometric coarsening of a periodic box (the cfg5 Q1 hierarchy): the
+    coarse cells are the 2x2x2 fine cells' outer corners, wrap cells keep
+    their physical corners, periodic flags survive; odd / too small periodic
+    counts stop the coarsening."""
+    from paper_1910_03032_b200 import geometry, structured as S
+    lo, hi = (-np.pi,) * 3, (np.pi,) * 3
+    m = geometry.cartesian_mesh((8, 6, 12), lows=lo, highs=hi, periodic=(True,) * 3)
+    c = S.coarsen_box(m)
+    ref = geometry.cartesian_mesh((4, 3, 6), lows=lo, highs=hi, periodic=(True,) * 3)
+    assert c.counts == (4, 3, 6) and c.periodic == (True,) * 3
+    assert np.array_equal(c.elements, ref.elements)
+    assert np.abs(c.corners - ref.corners).max() == 0.0
+    assert S.can_coarsen_box(m) and not S.can_coarsen_box(c)
+    pm = geometry.perturb_mesh(m, 0.05, seed=4)
+    pc = S.coarsen_box(pm)
+    F = pm.corners.reshape(12, 6, 8, 8, 3)
+    assert np.array_equal(pc.corners.reshape(6, 3, 4, 8, 3)[2, 1, 3, 7], F[5, 3, 7, 7])
+    assert np.array_equal(pc.corners.reshape(6, 3, 4, 8, 3)[0, 0, 0, 0], F[0, 0, 0, 0])
