@@ -568,12 +568,13 @@ def _max_over_ranks(v):
     return float(t.item())
 
 
-def box_tgv_sharded(comm, p=5, n=32, steps=2, reduce_max=None):
+def box_tgv_sharded(comm, p=5, n=64, steps=2, reduce_max=None):
     """cfg5 on N GPUs: the periodic Taylor-Green projection step sharded over
     z-slabs on a ring (dist_periodic.DistProjectionStepper), strong scaling of
-    the n^3 box (32^3 p = 5: 12.3M velocity + 4.1M pressure DoFs, the
-    single-GPU box_tgv problem).  Per-step time from CUDA events between
-    barriers; reduce_max(ms) -> max over ranks (NCCL all-reduce in the bench)."""
+    the n^3 box (64^3 p = 5: 98.3M velocity + 32.8M pressure DoFs; 16 slab
+    units of 4 layers, balanced on 2, 4 and 8 ranks).  Per-step time from CUDA
+    events between barriers; reduce_max(ms) -> max over ranks (NCCL
+    all-reduce in the bench)."""
     import gc
     import torch
     from paper_1910_03032_b200 import dist_periodic as DP, geometry
