@@ -595,6 +595,11 @@ class DistProjectionStepper:
     def _helmholtz(self, b0):
         key = round(b0, 12)
         if key not in self._helm:
+            # one Helmholtz system at a time: the start-up orders (BDF1, BDF2)
+            # use theirs once, and each holds a full LOR hierarchy
+            self._helm.clear()
+            import gc
+            gc.collect()
             c = b0 / self.dt
             op = mfop.HelmholtzOperator(self.vv, self.geom, c=c, nu=self.nu)
             A = DistFieldOperator(op.apply_into, self.lv, self.comm, 3, 3)

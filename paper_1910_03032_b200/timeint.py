@@ -189,6 +189,11 @@ class ProjectionStepper:
     def _helmholtz(self, b0):
         key = round(b0, 12)
         if key not in self._helm:
+            # one Helmholtz system at a time: the start-up orders (BDF1, BDF2)
+            # use theirs once, and each holds a full LOR hierarchy
+            self._helm.clear()
+            import gc
+            gc.collect()
             c = b0 / self.dt
             op = mfop.HelmholtzOperator(self.vspace, self.geom, c=c, nu=self.nu)
             A = mfop.ConstrainedOperator(op, self.bdofs)

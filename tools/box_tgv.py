@@ -11,6 +11,21 @@ sys.path.insert(0, ".")
 from paper_1910_03032_b200 import geometry, timeint  # noqa: E402
 
 p, n, steps = (int(a) for a in sys.argv[1:4])
+import threading  # noqa: E402
+
+_peak = [0]
+_stop = threading.Event()
+
+
+def _sample():  # device-wide memory in use (the C library allocates outside torch)
+    while not _stop.is_set():
+        free, total = torch.cuda.mem_get_info()
+        _peak[0] = max(_peak[0], total - free)
+        time.sleep(0.02)
+
+
+torch.cuda.init()
+threading.Thread(target=_sample, daemon=True).start()
 m = geometry.cartesian_mesh((n, n, n), lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
                             periodic=(True,) * 3)
 t0 = time.perf_counter()
@@ -41,4 +56,7 @@ print(json.dumps({"p": p, "cells": n, "velocity_dofs": int(st.vspace.ndofs),
                   "pressure_dofs": int(st.pspace.ndofs), "ms_per_step": round(ms, 2),
                   "iterations_mass_pressure_helmholtz": its, "phase_ms": ph,
                   "setup_s": round(setup, 2), "kinetic_energy": st.kinetic_energy(),
-                  "mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2)}))
+                  "torch_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2),
+                  "device_peak_gb": round(_peak[0] / 1e9, 2),
+                  "device_now_gb": round((lambda fi: fi[1] - fi[0])(torch.cuda.mem_get_info()) / 1e9, 2)}))
+_stop.set()
