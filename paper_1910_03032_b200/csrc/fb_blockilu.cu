@@ -1042,7 +1042,8 @@ __device__ __forceinline__ void packed_rows(const double* vals, const double* in
     // sweep -5 %); with 4 lanes per row the redundant loads cost more (p = 4 +3 %)
     int row = 0;
     double yr = 0.0, iv = 1.0;
-    if constexpr (S <= 2) {
+    constexpr bool HOIST = S <= 2 && NW == 2;  // large blocks only (p = 4 measured neutral-to-worse)
+    if constexpr (HOIST) {
       row = live ? rows[t] : 0;
       yr = live ? y[row] : 0.0;
       iv = (live && has_inv) ? inv[t] : 1.0;
@@ -1063,7 +1064,7 @@ __device__ __forceinline__ void packed_rows(const double* vals, const double* in
     if constexpr (S >= 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     if constexpr (S >= 4) acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     if (live && sub == 0) {
-      if constexpr (S > 2) {
+      if constexpr (!HOIST) {
         row = rows[t];
         yr = y[row];
         iv = has_inv ? inv[t] : 1.0;
