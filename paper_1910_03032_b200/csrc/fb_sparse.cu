@@ -316,6 +316,17 @@ int fb_trisolve_solve(const fb_trisolve* T, const double* b, double* x, void* st
   FB_REQUIRE(b != x, "in-place triangular solve is not supported");
   if (T->n == 0) return FB_OK;
   cudaStream_t st = as_stream(stream);
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  FB_TRY_CUDA(cudaStreamIsCapturing(st, &cap_status));
+  if (cap_status == cudaStreamCaptureStatusActive) {
+    // inside a caller's stream capture (the device-resident CG loop): the
+    // level kernels themselves become nodes of the caller's graph (no nested
+    // graph launch, no host-side epoch)
+    trisolve_levels(T, b, x, st);
+    launch_counter() += T->nlevels;
+    FB_CHECK_LAUNCH();
+    return FB_OK;
+  }
   if (g_trisolve_mode == 1) {
     // one graph per (b, x, stream) binding; re-captured when the operands change
     if (!T->graph || T->graph_b != b || T->graph_x != x || T->graph_stream != st) {

@@ -992,8 +992,11 @@ class LORPreconditioner(_DeviceMixin):
     @property
     def graph_safe(self):
         """The V-cycle is device launches only on preallocated level vectors
-        (block smoother, dense coarse inverse, no mean projection)."""
-        return (self.smoother_kind == "block" and isinstance(self._bottom, DenseInverseSolver)
+        (block smoother, or the global ILU whose level-scheduled triangular
+        solves capture as plain kernels; dense-inverse or device sparse-LU
+        coarse solve; no mean projection)."""
+        return (self.smoother_kind in ("block", "global")
+                and isinstance(self._bottom, (DenseInverseSolver, SparseLUSolver))
                 and not self.pure_neumann)
 
     def clone_workspace(self):
