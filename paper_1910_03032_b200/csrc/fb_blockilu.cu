@@ -1360,7 +1360,8 @@ template <int NSLOT>
 static int launch_packed(const fb_blockilu* B, const TriPart& a, bool ua, const TriPart& b,
                          bool ub, const double* r, double* out, cudaStream_t st) {
   static const int nw_env = getenv("FB_BILU_NW") ? atoi(getenv("FB_BILU_NW")) : 0;
-  const int nw = nw_env > 0 ? nw_env : (B->max_block > 1024 ? 2 : 1);
+  // by the typical block (first-touch boundary blocks are larger than interior ones)
+  const int nw = nw_env > 0 ? nw_env : (B->n / std::max(B->nblocks, 1) > 1024 ? 2 : 1);
   if (nw == 2) return launch_packed_w<NSLOT, 2>(B, a, ua, b, ub, r, out, st);
   return launch_packed_w<NSLOT, 1>(B, a, ua, b, ub, r, out, st);
 }
