@@ -1,3 +1,6 @@
+"""Search the work-buffer pitches (x-row pitch, z-plane pitch, element pad) of
+the fused kernel that minimise shared-memory wavefronts (bank_model.py's
+access model); produced the SF3Pitch tables in csrc/sf3_fast.cuh."""
 import itertools, sys
 
 
