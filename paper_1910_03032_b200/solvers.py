@@ -1037,9 +1037,14 @@ class BlockDiagonalPreconditioner(_DeviceMixin):
         self.ns = ndofs_scalar
         self._apply = _device_apply(scalar_precond)
         # components are independent: with per-component workspaces the
-        # (latency-bound) V-cycles run concurrently on their own streams
+        # (latency-bound) V-cycles run concurrently on their own streams.
+        # Only for small components: measured on p = 5 box hierarchies
+        # (tools/bd_concurrency.py), 0.5M rows per component 2.0x faster,
+        # 1.7M 1.14x, 4.1M even, 13.8M / 32.8M 1.3x / 1.4x SLOWER than one
+        # after the other (the three hierarchies then compete for L2 / HBM).
         self._par = None
-        if vdim > 1 and hasattr(scalar_precond, "clone_workspace"):
+        par_max = int(os.environ.get("FB_BD_CONCURRENT_MAX", "3000000"))
+        if vdim > 1 and hasattr(scalar_precond, "clone_workspace") and ndofs_scalar <= par_max:
             clones = [scalar_precond.clone_workspace() for _ in range(vdim - 1)]
             if all(c is not None for c in clones) and torch.cuda.is_available():
                 self._par = [scalar_precond] + clones
