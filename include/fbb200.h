@@ -209,6 +209,11 @@ int fb_csr_spmv(const fb_csr* A, const double* x_dev, double* y_dev, void* strea
 /* y = b - A x */
 int fb_csr_residual(const fb_csr* A, const double* b_dev, const double* x_dev, double* y_dev,
                     void* stream);
+/* y_j = b_j - A x_j (b NULL: y_j = A x_j) for nv = 1..4 vectors stored at a
+ * common stride (the components of a vector field sharing one scalar level
+ * matrix): each entry is read once; per vector bitwise fb_csr_residual. */
+int fb_csr_residual_multi(const fb_csr* A, int nv, const double* b_dev, const double* x_dev,
+                          double* y_dev, int64_t stride, void* stream);
 /* Sparse triangular solve T x = b (lower=1: forward, 0: backward; unit_diag
  * ignores/omits the diagonal).  Sync-free: one launch per solve. */
 int fb_trisolve_create(int64_t n, const int64_t* indptr_host, const int64_t* indices_host,

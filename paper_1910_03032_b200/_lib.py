@@ -80,6 +80,7 @@ _SIGS = [
     ("fb_csr_destroy", None, [_vp]),
     ("fb_csr_spmv", _int, [_vp, _vp, _vp, _vp]),
     ("fb_csr_residual", _int, [_vp, _vp, _vp, _vp, _vp]),
+    ("fb_csr_residual_multi", _int, [_vp, _int, _vp, _vp, _vp, _i64, _vp]),
     ("fb_trisolve_create", _int, [_i64, _vp, _vp, _vp, _int, _int, C.POINTER(_vp)]),
     ("fb_trisolve_destroy", None, [_vp]),
     ("fb_trisolve_solve", _int, [_vp, _vp, _vp, _vp]),

@@ -100,6 +100,43 @@ __global__ void __launch_bounds__(256) csr_spmv_group_kernel(int64_t nrows,
   if (live && lane == 0) y[r] = b ? __ldg(b + r) - acc : acc;
 }
 
+// Several right-hand sides at once (NV vectors at a common stride, e.g. the
+// components of a vector field sharing one scalar LOR level): each matrix
+// entry and column index is loaded once for all NV products.  Per vector the
+// entry order and the butterfly combine are those of csr_spmv_group_kernel<4>,
+// so every result is bitwise the single-vector one.
+template <int NV>
+__global__ void __launch_bounds__(256) csr_spmv_group_multi_kernel(
+    int64_t nrows, const int64_t* __restrict__ ip, const int* __restrict__ ix,
+    const double* __restrict__ v, const double* __restrict__ x, const double* __restrict__ b,
+    double* __restrict__ y, int64_t stride) {
+  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 4;
+  const int lane = threadIdx.x % 4;
+  const bool live = r < nrows;
+  double acc[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) acc[j] = 0.0;
+  if (live) {
+    const int64_t e0 = __ldg(ip + r), e1 = __ldg(ip + r + 1);
+    for (int64_t k = e0 + lane; k < e1; k += 4) {
+      const double a = __ldg(v + k);
+      const int c = __ldg(ix + k);
+#pragma unroll
+      for (int j = 0; j < NV; ++j) acc[j] = fma(a, __ldg(x + j * stride + c), acc[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  }
+  if (live && lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      y[j * stride + r] = b ? __ldg(b + j * stride + r) - acc[j] : acc[j];
+  }
+}
+
 // y = A^T x for CSR A without a stored transpose is not deterministic in
 // parallel; transposes are stored explicitly by the caller instead.
 
@@ -232,6 +269,25 @@ int fb_csr_residual(const fb_csr* A, const double* b, const double* x, double* y
   else
     csr_spmv_kernel<<<ceil_div(A->nrows, 128), 128, 0, as_stream(stream)>>>(
         A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, b, y);
+  FB_CHECK_LAUNCH();
+  return FB_OK;
+}
+
+// y_j = b_j - A x_j (b == NULL: y_j = A x_j) for nv vectors at a common stride
+int fb_csr_residual_multi(const fb_csr* A, int nv, const double* b, const double* x, double* y,
+                          int64_t stride, void* stream) {
+  FB_REQUIRE(A != nullptr, "matrix is NULL");
+  FB_REQUIRE(nv >= 1 && nv <= 4, "nv must be 1..4");
+  FB_REQUIRE(A->warp_rows, "multi-vector SpMV needs a device-assembled (4 lanes per row) matrix");
+  if (A->nrows == 0) return FB_OK;
+  const unsigned grid = unsigned(ceil_div(A->nrows * 4, 256));
+  cudaStream_t st = as_stream(stream);
+  switch (nv) {
+    case 1: csr_spmv_group_multi_kernel<1><<<grid, 256, 0, st>>>(A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, b, y, stride); break;
+    case 2: csr_spmv_group_multi_kernel<2><<<grid, 256, 0, st>>>(A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, b, y, stride); break;
+    case 3: csr_spmv_group_multi_kernel<3><<<grid, 256, 0, st>>>(A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, b, y, stride); break;
+    default: csr_spmv_group_multi_kernel<4><<<grid, 256, 0, st>>>(A->nrows, A->indptr.ptr, A->indices.ptr, A->data.ptr, x, b, y, stride); break;
+  }
   FB_CHECK_LAUNCH();
   return FB_OK;
 }

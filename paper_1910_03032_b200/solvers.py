@@ -1051,6 +1051,13 @@ class BlockDiagonalPreconditioner(_DeviceMixin):
                 self._streams = [torch.cuda.Stream(device=dev.device()) for _ in range(vdim)]
                 self._done = [torch.cuda.Event() for _ in range(vdim)]
                 self._fork = torch.cuda.Event()
+        # large components one after the other: with one V-cycle for all of
+        # them the fine-level residuals share a pass over the level matrix
+        self._multi = (self._par is None and vdim > 1
+                       and hasattr(scalar_precond, "apply_multi_into")
+                       and os.environ.get("FB_BD_MULTI", "1") != "0")
+        if self._multi:
+            scalar_precond.prepare_multi(vdim)
 
     @property
     def graph_safe(self):
@@ -1070,6 +1077,8 @@ class BlockDiagonalPreconditioner(_DeviceMixin):
             for e in self._done:
                 cur.wait_event(e)
             return out
+        if self._multi:
+            return self.inner.apply_multi_into(r, out, self.vdim, ns, stream)
         for c in range(self.vdim):
             self._apply(r[c * ns:(c + 1) * ns], out[c * ns:(c + 1) * ns])
         return out

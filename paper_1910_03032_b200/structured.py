@@ -510,6 +510,48 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
             super()._cycle(level, self._rk, self._dk, st)
             vec.axpby(1.0, self._dk, 1.0, x, st)
 
+    def prepare_multi(self, nv):
+        """Workspaces of apply_multi_into for nv components (allocated up front
+        so a captured CG loop never allocates)."""
+        n0 = self.levels[0][0].ndofs_scalar
+        if getattr(self, "_mt", None) is None or self._mt.shape[0] != nv * n0:
+            self._mt, self._mt2 = dev.empty(nv * n0), dev.empty(nv * n0)
+        return self
+
+    def apply_multi_into(self, r, out, nv, stride, stream=None):
+        """nv right-hand sides at a common stride (the components of a vector
+        field): every component gets exactly apply_into's V-cycle (bitwise),
+        but the fine-level residuals of all components share one pass over the
+        level matrix (vec.DeviceCSR.residual_multi_into)."""
+        st = dev.stream_handle() if stream is None else stream
+        if self.pure_neumann or len(self.levels) < 2 or self.q1_index == 0:
+            for c in range(nv):
+                self.apply_into(r[c * stride:(c + 1) * stride], out[c * stride:(c + 1) * stride],
+                                stream)
+            return out
+        self.prepare_multi(nv)
+        A, sm = self._A[0], self.smoothers[0]
+        t, t2 = self._mt, self._mt2
+        m = nv * stride
+
+        def sl(v, c):
+            return v[c * stride:(c + 1) * stride]
+
+        for c in range(nv):
+            sm.forward_into(sl(r, c), sl(out, c), st)
+        A.residual_multi_into(nv, stride, r, out, t, st)
+        rc, xc = self._r[1], self._x[1]
+        for c in range(nv):
+            self._Pt[0].apply_into(sl(t, c), rc, st)
+            self._cycle(1, rc, xc, st)
+            self._P[0].apply_into(xc, sl(t, c), st)
+        vec.axpby(1.0, t[:m], 1.0, out[:m], st)
+        A.residual_multi_into(nv, stride, r, out, t, st)
+        for c in range(nv):
+            sm.backward_into(sl(t, c), sl(t2, c), st)
+        vec.axpby(1.0, t2[:m], 1.0, out[:m], st)
+        return out
+
     def clone_workspace(self):
         """Concurrent copy for BlockDiagonalPreconditioner: own level vectors
         and own transfers (a transfer keeps its per-element restriction

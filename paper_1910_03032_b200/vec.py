@@ -163,6 +163,13 @@ class DeviceCSR:
                                             _st(stream)))
         return y
 
+    def residual_multi_into(self, nv, stride, b, x, y, stream=None):
+        """y_j = b_j - A x_j for nv vectors at a common stride (one matrix read;
+        device-assembled matrices only)."""
+        _lib.check(_lib.lib.fb_csr_residual_multi(self.handle, int(nv), b.data_ptr(), x.data_ptr(),
+                                                  y.data_ptr(), int(stride), _st(stream)))
+        return y
+
 
 class TriSolve:
     """Sparse triangular solve on the device (sync-free, one launch)."""

@@ -453,3 +453,33 @@ def test_periodic_coarsen_box():
     F = pm.corners.reshape(12, 6, 8, 8, 3)
     assert np.array_equal(pc.corners.reshape(6, 3, 4, 8, 3)[2, 1, 3, 7], F[5, 3, 7, 7])
     assert np.array_equal(pc.corners.reshape(6, 3, 4, 8, 3)[0, 0, 0, 0], F[0, 0, 0, 0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,periodic", [(4, False), (5, True), (3, False)])
+def test_vector_vcycle_multi_rhs_is_bitwise_per_component(p, periodic, monkeypatch):
+    """Vector preconditioner on large components (no concurrent streams): the
+    shared-matrix multi-RHS V-cycle (BoxLORPreconditioner.apply_multi_into)
+    equals the per-component V-cycles bitwise."""
+    import torch
+    from paper_1910_03032_b200 import geometry, solvers, structured as S
+    counts = (6, 6, 8)
+    if periodic:
+        m = geometry.cartesian_mesh(counts, lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
+                                    periodic=(True,) * 3)
+    else:
+        m = geometry.perturb_mesh(geometry.cartesian_mesh(counts), 0.05, seed=6)
+    sp = S.BoxSpace(m, p, block=2, device=torch.device("cuda"))
+    cyc = S.BoxLORPreconditioner(sp, "helmholtz", nu=0.01, c=20.0, max_coarse=200)
+    monkeypatch.setenv("FB_BD_CONCURRENT_MAX", "0")
+    monkeypatch.setenv("FB_BD_MULTI", "1")
+    Pm = solvers.BlockDiagonalPreconditioner(cyc, 3, sp.ndofs)
+    monkeypatch.setenv("FB_BD_MULTI", "0")
+    Ps = solvers.BlockDiagonalPreconditioner(cyc, 3, sp.ndofs)
+    assert Pm._multi and not Ps._multi and Pm._par is None
+    r = torch.from_numpy(np.random.default_rng(8).standard_normal(3 * sp.ndofs)).cuda()
+    zm, zs = torch.empty_like(r), torch.empty_like(r)
+    Pm.apply_into(r, zm)
+    Ps.apply_into(r, zs)
+    torch.cuda.synchronize()
+    assert torch.equal(zm, zs)

@@ -25,7 +25,8 @@ def _sample():  # device-wide memory in use (the C library allocates outside tor
 
 
 torch.cuda.init()
-threading.Thread(target=_sample, daemon=True).start()
+_th = threading.Thread(target=_sample, daemon=True)
+_th.start()
 m = geometry.cartesian_mesh((n, n, n), lows=(-np.pi,) * 3, highs=(np.pi,) * 3,
                             periodic=(True,) * 3)
 t0 = time.perf_counter()
@@ -52,6 +53,8 @@ torch.cuda.synchronize()
 ms = 1e3 * (time.perf_counter() - t0) / steps
 st.profile = True
 ph = st.step().phase_ms
+_stop.set()
+_th.join()
 print(json.dumps({"p": p, "cells": n, "velocity_dofs": int(st.vspace.ndofs),
                   "pressure_dofs": int(st.pspace.ndofs), "ms_per_step": round(ms, 2),
                   "iterations_mass_pressure_helmholtz": its, "phase_ms": ph,
@@ -59,4 +62,3 @@ print(json.dumps({"p": p, "cells": n, "velocity_dofs": int(st.vspace.ndofs),
                   "torch_mem_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2),
                   "device_peak_gb": round(_peak[0] / 1e9, 2),
                   "device_now_gb": round((lambda fi: fi[1] - fi[0])(torch.cuda.mem_get_info()) / 1e9, 2)}))
-_stop.set()
