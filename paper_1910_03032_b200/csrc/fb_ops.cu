@@ -255,13 +255,15 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // per CTA: double-buffered map/slot stage, gather buffer, 4 work buffers per
 // element (34-52 KB); the grid is persistent (all CTAs resident).
 // Runtime-selectable launch shapes (tuning): g_fast_cfg[p] picks a variant.
+// p = 4 default (v7): 2 elements x 96 threads at 4 CTAs / SM -- the 5-CTA shape
+// capped registers at 128 and spilled; 0.566 -> 0.545 ms (tools/tune_fast.py).
 // Defaults measured with tools/tune_fast.py: p = 2, 3, 5, 6 stage their
 // factor blocks in shared memory through the TMA engine (p = 3: +5 %, p = 4
 // with the z-line schedule: +9 %, p = 5:
 // +14 %, p = 2, 6: +1-2 %); at p = 7, 8 the extra 41-56 KB per CTA costs more
 // occupancy than it saves.
-static const int kFastCfgDefault[9] = {0, 0, 0, 5, 6, 5, 0, 0, 6};
-static int g_fast_cfg[9] = {0, 0, 0, 5, 6, 5, 0, 0, 6};
+static const int kFastCfgDefault[9] = {0, 0, 0, 5, 7, 5, 0, 0, 6};
+static int g_fast_cfg[9] = {0, 0, 0, 5, 7, 5, 0, 0, 6};
 
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   const int v = g_fast_cfg[op->rv->p < 9 ? op->rv->p : 0];
@@ -287,7 +289,7 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
       if (v == 4) return launch_fast_kind<5, 6, 1, 64, 12, 2>(op, x, y, st);
       if (v == 5) return launch_fast_kind<5, 6, 1, 96, 8, 2>(op, x, y, st);
       if (v == 6) return launch_fast_kind<5, 6, 2, 96, 5, 3>(op, x, y, st);
-      if (v == 7) return launch_fast_kind<5, 6, 2, 64, 8, 3>(op, x, y, st);
+      if (v == 7) return launch_fast_kind<5, 6, 2, 96, 4, 3>(op, x, y, st);
       return launch_fast_kind<5, 6, 2, 96, 8>(op, x, y, st);
     case 5:
       if (v == 1) return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
