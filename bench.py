@@ -814,6 +814,29 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     e2e_ms = ea.elapsed_time(eb) / e2e_steps
     ok = all(torch.equal(hy[i], pr["y"].cpu()) for i, pr in enumerate(probs))
+
+    # the same copies with the applies removed: the PCIe bound of the e2e figure
+    # on this box (hosts differ in link / NUMA placement from box to box)
+    def copy_step():
+        for i, pr in enumerate(probs):
+            with torch.cuda.stream(s_in):
+                pr["x"].copy_(hx[i], non_blocking=True)
+                done_in[i].record(s_in)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(done_in[i])
+                hy[i].copy_(pr["y"], non_blocking=True)
+
+    copy_step()
+    torch.cuda.synchronize()
+    ea.record(s_in)
+    s_out.wait_event(ea)
+    for _ in range(e2e_steps):
+        copy_step()
+    tail_in.record(s_in)
+    s_out.wait_event(tail_in)
+    eb.record(s_out)
+    torch.cuda.synchronize()
+    copy_ms = ea.elapsed_time(eb) / e2e_steps
     if world > 1:
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -888,6 +911,12 @@ def run_ours(args, rank, world):
                 "note": "HelmholtzOperator.apply_into per degree, pinned-host x/y copies inside "
                         "the timed region, H2D/apply/D2H pipelined over the sweep on 3 streams",
                 "readback_matches_device": ok,
+                "copy_only": {"ms_per_step": round(copy_ms, 3),
+                              "gdofs": round(world * dofs_step / (copy_ms * 1e-3) / 1e9, 4),
+                              "gbps_per_direction": round(8 * dofs_step / (copy_ms * 1e-3) / 1e9,
+                                                          1),
+                              "note": "same pinned H2D/D2H copies, applies removed: the "
+                                      "PCIe bound of this box"},
                 "numpy_api": {"value": round(world * dofs_step / (numpy_ms * 1e-3) / 1e9, 4),
                               "unit": "GDoF/s",
                               "note": "HelmholtzOperator.apply(numpy) per degree: pageable, "

@@ -257,13 +257,15 @@ int launch_fast_kind(const fb_operator* op, const double* x, double* y, cudaStre
 // Runtime-selectable launch shapes (tuning): g_fast_cfg[p] picks a variant.
 // p = 4 default (v7): 2 elements x 96 threads at 4 CTAs / SM -- the 5-CTA shape
 // capped registers at 128 and spilled; 0.566 -> 0.545 ms (tools/tune_fast.py).
+// p = 5, 6 defaults (v6): the z-line schedule (ZL = 3) with a register budget
+// of 158 / 211 (no spills): p = 5 0.484 -> 0.451 ms, p = 6 0.419 -> 0.352 ms.
 // Defaults measured with tools/tune_fast.py: p = 2, 3, 5, 6 stage their
 // factor blocks in shared memory through the TMA engine (p = 3: +5 %, p = 4
 // with the z-line schedule: +9 %, p = 5:
 // +14 %, p = 2, 6: +1-2 %); at p = 7, 8 the extra 41-56 KB per CTA costs more
 // occupancy than it saves.
-static const int kFastCfgDefault[9] = {0, 0, 0, 5, 7, 5, 0, 0, 6};
-static int g_fast_cfg[9] = {0, 0, 0, 5, 7, 5, 0, 0, 6};
+static const int kFastCfgDefault[9] = {0, 0, 0, 5, 7, 6, 6, 0, 6};
+static int g_fast_cfg[9] = {0, 0, 0, 5, 7, 6, 6, 0, 6};
 
 int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t st) {
   const int v = g_fast_cfg[op->rv->p < 9 ? op->rv->p : 0];
@@ -271,13 +273,13 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
     case 1: return launch_fast_kind<2, 3, 32, 288, 3>(op, x, y, st);  // (p=1 uses sf3_q1)
     case 2:
       if (v == 1) return launch_fast_kind<3, 4, 16, 256, 3, true>(op, x, y, st);
-      if (v == 2) return launch_fast_kind<3, 4, 8, 128, 6, false>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<3, 4, 4, 64, 6, 3>(op, x, y, st);
       if (v == 3) return launch_fast_kind<3, 4, 4, 64, 8, 3>(op, x, y, st);
       if (v == 4) return launch_fast_kind<3, 4, 4, 64, 10, 3>(op, x, y, st);
       return launch_fast_kind<3, 4, 4, 64, 10, true>(op, x, y, st);
     case 3:
-      if (v == 1) return launch_fast_kind<4, 5, 8, 256, 3, true>(op, x, y, st);
-      if (v == 2) return launch_fast_kind<4, 5, 4, 128, 6, false>(op, x, y, st);
+      if (v == 1) return launch_fast_kind<4, 5, 2, 64, 6, 3>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<4, 5, 4, 128, 3, 3>(op, x, y, st);
       if (v == 3) return launch_fast_kind<4, 5, 2, 64, 8, 3>(op, x, y, st);
       if (v == 4) return launch_fast_kind<4, 5, 2, 64, 10, 3>(op, x, y, st);
       if (v == 5) return launch_fast_kind<4, 5, 4, 128, 4, 3>(op, x, y, st);
@@ -286,28 +288,32 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
       if (v == 1) return launch_fast_kind<5, 6, 4, 160, 5>(op, x, y, st);
       if (v == 2) return launch_fast_kind<5, 6, 1, 64, 12>(op, x, y, st);
       if (v == 3) return launch_fast_kind<5, 6, 2, 96, 6, 2>(op, x, y, st);
-      if (v == 4) return launch_fast_kind<5, 6, 1, 64, 12, 2>(op, x, y, st);
-      if (v == 5) return launch_fast_kind<5, 6, 1, 96, 8, 2>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<5, 6, 1, 64, 6, 3>(op, x, y, st);
+      if (v == 5) return launch_fast_kind<5, 6, 1, 64, 4, 3>(op, x, y, st);
       if (v == 6) return launch_fast_kind<5, 6, 2, 96, 5, 3>(op, x, y, st);
       if (v == 7) return launch_fast_kind<5, 6, 2, 96, 4, 3>(op, x, y, st);
       return launch_fast_kind<5, 6, 2, 96, 8>(op, x, y, st);
     case 5:
-      if (v == 1) return launch_fast_kind<6, 7, 3, 192, 4>(op, x, y, st);
-      if (v == 2) return launch_fast_kind<6, 7, 2, 128, 6>(op, x, y, st);
-      if (v == 3) return launch_fast_kind<6, 7, 1, 64, 8, 2>(op, x, y, st);
-      if (v == 4) return launch_fast_kind<6, 7, 1, 96, 6, 2>(op, x, y, st);
+      if (v == 1) return launch_fast_kind<6, 7, 1, 64, 6, 3>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<6, 7, 1, 64, 4, 3>(op, x, y, st);
+      if (v == 3) return launch_fast_kind<6, 7, 1, 64, 5, 3>(op, x, y, st);
+      if (v == 4) return launch_fast_kind<6, 7, 1, 96, 3, 3>(op, x, y, st);
       if (v == 5) return launch_fast_kind<6, 7, 2, 128, 3, 2>(op, x, y, st);
+      if (v == 6) return launch_fast_kind<6, 7, 2, 128, 3, 3>(op, x, y, st);
+      if (v == 7) return launch_fast_kind<6, 7, 2, 96, 4, 3>(op, x, y, st);
       return launch_fast_kind<6, 7, 1, 64, 10>(op, x, y, st);
     case 6:
-      if (v == 1) return launch_fast_kind<7, 8, 2, 128, 6>(op, x, y, st);
+      if (v == 1) return launch_fast_kind<7, 8, 2, 128, 2, 3>(op, x, y, st);
       if (v == 2) return launch_fast_kind<7, 8, 2, 192, 4>(op, x, y, st);
       if (v == 3) return launch_fast_kind<7, 8, 1, 96, 5, 2>(op, x, y, st);
       if (v == 4) return launch_fast_kind<7, 8, 1, 128, 4, 2>(op, x, y, st);
       if (v == 5) return launch_fast_kind<7, 8, 1, 64, 6, 2>(op, x, y, st);
+      if (v == 6) return launch_fast_kind<7, 8, 1, 64, 4, 3>(op, x, y, st);
+      if (v == 7) return launch_fast_kind<7, 8, 1, 64, 3, 3>(op, x, y, st);
       return launch_fast_kind<7, 8, 1, 96, 8>(op, x, y, st);
     case 7:
-      if (v == 1) return launch_fast_kind<8, 9, 2, 192, 3>(op, x, y, st);
-      if (v == 2) return launch_fast_kind<8, 9, 1, 96, 6>(op, x, y, st);
+      if (v == 1) return launch_fast_kind<8, 9, 1, 96, 3, 3>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<8, 9, 1, 160, 2, 3>(op, x, y, st);
       if (v == 3) return launch_fast_kind<8, 9, 1, 128, 3, 2>(op, x, y, st);
       if (v == 4) return launch_fast_kind<8, 9, 1, 192, 2, 2>(op, x, y, st);
       if (v == 5) return launch_fast_kind<8, 9, 1, 96, 3, 2>(op, x, y, st);
@@ -315,8 +321,8 @@ int launch_fast(const fb_operator* op, const double* x, double* y, cudaStream_t 
       if (v == 7) return launch_fast_kind<8, 9, 1, 192, 2, 3>(op, x, y, st);
       return launch_fast_kind<8, 9, 1, 128, 4>(op, x, y, st);
     case 8:
-      if (v == 1) return launch_fast_kind<9, 10, 1, 96, 5>(op, x, y, st);
-      if (v == 2) return launch_fast_kind<9, 10, 2, 224, 2>(op, x, y, st);
+      if (v == 1) return launch_fast_kind<9, 10, 1, 96, 2, 3>(op, x, y, st);
+      if (v == 2) return launch_fast_kind<9, 10, 1, 160, 1, 3>(op, x, y, st);
       if (v == 3) return launch_fast_kind<9, 10, 1, 128, 2, 2>(op, x, y, st);
       if (v == 4) return launch_fast_kind<9, 10, 1, 192, 2, 2>(op, x, y, st);
       if (v == 5) return launch_fast_kind<9, 10, 1, 256, 1, 2>(op, x, y, st);

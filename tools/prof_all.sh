@@ -5,7 +5,7 @@ python bench.py > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err
 python bench.py --impl reference > gpurun_out/final/bench_ref.json 2> gpurun_out/final/bench_ref.err
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv python bench.py --steps 2 --warmup 1 --no-cpu --no-pcg --no-cfg3 --no-callers > gpurun_out/final/launches.csv 2> gpurun_out/final/launches.err
 python tools/launch_shares.py gpurun_out/final/launches.csv gpurun_out/final/launch_shares.txt gpurun_out/final/traffic.json > /dev/null 2>&1
-for p in 4 8; do
+for p in 4 6 8; do
   ncu --set full --import-source on --clock-control none -k regex:sf3_fast_kernel -s 2 -c 1 -o /tmp/k$p python tools/profile_apply.py --p $p --dofs 1e7 > /dev/null 2>&1
   python tools/ncu_summary.py /tmp/k$p.ncu-rep > gpurun_out/final/ncu_full_p$p.txt 2>&1
 done
