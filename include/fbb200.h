@@ -337,6 +337,10 @@ int fb_transfer_set_origin(fb_transfer* T, int64_t x0, int64_t y0, int64_t z0);
 int fb_index_add(int64_t n, const int* idx_dev, const double* v_dev, double* y_dev, void* stream);
 /* xf = P xc */
 int fb_transfer_prolong(const fb_transfer* T, const double* xc_dev, double* xf_dev, void* stream);
+/* xf += P xc (coarse-grid correction in place; rounding of xf = 1*(P xc) + 1*xf,
+ * reference solvers.py:381 `x = x + P @ ...`) */
+int fb_transfer_prolong_add(const fb_transfer* T, const double* xc_dev, double* xf_dev,
+                            void* stream);
 /* xc = P^T xf (deterministic) */
 int fb_transfer_restrict(const fb_transfer* T, const double* xf_dev, double* xc_dev, void* stream);
 

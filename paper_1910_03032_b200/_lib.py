@@ -112,6 +112,7 @@ _SIGS = [
     ("fb_transfer_set_origin", _int, [_vp, _i64, _i64, _i64]),
     ("fb_index_add", _int, [_i64, _vp, _vp, _vp, _vp]),
     ("fb_transfer_prolong", _int, [_vp, _vp, _vp, _vp]),
+    ("fb_transfer_prolong_add", _int, [_vp, _vp, _vp, _vp]),
     ("fb_transfer_restrict", _int, [_vp, _vp, _vp, _vp]),
     ("fb_set_blockilu_pipeline", _int, [_int, _int]),
 ]

@@ -257,6 +257,7 @@ struct TransferView {
   int nf, nc;
   int periodic;
   int64_t gn[3];
+  int add;  // prolongation: xf += P xc instead of xf = P xc
 };
 
 // fine element e: per-axis coordinates and weight tables
@@ -333,7 +334,10 @@ __global__ void __launch_bounds__(32 * kTE) transfer_prolong_kernel(TransferView
       }
       acc += w[2][l2 * nc + c] * ab;
     }
-    xf[__ldg(T.fmap + e * nf3 + l)] = acc;
+    {
+      double* d = xf + __ldg(T.fmap + e * nf3 + l);
+      *d = T.add ? __dadd_rn(acc, *d) : acc;
+    }
   }
 }
 
@@ -446,7 +450,7 @@ __global__ void __launch_bounds__(32 * kTE) transfer_prolong_sf_kernel(TransferV
     double acc = 0.0;
 #pragma unroll
     for (int c = 0; c < nc; ++c) acc += w[2][l2 * nc + c] * t2[(c * nf + l1) * nf + l0];
-    xf[fm[i]] = acc;
+    xf[fm[i]] = T.add ? __dadd_rn(acc, xf[fm[i]]) : acc;
   }
 }
 
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(256) transfer_q1_kernel(TransferView T, int64_
         }
         acc += w[2][l2 * 2 + c] * ab;
       }
-      out[fmap[l]] = acc;
+      out[fmap[l]] = T.add ? __dadd_rn(acc, out[fmap[l]]) : acc;
     }
   } else {
     double rf[8];
@@ -626,7 +630,8 @@ __global__ void __launch_bounds__(256) transfer_thread_kernel(TransferView T, in
         }
         acc += w[2][l2 * NC + c] * ab;
       }
-      out[__ldg(T.fmap + e * nf3 + l)] = acc;
+      double* d = out + __ldg(T.fmap + e * nf3 + l);
+      *d = T.add ? __dadd_rn(acc, *d) : acc;
     }
   } else {
     double rf[nf3];
@@ -836,31 +841,33 @@ static TransferView transfer_view(const fb_transfer* T) {
   return TransferView{restriction_map(T->fine), restriction_map(T->hmap), T->W.ptr, T->widx.ptr,
                       T->counts[0], T->counts[1], T->counts[2], T->origin[0], T->origin[1],
                       T->origin[2], T->nf, T->nc, T->periodic,
-                      {T->gcounts[0], T->gcounts[1], T->gcounts[2]}};
+                      {T->gcounts[0], T->gcounts[1], T->gcounts[2]}, 0};
 }
 
 }  // extern "C"
 
 template <bool PROLONG, int NF, int NC>
 static int launch_transfer_t(const fb_transfer* T, const double* in, double* out,
-                             cudaStream_t st) {
+                             cudaStream_t st, int add) {
   const dim3 grid(unsigned(ceil_div(T->ne, kTE))), block(32 * kTE);
+  TransferView V = transfer_view(T);
+  V.add = PROLONG ? add : 0;
   if constexpr (NF == 2 && NC == 2) {
-    transfer_q1_kernel<PROLONG><<<unsigned(ceil_div(T->ne, 256)), 256, 0, st>>>(transfer_view(T),
+    transfer_q1_kernel<PROLONG><<<unsigned(ceil_div(T->ne, 256)), 256, 0, st>>>(V,
                                                                                T->ne, in, out);
   } else if constexpr (NF == 3) {
     transfer_thread_kernel<PROLONG, NF, NC><<<unsigned(ceil_div(T->ne, 256)), 256, 0, st>>>(
-        transfer_view(T), T->ne, in, out);
+        V, T->ne, in, out);
   } else if constexpr (NF >= 4) {
     if (PROLONG)
-      transfer_prolong_sf_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
+      transfer_prolong_sf_kernel<NF, NC><<<grid, block, 0, st>>>(V, T->ne, in, out);
     else
-      transfer_restrict_sf_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
+      transfer_restrict_sf_kernel<NF, NC><<<grid, block, 0, st>>>(V, T->ne, in, out);
   } else {
     if (PROLONG)
-      transfer_prolong_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
+      transfer_prolong_kernel<NF, NC><<<grid, block, 0, st>>>(V, T->ne, in, out);
     else
-      transfer_restrict_kernel<NF, NC><<<grid, block, 0, st>>>(transfer_view(T), T->ne, in, out);
+      transfer_restrict_kernel<NF, NC><<<grid, block, 0, st>>>(V, T->ne, in, out);
   }
   FB_CHECK_LAUNCH();
   return FB_OK;
@@ -868,17 +875,18 @@ static int launch_transfer_t(const fb_transfer* T, const double* in, double* out
 
 // the degree ladder p -> ceil(p/2) (p = 2..8) and the Q1 h-coarsening levels
 template <bool PROLONG>
-static int launch_transfer(const fb_transfer* T, const double* in, double* out, cudaStream_t st) {
+static int launch_transfer(const fb_transfer* T, const double* in, double* out, cudaStream_t st,
+                           int add = 0) {
   switch (T->nf * 16 + T->nc) {
-    case 2 * 16 + 2: return launch_transfer_t<PROLONG, 2, 2>(T, in, out, st);
-    case 3 * 16 + 2: return launch_transfer_t<PROLONG, 3, 2>(T, in, out, st);
-    case 4 * 16 + 3: return launch_transfer_t<PROLONG, 4, 3>(T, in, out, st);
-    case 5 * 16 + 3: return launch_transfer_t<PROLONG, 5, 3>(T, in, out, st);
-    case 6 * 16 + 4: return launch_transfer_t<PROLONG, 6, 4>(T, in, out, st);
-    case 7 * 16 + 4: return launch_transfer_t<PROLONG, 7, 4>(T, in, out, st);
-    case 8 * 16 + 5: return launch_transfer_t<PROLONG, 8, 5>(T, in, out, st);
-    case 9 * 16 + 5: return launch_transfer_t<PROLONG, 9, 5>(T, in, out, st);
-    default: return launch_transfer_t<PROLONG, 0, 0>(T, in, out, st);
+    case 2 * 16 + 2: return launch_transfer_t<PROLONG, 2, 2>(T, in, out, st, add);
+    case 3 * 16 + 2: return launch_transfer_t<PROLONG, 3, 2>(T, in, out, st, add);
+    case 4 * 16 + 3: return launch_transfer_t<PROLONG, 4, 3>(T, in, out, st, add);
+    case 5 * 16 + 3: return launch_transfer_t<PROLONG, 5, 3>(T, in, out, st, add);
+    case 6 * 16 + 4: return launch_transfer_t<PROLONG, 6, 4>(T, in, out, st, add);
+    case 7 * 16 + 4: return launch_transfer_t<PROLONG, 7, 4>(T, in, out, st, add);
+    case 8 * 16 + 5: return launch_transfer_t<PROLONG, 8, 5>(T, in, out, st, add);
+    case 9 * 16 + 5: return launch_transfer_t<PROLONG, 9, 5>(T, in, out, st, add);
+    default: return launch_transfer_t<PROLONG, 0, 0>(T, in, out, st, add);
   }
 }
 
@@ -889,6 +897,14 @@ int fb_transfer_prolong(const fb_transfer* T, const double* xc, double* xf, void
   FB_REQUIRE(T != nullptr, "transfer is NULL");
   if (T->ne == 0) return FB_OK;
   return launch_transfer<true>(T, xc, xf, as_stream(stream));
+}
+
+// xf += P xc (the V-cycle's coarse-grid correction without a temporary and an
+// axpby pass; the same rounding as xf = 1 * (P xc) + 1 * xf)
+int fb_transfer_prolong_add(const fb_transfer* T, const double* xc, double* xf, void* stream) {
+  FB_REQUIRE(T != nullptr, "transfer is NULL");
+  if (T->ne == 0) return FB_OK;
+  return launch_transfer<true>(T, xc, xf, as_stream(stream), 1);
 }
 
 // xc (coarse L-vector) = P^T xf, deterministic (per-element contributions,

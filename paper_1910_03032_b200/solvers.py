@@ -265,11 +265,22 @@ class _CGGraph:
         _lib.check(_lib.lib.fb_while_graph_create(C.byref(g)))
         self.graph = g
         handle = _lib.lib.fb_while_graph_handle(g)
+        # no cyclic GC while capturing: a collected space / transfer / matrix
+        # frees device memory in its __del__, and a cudaFree inside the capture
+        # invalidates it (seen as an order-dependent "previous error during
+        # capture" once earlier tests left such cycles behind)
+        import gc
+        gc_was_enabled = gc.isenabled()
+        gc.disable()
         _lib.check(_lib.lib.fb_while_graph_begin(g, st))
         try:
             self._iteration(st, False, handle, 1)
         finally:
-            _lib.check(_lib.lib.fb_while_graph_end(g, st))
+            try:
+                _lib.check(_lib.lib.fb_while_graph_end(g, st))
+            finally:
+                if gc_was_enabled:
+                    gc.enable()
 
     def solve(self, bd, cfg, t0):
         cur = torch.cuda.current_stream()
@@ -983,8 +994,12 @@ class LORPreconditioner(_DeviceMixin):
         rc, xc = self._r[level + 1], self._x[level + 1]
         self._Pt[level].apply_into(t, rc, st)
         self._cycle(level + 1, rc, xc, st)
-        self._P[level].apply_into(xc, t, st)
-        vec.axpby(1.0, t, 1.0, x, st)
+        P = self._P[level]
+        if hasattr(P, "apply_add_into"):  # structured transfer: x += P xc in one pass
+            P.apply_add_into(xc, x, st)
+        else:
+            P.apply_into(xc, t, st)
+            vec.axpby(1.0, t, 1.0, x, st)
         A.residual_into(r, x, t, st)
         sm.backward_into(t, t2, st)
         vec.axpby(1.0, t2, 1.0, x, st)

@@ -419,6 +419,13 @@ class BoxTransfer:
                                                 dev.stream_handle() if stream is None else stream))
         return xf
 
+    def prolong_add_into(self, xc, xf, stream=None):
+        """xf += P xc in one pass (bitwise equal to prolong_into + axpby)."""
+        _lib.check(_lib.lib.fb_transfer_prolong_add(self.handle, xc.data_ptr(), xf.data_ptr(),
+                                                    dev.stream_handle() if stream is None
+                                                    else stream))
+        return xf
+
     def restrict_into(self, xf, xc, stream=None):
         _lib.check(_lib.lib.fb_transfer_restrict(self.handle, xf.data_ptr(), xc.data_ptr(),
                                                  dev.stream_handle() if stream is None else stream))
@@ -431,6 +438,9 @@ class _Prolong:
 
     def apply_into(self, x, y, stream=None):
         return self.T.prolong_into(x, y, stream)
+
+    def apply_add_into(self, x, y, stream=None):
+        return self.T.prolong_add_into(x, y, stream)
 
 
 class _Restrict:

@@ -142,6 +142,38 @@ def test_p_transfer_matches_nodal_interpolation(p):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("periodic", [False, True])
+def test_prolong_add_is_bitwise_prolong_plus_axpby(p, periodic):
+    """fb_transfer_prolong_add (the V-cycle's x += P xc) against prolong_into +
+    axpby, bitwise, for every transfer kernel: Q1 h-transfer (p = 1), thread
+    (nf = 3), sum-factorized (nf >= 4)."""
+    import torch
+    from paper_1910_03032_b200 import device as dev, geometry, structured as S, vec
+    counts = (6, 4, 8) if p > 1 else (12, 8, 10)
+    m = geometry.cartesian_mesh(counts, periodic=(True, False, True) if periodic else None)
+    cuda = torch.device("cuda")
+    fine = S.BoxSpace(m, p, block=2 if p > 1 else 4, device=cuda)
+    if p > 1:
+        pc = max(1, (p + 1) // 2)
+        coarse = S.BoxSpace(m, pc, block=2 if pc > 1 else 4, device=cuda)
+    else:
+        coarse = S.BoxSpace(S.coarsen_box(m), 1, block=4, device=cuda)
+    T = S.BoxTransfer(fine, coarse)
+    rng = np.random.default_rng(p)
+    xc = dev.to_device(rng.standard_normal(coarse.ndofs_scalar))
+    x0 = dev.to_device(rng.standard_normal(fine.ndofs_scalar))
+    t = torch.empty_like(x0)
+    T.prolong_into(xc, t)
+    want = x0.clone()
+    vec.axpby(1.0, t, 1.0, want)
+    got = x0.clone()
+    T.prolong_add_into(xc, got)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
+@pytest.mark.gpu
 def test_h_transfer_adjoint_and_linear_reproduction():
     import torch
     from paper_1910_03032_b200 import device as dev, geometry, structured as S
