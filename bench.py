@@ -815,15 +815,15 @@ def run_ours(args, rank, world):
     e2e_ms = ea.elapsed_time(eb) / e2e_steps
     ok = all(torch.equal(hy[i], pr["y"].cpu()) for i, pr in enumerate(probs))
 
-    # the same copies with the applies removed: the PCIe bound of the e2e figure
-    # on this box (hosts differ in link / NUMA placement from box to box)
+    # the same copies with the applies removed, H2D and D2H streams independent
+    # (full duplex): the PCIe bound of the e2e figure on this box (hosts differ
+    # in link / NUMA placement from box to box)
     def copy_step():
         for i, pr in enumerate(probs):
             with torch.cuda.stream(s_in):
                 pr["x"].copy_(hx[i], non_blocking=True)
                 done_in[i].record(s_in)
             with torch.cuda.stream(s_out):
-                s_out.wait_event(done_in[i])
                 hy[i].copy_(pr["y"], non_blocking=True)
 
     copy_step()
