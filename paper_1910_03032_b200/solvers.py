@@ -19,8 +19,10 @@ to the device once.  Any other ``.apply``/callable is treated as a host
 (numpy) function and called through a device<->host round trip.
 """
 
+import gc
 import math
 import os
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -207,6 +209,27 @@ GRAPH_MAX_N = 20_000_000
 TRUE_RESIDUAL_PERIOD = 50  # solvers.py:145-150
 
 
+
+_gc_lock = threading.Lock()
+_gc_state = {"depth": 0, "was_enabled": False}
+
+
+def _gc_pause(enter):
+    """Cyclic GC off while any thread captures a CUDA graph (in-process ranks
+    capture concurrently): a collected object's __del__ may cudaFree, which
+    invalidates a capture in progress."""
+    with _gc_lock:
+        if enter:
+            if _gc_state["depth"] == 0:
+                _gc_state["was_enabled"] = gc.isenabled()
+                gc.disable()
+            _gc_state["depth"] += 1
+        else:
+            _gc_state["depth"] -= 1
+            if _gc_state["depth"] == 0 and _gc_state["was_enabled"]:
+                gc.enable()
+
+
 class _CGGraph:
     """One captured PCG iteration for a fixed (A, precond, n): the body of a
     device-side while loop.  Vectors, scalars and dot partials are owned
@@ -269,9 +292,7 @@ class _CGGraph:
         # frees device memory in its __del__, and a cudaFree inside the capture
         # invalidates it (seen as an order-dependent "previous error during
         # capture" once earlier tests left such cycles behind)
-        import gc
-        gc_was_enabled = gc.isenabled()
-        gc.disable()
+        _gc_pause(True)
         _lib.check(_lib.lib.fb_while_graph_begin(g, st))
         try:
             self._iteration(st, False, handle, 1)
@@ -279,8 +300,7 @@ class _CGGraph:
             try:
                 _lib.check(_lib.lib.fb_while_graph_end(g, st))
             finally:
-                if gc_was_enabled:
-                    gc.enable()
+                _gc_pause(False)
 
     def solve(self, bd, cfg, t0):
         cur = torch.cuda.current_stream()

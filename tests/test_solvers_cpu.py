@@ -86,3 +86,39 @@ def test_oracle_cg_iterations_cfg1(gold):
     x, its, _ = krylov.cg(A, b, precond=vc, rel_tol=1e-8, max_iters=300)
     assert abs(its - c["iterations"][0]) <= 1
     assert rel_err(x, gold["cfg1_poisson/x0"]) < 1e-6
+
+
+def test_gc_pause_nests_across_threads():
+    """The CG-graph capture pauses cyclic GC; in-process ranks capture
+    concurrently, so the pause is reference counted and restores the
+    caller's setting only when the last capture ends."""
+    import gc
+    import threading
+    from paper_1910_03032_b200 import solvers as S
+    assert gc.isenabled()
+    barrier = threading.Barrier(3)
+    seen = []
+
+    def rank():
+        S._gc_pause(True)
+        barrier.wait()
+        seen.append(gc.isenabled())
+        barrier.wait()
+        S._gc_pause(False)
+
+    ts = [threading.Thread(target=rank) for _ in range(2)]
+    for t in ts:
+        t.start()
+    barrier.wait()
+    barrier.wait()
+    for t in ts:
+        t.join()
+    assert seen == [False, False]
+    assert gc.isenabled()
+    gc.disable()
+    try:
+        S._gc_pause(True)
+        S._gc_pause(False)
+        assert not gc.isenabled()  # a caller that had GC off keeps it off
+    finally:
+        gc.enable()
