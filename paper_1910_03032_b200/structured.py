@@ -554,8 +554,7 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
         for c in range(nv):
             self._Pt[0].apply_into(sl(t, c), rc, st)
             self._cycle(1, rc, xc, st)
-            self._P[0].apply_into(xc, sl(t, c), st)
-        vec.axpby(1.0, t[:m], 1.0, out[:m], st)
+            self._P[0].apply_add_into(xc, sl(out, c), st)  # out_c += P xc
         A.residual_multi_into(nv, stride, r, out, t, st)
         for c in range(nv):
             sm.backward_into(sl(t, c), sl(t2, c), st)
