@@ -526,8 +526,7 @@ class DistLORPreconditioner:
         self.hT.restrict_into(t, self._rh)
         self.comm.allreduce_sum(self._rh)
         self.coarse.apply_into(self._rh, self._xh)
-        self.hT.prolong_into(self._xh, t)
-        vec.axpby(1.0, t[:n], 1.0, x[:n])
+        self.hT.prolong_add_into(self._xh, x)  # owned x += P xc; ghosts refreshed below
         q1.ghost_update(self.comm, x)
         A.residual_into(r, x, t)
         sm.backward_into(t, t2)
@@ -577,8 +576,7 @@ class DistLORPreconditioner:
             cl.ghost_update(self.comm, xc, top1=False)
         else:
             self._coarse_solve(rc, xc)
-        T.prolong_into(xc, t)
-        vec.axpby(1.0, t[:n], 1.0, x[:n])
+        T.prolong_add_into(xc, x)  # owned x += P xc; ghosts refreshed below
         lv.ghost_update(self.comm, x)
         A.residual_into(r, x, t)
         sm.backward_into(t, t2)

@@ -321,8 +321,7 @@ class DistPeriodicLOR:
             cl.ghost_update(self.comm, xc)
         else:
             self._coarse_solve(rc, xc)
-        T.prolong_into(xc, t)
-        vec.axpby(1.0, t[:n], 1.0, x[:n])
+        T.prolong_add_into(xc, x)  # owned x += P xc; ghosts refreshed below
         lv.ghost_update(self.comm, x)
         A.residual_into(r, x, t)
         sm.backward_into(t, t2)
