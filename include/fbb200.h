@@ -247,6 +247,12 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r_dev, 
 /* Sweep the factor runs: 0 = CSR level loop, 1 = ELL, 2 = level-packed
  * TMA ring (fb_set_blockilu_packed). */
 int fb_blockilu_sweep_kind(const fb_blockilu* B);
+/* out += (LU)^-1 r (transpose 0) / (LU)^-T r (transpose 1): the V-cycle's
+ * smoothing correction x += M^-1 (b - A x) (reference solvers.py:382) added in
+ * the sweep's final store; level-packed sweeps only (sweep kind 2), else
+ * FB_ERR_ARG */
+int fb_blockilu_apply_add(const fb_blockilu* B, int transpose, const double* r_dev,
+                          double* out_dev, void* stream);
 /* y = M x for a dense row-major n x n matrix (coarse-level inverse). */
 int fb_dense_mv(int64_t n, const double* M_dev, const double* x_dev, double* y_dev, void* stream);
 /* LOR matrix of a degree-p space on its nodal sub-cell mesh (lor.py:61-99):

@@ -94,6 +94,7 @@ _SIGS = [
     ("fb_blockilu_create", _int, [_i64, _int, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)]),
     ("fb_blockilu_info", _int, [_vp, _vp, _vp, _vp, _vp]),
     ("fb_blockilu_sweep_kind", _int, [_vp]),
+    ("fb_blockilu_apply_add", _int, [_vp, _int, _vp, _vp, _vp]),
     ("fb_blockilu_destroy", None, [_vp]),
     ("fb_blockilu_apply", _int, [_vp, _int, _vp, _vp, _vp]),
     ("fb_dense_mv", _int, [_i64, _vp, _vp, _vp, _vp]),

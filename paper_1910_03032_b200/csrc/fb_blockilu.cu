@@ -1145,7 +1145,7 @@ template <int NSLOT, int NW>
 __global__ void __launch_bounds__(32 * NW) block_ilu_packed_kernel(
     const int* __restrict__ block_ptr, const int* __restrict__ new2old, PackView A, PackView Bv,
     const double* __restrict__ r, double* __restrict__ out, int slot_bytes, int KA, int KB,
-    int max_block, int max_grp) {
+    int max_block, int max_grp, int add) {
   extern __shared__ __align__(16) unsigned char psm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(psm);
   unsigned char* ring = psm + 128;
@@ -1166,7 +1166,10 @@ __global__ void __launch_bounds__(32 * NW) block_ilu_packed_kernel(
   packed_tri<NSLOT, NW>(A, b, y, bars, ring, slot_bytes, KA, soff, sR, sE, used);
   packed_tri<NSLOT, NW>(Bv, b, y, bars, ring, slot_bytes, KB, soff, sR, sE, used);
   pk_sync<NW>();
-  for (int i = lane; i < nb; i += 32 * NW) out[new2old ? new2old[bs + i] : bs + i] = y[i];
+  for (int i = lane; i < nb; i += 32 * NW) {
+    const int o = new2old ? new2old[bs + i] : bs + i;
+    out[o] = add ? __dadd_rn(y[i], out[o]) : y[i];  // add: out += M^-1 r (axpby rounding)
+  }
 }
 
 __global__ void pack_count_kernel(int64_t nlev, const int* __restrict__ grp,
@@ -1333,7 +1336,7 @@ static int build_packed(fb_blockilu* B) {
 
 template <int NSLOT, int NW>
 static int launch_packed_w(const fb_blockilu* B, const TriPart& a, bool ua, const TriPart& b,
-                           bool ub, const double* r, double* out, cudaStream_t st) {
+                           bool ub, const double* r, double* out, cudaStream_t st, int add) {
   const int sb = (std::max(a.max_group, b.max_group) + 15) / 16 * 16;
   const size_t smem = packed_smem(NSLOT, sb, B->max_block, B->max_grp);
   static size_t configured = 0;
@@ -1350,7 +1353,7 @@ static int launch_packed_w(const fb_blockilu* B, const TriPart& a, bool ua, cons
   const PackView pb{b.pk.ptr, b.loff.ptr, b.lne.ptr, b.grp.ptr, b.blk_grp.ptr, ub ? 0 : 1, s4, s2};
   block_ilu_packed_kernel<NSLOT, NW><<<B->nblocks, 32 * NW, smem, st>>>(
       B->block_ptr.ptr, B->new2old.ptr, pa, pb, r, out, sb, a.lev_group, b.lev_group,
-      B->max_block, B->max_grp);
+      B->max_block, B->max_grp, add);
   FB_CHECK_LAUNCH();
   return FB_OK;
 }
@@ -1358,12 +1361,12 @@ static int launch_packed_w(const fb_blockilu* B, const TriPart& a, bool ua, cons
 // warps per block: FB_BILU_NW=<1|2> (A/B runs), else by block size
 template <int NSLOT>
 static int launch_packed(const fb_blockilu* B, const TriPart& a, bool ua, const TriPart& b,
-                         bool ub, const double* r, double* out, cudaStream_t st) {
+                         bool ub, const double* r, double* out, cudaStream_t st, int add = 0) {
   static const int nw_env = getenv("FB_BILU_NW") ? atoi(getenv("FB_BILU_NW")) : 0;
   // by the typical block (first-touch boundary blocks are larger than interior ones)
   const int nw = nw_env > 0 ? nw_env : (B->n / std::max(B->nblocks, 1) > 1024 ? 2 : 1);
-  if (nw == 2) return launch_packed_w<NSLOT, 2>(B, a, ua, b, ub, r, out, st);
-  return launch_packed_w<NSLOT, 1>(B, a, ua, b, ub, r, out, st);
+  if (nw == 2) return launch_packed_w<NSLOT, 2>(B, a, ua, b, ub, r, out, st, add);
+  return launch_packed_w<NSLOT, 1>(B, a, ua, b, ub, r, out, st, add);
 }
 
 extern "C" {
@@ -1520,6 +1523,26 @@ int fb_blockilu_apply(const fb_blockilu* B, int transpose, const double* r, doub
     default:
       if (pipe && small_grid(B)) return launch_block_ilu<32, 2>(B, a, b, r, out, st);
       return pipe ? launch_block_ilu<32, true>(B, a, b, r, out, st) : launch_block_ilu<32, false>(B, a, b, r, out, st);
+  }
+}
+
+// out += (LU)^-1 r / (LU)^-T r, level-packed sweeps only (fb_blockilu_sweep_kind
+// == 2): the smoother's correction added in the sweep's final store, with the
+// rounding of a separate out = 1 * (M^-1 r) + 1 * out
+int fb_blockilu_apply_add(const fb_blockilu* B, int transpose, const double* r, double* out,
+                          void* stream) {
+  FB_REQUIRE(B != nullptr, "smoother is NULL");
+  FB_REQUIRE(r != out, "in-place smoother application is not supported");
+  FB_REQUIRE(B->nblocks == 0 || B->L.pk.ptr, "add mode needs the level-packed sweep");
+  if (B->nblocks == 0) return FB_OK;
+  const TriPart& pa = transpose ? B->Ut : B->L;
+  const TriPart& pb = transpose ? B->Lt : B->U;
+  const bool ua = !transpose, ub = transpose;
+  cudaStream_t st = as_stream(stream);
+  switch (pack_slots()) {
+    case 3: return launch_packed<3>(B, pa, ua, pb, ub, r, out, st, 1);
+    case 4: return launch_packed<4>(B, pa, ua, pb, ub, r, out, st, 1);
+    default: return launch_packed<2>(B, pa, ua, pb, ub, r, out, st, 1);
   }
 }
 

@@ -867,6 +867,22 @@ class BlockILU0Smoother:
     def backward_into(self, r, out, stream=None):
         return self._apply(r, out, True, stream)
 
+    @property
+    def adds_in_place(self):
+        """True when backward_add_into is available (level-packed sweeps)."""
+        if getattr(self, "_adds", None) is None:
+            self._adds = (self.jacobi is None and getattr(self, "handle", None) is not None
+                          and self._lib.lib.fb_blockilu_sweep_kind(self.handle) == 2)
+        return self._adds
+
+    def backward_add_into(self, r, out, stream=None):
+        """out += (LU)^-T r in the sweep's final store (bitwise backward_into
+        followed by axpby(1, t, 1, out))."""
+        self._lib.check(self._lib.lib.fb_blockilu_apply_add(
+            self.handle, 1, r.data_ptr(), out.data_ptr(),
+            dev.stream_handle() if stream is None else stream))
+        return out
+
     forward = ILU0Smoother.forward
     backward = ILU0Smoother.backward
 
@@ -1021,8 +1037,11 @@ class LORPreconditioner(_DeviceMixin):
             P.apply_into(xc, t, st)
             vec.axpby(1.0, t, 1.0, x, st)
         A.residual_into(r, x, t, st)
-        sm.backward_into(t, t2, st)
-        vec.axpby(1.0, t2, 1.0, x, st)
+        if getattr(sm, "adds_in_place", False):  # x += M^-T t in the sweep's store
+            sm.backward_add_into(t, x, st)
+        else:
+            sm.backward_into(t, t2, st)
+            vec.axpby(1.0, t2, 1.0, x, st)
 
     @property
     def graph_safe(self):

@@ -556,9 +556,13 @@ class BoxLORPreconditioner(solvers.LORPreconditioner):
             self._cycle(1, rc, xc, st)
             self._P[0].apply_add_into(xc, sl(out, c), st)  # out_c += P xc
         A.residual_multi_into(nv, stride, r, out, t, st)
-        for c in range(nv):
-            sm.backward_into(sl(t, c), sl(t2, c), st)
-        vec.axpby(1.0, t2[:m], 1.0, out[:m], st)
+        if getattr(sm, "adds_in_place", False):
+            for c in range(nv):
+                sm.backward_add_into(sl(t, c), sl(out, c), st)
+        else:
+            for c in range(nv):
+                sm.backward_into(sl(t, c), sl(t2, c), st)
+            vec.axpby(1.0, t2[:m], 1.0, out[:m], st)
         return out
 
     def clone_workspace(self):

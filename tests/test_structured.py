@@ -464,6 +464,17 @@ def test_packed_block_ilu_sweep_matches_csr_sweep(p, counts):
         again = getattr(sms[1], f)(r, torch.empty_like(r))
         assert torch.equal(got, again), f
         assert rel_err(got.cpu().numpy(), want.cpu().numpy()) < 1e-13, f
+    # the V-cycle's post-smoothing x += M^-T t in the sweep's store: bitwise
+    # the separate sweep + axpby; the CSR sweeps refuse the add mode
+    from paper_1910_03032_b200 import vec
+    assert sms[1].adds_in_place and not sms[0].adds_in_place
+    x0 = torch.from_numpy(np.random.default_rng(8).standard_normal(space.ndofs)).cuda()
+    want = x0.clone()
+    vec.axpby(1.0, sms[1].backward_into(r, torch.empty_like(r)), 1.0, want)
+    got = sms[1].backward_add_into(r, x0.clone())
+    assert torch.equal(got, want)
+    with pytest.raises(ValueError):
+        sms[0].backward_add_into(r, x0.clone())
 
 
 def test_periodic_coarsen_box():
