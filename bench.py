@@ -843,8 +843,9 @@ def run_ours(args, rank, world):
         e2e_ms = float(t.item())
 
     # the drop-in call a reference user makes: op.apply(numpy array) per degree
-    # (pageable host memory, synchronous H2D / apply / D2H; no pipelining)
-    xh = [h.numpy() for h in hx]
+    # (pageable input, synchronous H2D / apply / D2H into a pinned result; no
+    # pipelining)
+    xh = [h.numpy().copy() for h in hx]  # ordinary (pageable) user arrays
     for pr, xv in zip(probs, xh):
         pr["op"].apply(xv)
     torch.cuda.synchronize()
@@ -919,8 +920,10 @@ def run_ours(args, rank, world):
                                       "PCIe bound of this box"},
                 "numpy_api": {"value": round(world * dofs_step / (numpy_ms * 1e-3) / 1e9, 4),
                               "unit": "GDoF/s",
-                              "note": "HelmholtzOperator.apply(numpy) per degree: pageable, "
-                                      "synchronous copies, host wall clock, one sweep"}},
+                              "note": "HelmholtzOperator.apply(numpy) per degree on ordinary "
+                                      "(pageable) numpy inputs: synchronous H2D, result "
+                                      "returned in pinned host memory (device.to_host), "
+                                      "host wall clock, one sweep"}},
         "gpu_launches": int(launches),
         "clocks": clk,
         "warmup_steps_run": nw,
