@@ -843,8 +843,8 @@ def run_ours(args, rank, world):
         e2e_ms = float(t.item())
 
     # the drop-in call a reference user makes: op.apply(numpy array) per degree
-    # (pageable input, synchronous H2D / apply / D2H into a pinned result; no
-    # pipelining)
+    # (pageable input arrays; synchronous H2D / apply / D2H through cached pinned
+    # blocks; no pipelining)
     xh = [h.numpy().copy() for h in hx]  # ordinary (pageable) user arrays
     for pr, xv in zip(probs, xh):
         pr["op"].apply(xv)
@@ -921,9 +921,10 @@ def run_ours(args, rank, world):
                 "numpy_api": {"value": round(world * dofs_step / (numpy_ms * 1e-3) / 1e9, 4),
                               "unit": "GDoF/s",
                               "note": "HelmholtzOperator.apply(numpy) per degree on ordinary "
-                                      "(pageable) numpy inputs: synchronous H2D, result "
-                                      "returned in pinned host memory (device.to_host), "
-                                      "host wall clock, one sweep"}},
+                                      "(pageable) numpy inputs, synchronous; operand and "
+                                      "result cross through cached pinned host blocks "
+                                      "(device.to_device / to_host); host wall clock, one "
+                                      "sweep"}},
         "gpu_launches": int(launches),
         "clocks": clk,
         "warmup_steps_run": nw,

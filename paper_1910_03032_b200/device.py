@@ -10,6 +10,7 @@ import numpy as np
 import torch
 
 _DEVICE = None
+_PINNED_MIN_BYTES = 1 << 20  # host arrays from 1 MB up cross through pinned memory
 
 
 def device():
@@ -35,7 +36,15 @@ def to_device(x, dtype=torch.float64):
         t = x.to(device=device(), dtype=dtype)
         return t.contiguous()
     arr = np.ascontiguousarray(x, dtype=np.float64 if dtype == torch.float64 else None)
-    return torch.from_numpy(arr).to(device())
+    src = torch.from_numpy(arr)
+    if arr.nbytes >= _PINNED_MIN_BYTES:
+        # stage through page-locked memory from torch's caching host allocator:
+        # a threaded host copy, then an async H2D in stream order (the block
+        # is not reused before that copy completes)
+        h = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+        h.copy_(src)
+        return h.to(device(), non_blocking=True)
+    return src.to(device())
 
 
 def empty(n, dtype=torch.float64):
@@ -44,9 +53,6 @@ def empty(n, dtype=torch.float64):
 
 def zeros(n, dtype=torch.float64):
     return torch.zeros(n, dtype=dtype, device=device())
-
-
-_PINNED_MIN_BYTES = 1 << 20
 
 
 def to_host(t):

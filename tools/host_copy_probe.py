@@ -61,3 +61,6 @@ sys.path.insert(0, ".")
 from paper_1910_03032_b200 import device as dev  # noqa: E402
 print({"d2h_to_host_ms": t(lambda: dev.to_host(d)),
        "d2h_to_host_matches": bool(np.array_equal(dev.to_host(d), d.cpu().numpy()))})
+print({"h2d_to_device_ms": t(lambda: dev.to_device(x)),
+       "h2d_to_device_matches": bool(np.array_equal(dev.to_device(x).cpu().numpy(), x)),
+       "torch_threads": torch.get_num_threads()})
